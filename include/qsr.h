@@ -1,0 +1,219 @@
+/*
+ * qsr.h — C ABI of the B200-native stabilizer-tableau engine (libqsr.so).
+ *
+ * This is the drop-in boundary for the hot path named in BASELINE.json's north_star:
+ * the reference's single-shot simulate / measure / sample API of proj/include/quasar
+ * (arXiv 2603.14641, "QuaSARQ"). Every entry point below replaces one reference
+ * function; the citation after each declaration is the reference interface it stands
+ * for (paths relative to the reference's proj/include/quasar/).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch / CUDA types cross the boundary.
+ *  - Every function returns a qsr_status. On failure, qsr_last_error() returns a
+ *    thread-local message. The reference throws std::invalid_argument /
+ *    std::out_of_range / std::logic_error; the status codes map 1:1 onto those types
+ *    and the C++ shim (include/quasar_gpu.hpp) rethrows the same exception type.
+ *  - Validation happens on the host before any device state is mutated, as the
+ *    reference validates before mutating.
+ *  - Calls are synchronous (stream-synchronised before return) like the reference.
+ *  - Word type is fixed to uint64_t (the reference's default W).
+ *  - Host tableau buffers use the reference's storage layout exactly
+ *    (tableau.hpp:51-61): ColumnMajor word (q, j) at q*2k + j; RowMajor word
+ *    (i, col) at i*2*n_pad + col; signs 2k words. Device storage is private.
+ */
+#ifndef QSR_H_
+#define QSR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSR_ABI_VERSION 1
+
+typedef int qsr_status;
+enum {
+    QSR_OK = 0,
+    QSR_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+    QSR_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    QSR_LOGIC_ERROR = 3,      /* std::logic_error (odd phase = corrupted tableau) */
+    QSR_CUDA_ERROR = 4,
+    QSR_OUT_OF_MEMORY = 5,
+    QSR_NCCL_ERROR = 6,
+    QSR_INTERNAL = 7
+};
+
+/* GateKind, same numbering as circuit.hpp:29-42. */
+enum {
+    QSR_X = 0, QSR_Y, QSR_Z, QSR_H, QSR_S, QSR_SDG,
+    QSR_CX, QSR_CY, QSR_CZ, QSR_SWAP, QSR_ISWAP, QSR_MEASURE
+};
+enum { QSR_COLUMN_MAJOR = 0, QSR_ROW_MAJOR = 1 };   /* tableau.hpp:30 Layout */
+enum { QSR_SINGLE_SHOT = 0, QSR_SAMPLING = 1 };     /* schedule.hpp:37 ScheduleMode */
+
+/* Byte-compatible with quasar::Gate (circuit.hpp:85-99): 12 bytes, kind @0, q0 @4, q1 @8,
+ * so `circuit.gates.data()` can be passed without repacking. */
+typedef struct qsr_gate {
+    uint8_t kind;
+    uint32_t q0;
+    uint32_t q1;
+} qsr_gate;
+
+/* Byte-compatible with quasar::MeasurementRecord::Entry (measure.hpp:42-46). */
+typedef struct qsr_record_entry {
+    uint32_t qubit;
+    uint8_t outcome;
+    uint8_t deterministic;
+} qsr_record_entry;
+
+/* quasar::PhaseTimers (measure.hpp:87-100). Filled from CUDA events (device time). */
+typedef struct qsr_phase_timers {
+    double to_seconds;
+    double t_seconds;
+    double cmp_seconds;
+    double ge_seconds;
+} qsr_phase_timers;
+
+/* quasar::RunReport (simulator.hpp:27-34). */
+typedef struct qsr_run_report {
+    qsr_phase_timers timers;
+    uint64_t gate_count;
+    uint64_t measure_count;
+    uint64_t probabilistic_count;
+    uint64_t window_count;
+    double total_seconds;
+} qsr_run_report;
+
+/* ---- library ------------------------------------------------------------------- */
+const char *qsr_last_error(void);
+int qsr_abi_version(void);
+qsr_status qsr_device_count(int *count);
+/* Kernel launches issued by this library since load (bench `gpu_launches`). */
+uint64_t qsr_launch_count(void);
+/* Page-locked host buffers for fast tableau / record transfers (cudaHostAlloc). */
+qsr_status qsr_host_alloc(uint64_t bytes, void **out);
+void qsr_host_free(void *p);
+
+/* ---- Philox-4x32-10 (rng.hpp:28-55) -------------------------------------------- */
+void qsr_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint64_t qsr_philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t index);
+
+/* ---- circuits (circuit.hpp:101-173) -------------------------------------------- */
+typedef struct qsr_circuit qsr_circuit;
+/* Circuit{num_qubits, gates}; check_valid() is applied (circuit.hpp:108-115). */
+qsr_status qsr_circuit_create(uint32_t num_qubits, const qsr_gate *gates, uint64_t ngates,
+                              qsr_circuit **out);
+/* generate_random(n, depth, seed, measure_prob) (circuit.hpp:132-173). */
+qsr_status qsr_generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measure_prob,
+                               qsr_circuit **out);
+qsr_status qsr_circuit_info(const qsr_circuit *c, uint32_t *num_qubits, uint64_t *ngates,
+                            uint64_t *nmeasure);
+const qsr_gate *qsr_circuit_gates(const qsr_circuit *c);
+void qsr_circuit_destroy(qsr_circuit *c);
+
+/* ---- schedules (schedule.hpp:32-137) ------------------------------------------- */
+typedef struct qsr_schedule qsr_schedule;
+/* schedule_windows(circuit, mode) (schedule.hpp:51-137): identical output, O(G). */
+qsr_status qsr_schedule_windows(const qsr_circuit *c, int mode, qsr_schedule **out);
+/* A caller-built Schedule: windows are [offsets[w], offsets[w+1]) of `gates`. */
+qsr_status qsr_schedule_create(const qsr_gate *gates, const uint64_t *offsets,
+                               const uint8_t *is_measurement, uint64_t nwindows, int mode,
+                               qsr_schedule **out);
+qsr_status qsr_schedule_info(const qsr_schedule *s, uint64_t *nwindows, uint64_t *ngates,
+                             int *mode);
+const qsr_gate *qsr_schedule_gates(const qsr_schedule *s);
+const uint64_t *qsr_schedule_offsets(const qsr_schedule *s);      /* nwindows + 1 */
+const uint8_t *qsr_schedule_is_measurement(const qsr_schedule *s); /* nwindows */
+void qsr_schedule_destroy(qsr_schedule *s);
+
+/* ---- device tableau (tableau.hpp:62-131) --------------------------------------- */
+typedef struct qsr_tableau qsr_tableau;
+/* Tableau<uint64_t>(n): all-zero planes, ColumnMajor (tableau.hpp:67-72). */
+qsr_status qsr_tableau_create(uint64_t n, int device, qsr_tableau **out);
+/* Tableau::basis_state(initstate) / zero_state (tableau.hpp:120-131); NULL = |0...0>. */
+qsr_status qsr_tableau_basis_state(qsr_tableau *t, const uint8_t *initstate);
+qsr_status qsr_tableau_info(const qsr_tableau *t, uint64_t *n, uint64_t *k, uint64_t *n_pad,
+                            int *layout);
+/* Host buffers in the reference layout: x, z = n_pad*2k words, s = 2k words. */
+qsr_status qsr_tableau_upload(qsr_tableau *t, const uint64_t *x, const uint64_t *z,
+                              const uint64_t *s, int layout);
+qsr_status qsr_tableau_download(const qsr_tableau *t, uint64_t *x, uint64_t *z, uint64_t *s);
+qsr_status qsr_tableau_clone(const qsr_tableau *t, qsr_tableau **out);
+void qsr_tableau_destroy(qsr_tableau *t);
+
+/* Tableau::transpose_in_place (tableau.hpp:166-176). */
+qsr_status qsr_transpose_in_place(qsr_tableau *t);
+
+/* apply_window(tableau, window) (gates.hpp:147-197). */
+qsr_status qsr_apply_window(qsr_tableau *t, const qsr_gate *gates, uint64_t ngates);
+
+/* Measurement pipeline (measure.hpp:104-442); the tableau must be RowMajor for the
+ * first six, as in the reference. */
+qsr_status qsr_find_probabilistic(qsr_tableau *t, const qsr_gate *gates, uint64_t ngates,
+                                  int64_t *out);                      /* measure.hpp:104 */
+qsr_status qsr_find_and_compact_pivots(qsr_tableau *t, uint64_t q, int64_t *entries /* n */,
+                                       uint64_t *count);               /* measure.hpp:130 */
+qsr_status qsr_parallel_ge(qsr_tableau *t, const int64_t *entries, uint64_t count,
+                           uint64_t block_targets);                    /* measure.hpp:161 */
+qsr_status qsr_swap_anti_commuting(qsr_tableau *t, uint64_t p, uint64_t q); /* :279 */
+qsr_status qsr_inject_x(qsr_tableau *t, uint64_t p);                  /* measure.hpp:335 */
+qsr_status qsr_deterministic_outcome(qsr_tableau *t, uint64_t q, uint8_t *outcome); /* :343 */
+/* measure_window(t, window, RandomStream(seed, kStreamMeasure) at *coin_index, ...)
+ * (measure.hpp:381-442). *coin_index advances by the coins consumed; `out` receives
+ * ngates entries in window order. `timers` may be NULL. */
+qsr_status qsr_measure_window(qsr_tableau *t, const qsr_gate *gates, uint64_t ngates,
+                              uint64_t seed, uint64_t *coin_index, qsr_record_entry *out,
+                              qsr_phase_timers *timers);
+
+/* run_single_shot<uint64_t>(circuit, schedule, seed) (simulator.hpp:46-76).
+ * schedule == NULL -> schedule_windows(circuit, single_shot). `record` must hold
+ * measure_count entries. If out_tableau != NULL it receives the final tableau (device). */
+qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint64_t seed,
+                               int device, qsr_tableau **out_tableau, qsr_record_entry *record,
+                               qsr_run_report *report);
+
+/* ---- resident engine (bench / repeated runs; same algorithm as qsr_run_single_shot) */
+typedef struct qsr_engine qsr_engine;
+qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int device,
+                             qsr_engine **out);
+/* One full single-shot pass on device-resident inputs; *device_ms = CUDA-event time. */
+qsr_status qsr_engine_run(qsr_engine *e, uint64_t seed, double *device_ms);
+/* Per-kernel-class device time of the last run (ms) and launch counts. */
+qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate_launches,
+                            double *transpose_ms, double *measure_ms, uint64_t *launches);
+qsr_status qsr_engine_record(const qsr_engine *e, qsr_record_entry *record);
+qsr_status qsr_engine_tableau(const qsr_engine *e, uint64_t *x, uint64_t *z, uint64_t *s);
+void qsr_engine_destroy(qsr_engine *e);
+
+/* ---- Pauli frames (frames.hpp:32-204) ------------------------------------------ */
+typedef struct qsr_frames qsr_frames;
+/* init_frames<uint64_t>(n, shots, seed) (frames.hpp:46-72). */
+qsr_status qsr_init_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
+                           qsr_frames **out);
+qsr_status qsr_frames_info(const qsr_frames *f, uint64_t *n, uint64_t *shots, uint64_t *kf);
+/* Host buffers in the reference layout: word (q, j) at q*kf + j. */
+qsr_status qsr_frames_download(const qsr_frames *f, uint64_t *xf, uint64_t *zf);
+qsr_status qsr_frames_upload(qsr_frames *f, const uint64_t *xf, const uint64_t *zf);
+/* apply_window_frames (frames.hpp:76-94). */
+qsr_status qsr_apply_window_frames(qsr_frames *f, const qsr_gate *gates, uint64_t ngates,
+                                   int is_measurement);
+/* measure_sample(f, window, record, seed, epoch) (frames.hpp:111-158); the ShotRecord
+ * lives inside the frames object. */
+qsr_status qsr_measure_sample(qsr_frames *f, const qsr_gate *gates, uint64_t ngates,
+                              int is_measurement, uint64_t seed, uint32_t epoch);
+/* ShotRecord<uint64_t> (frames.hpp:97-107): measured (nrows) and words (nrows*kf).
+ * Pass NULL buffers to query *nrows. */
+qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *measured,
+                             uint64_t *words);
+void qsr_frames_destroy(qsr_frames *f);
+/* sample<uint64_t>(circuit, shots, seed, report) (frames.hpp:163-204); the result is the
+ * frames object's ShotRecord. */
+qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
+                      qsr_frames **out, qsr_run_report *report);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSR_H_ */

@@ -1,0 +1,1081 @@
+// C ABI of libqsr (include/qsr.h): object lifetimes, host-side validation, layout conversion
+// between the reference's host storage and the device layouts, and the single-shot /
+// sampling drivers (reference simulator.hpp:46-76, frames.hpp:163-204).
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <new>
+#include <string>
+#include <unordered_map>
+
+#include "device.hpp"
+
+using namespace qsr;
+
+struct qsr_circuit : Circuit {};
+struct qsr_schedule : Schedule {};
+
+namespace qsr {
+
+uint64_t g_launches = 0;
+
+void cuda_check(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    if (e == cudaErrorMemoryAllocation) fail(QSR_OUT_OF_MEMORY, m);
+    fail(QSR_CUDA_ERROR, m);
+}
+
+DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
+    if (n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
+    if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "Tableau: n exceeds the supported maximum");
+    QSR_CUDA(cudaSetDevice(device));
+    k = (n + 63) / 64;
+    n_pad = 64 * k;
+    cm_pitch = round_up(2 * k, 16);
+    rm_pitch = round_up(k, 16);
+    plane_words = std::max(n_pad * cm_pitch, 2 * n_pad * rm_pitch);
+    cudaDeviceProp prop;
+    QSR_CUDA(cudaGetDeviceProperties(&prop, device));
+    num_sms = prop.multiProcessorCount;
+    QSR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    auto alloc = [&](uint64_t **p, uint64_t words) {
+        QSR_CUDA(cudaMalloc(p, words * 8));
+        QSR_CUDA(cudaMemsetAsync(*p, 0, words * 8, stream));
+    };
+    alloc(&x, plane_words);
+    alloc(&z, plane_words);
+    alloc(&x2, plane_words);
+    alloc(&z2, plane_words);
+    alloc(&s, cm_pitch);
+    QSR_CUDA(cudaMalloc(&tile_counters, (cm_pitch / 64 + 2) * 4));
+    QSR_CUDA(cudaMemsetAsync(tile_counters, 0, (cm_pitch / 64 + 2) * 4, stream));
+    alloc(&ms.mask, 2 * k + 2);
+    QSR_CUDA(cudaMalloc(&ms.rows, 2 * n_pad * 4));
+    QSR_CUDA(cudaMalloc(&ms.ctl, 64));
+    QSR_CUDA(cudaMemsetAsync(ms.ctl, 0, 64, stream));
+    alloc(&ms.partial_x, 128 * rm_pitch);
+    alloc(&ms.partial_z, 128 * rm_pitch);
+    QSR_CUDA(cudaMalloc(&ms.partial_e, 128 * 8));
+    QSR_CUDA(cudaMemsetAsync(ms.partial_e, 0, 128 * 8, stream));
+    QSR_CUDA(cudaMalloc(&ms.coin_index, 8));
+    QSR_CUDA(cudaMemsetAsync(ms.coin_index, 0, 8, stream));
+    QSR_CUDA(cudaMalloc(&ms.err, 4));
+    QSR_CUDA(cudaMemsetAsync(ms.err, 0, 4, stream));
+    configure_measure_kernels(*this);
+    QSR_CUDA(cudaStreamSynchronize(stream));
+}
+
+DeviceTableau::~DeviceTableau() {
+    cudaSetDevice(device);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void *p : {(void *)x, (void *)z, (void *)x2, (void *)z2, (void *)s, (void *)sign_partials,
+                    (void *)tile_counters, (void *)gate_buf, (void *)ms.mask, (void *)ms.rows,
+                    (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
+                    (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
+                    (void *)ms.coin_index, (void *)ms.err})
+        if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+void DeviceTableau::ensure_gate_buf(uint64_t ng) {
+    if (ng <= gate_buf_cap) return;
+    if (gate_buf) QSR_CUDA(cudaFree(gate_buf));
+    gate_buf_cap = std::max<uint64_t>(ng, 1024);
+    QSR_CUDA(cudaMalloc(&gate_buf, gate_buf_cap * 8));
+}
+
+void DeviceTableau::ensure_window_cap(uint64_t m) {
+    if (m <= ms.window_cap) return;
+    if (ms.flags) QSR_CUDA(cudaFree(ms.flags));
+    if (ms.out) QSR_CUDA(cudaFree(ms.out));
+    if (ms.mqubits) QSR_CUDA(cudaFree(ms.mqubits));
+    ms.window_cap = std::max<uint64_t>(m, 64);
+    QSR_CUDA(cudaMalloc(&ms.flags, ms.window_cap));
+    QSR_CUDA(cudaMalloc(&ms.out, ms.window_cap * sizeof(qsr_record_entry)));
+    QSR_CUDA(cudaMalloc(&ms.mqubits, ms.window_cap * 4));
+}
+
+void DeviceTableau::sync() { QSR_CUDA(cudaStreamSynchronize(stream)); }
+
+} // namespace qsr
+
+struct qsr_tableau {
+    std::unique_ptr<DeviceTableau> t;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+qsr_status guard(F &&f) {
+    try {
+        f();
+        return QSR_OK;
+    } catch (const Error &e) {
+        g_err = e.what();
+        return e.status;
+    } catch (const std::bad_alloc &) {
+        g_err = "host allocation failed";
+        return QSR_OUT_OF_MEMORY;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return QSR_INTERNAL;
+    }
+}
+
+#define REQUIRE_PTR(p)                                                                      \
+    do {                                                                                    \
+        if (!(p)) fail(QSR_INVALID_ARGUMENT, #p " must not be NULL");                       \
+    } while (0)
+
+void check_cm(const DeviceTableau &t, const char *who) {
+    if (t.layout != QSR_COLUMN_MAJOR)
+        fail(QSR_INVALID_ARGUMENT, std::string(who) + ": tableau must be ColumnMajor");
+}
+void check_rm(const DeviceTableau &t, const char *who) {
+    if (t.layout != QSR_ROW_MAJOR)
+        fail(QSR_INVALID_ARGUMENT, std::string(who) + ": tableau must be RowMajor");
+}
+
+std::vector<uint64_t> pack(const qsr_gate *g, uint64_t n) {
+    std::vector<uint64_t> v(n);
+    for (uint64_t i = 0; i < n; ++i) v[i] = pack_gate(g[i]);
+    return v;
+}
+
+uint64_t host_bit(const std::vector<uint64_t> &s, uint64_t word, uint64_t bit) {
+    return (s[word] >> bit) & 1;
+}
+
+// Device-resident schedule: packed gates + per-window measured qubits.
+struct DeviceSchedule {
+    int device = 0;
+    uint64_t *d_gates = nullptr;
+    std::vector<uint64_t> offsets;
+    std::vector<uint8_t> is_meas;
+    std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
+    uint64_t measure_count = 0, unitary_count = 0;
+    ~DeviceSchedule() {
+        if (d_gates) { cudaSetDevice(device); cudaFree(d_gates); }
+    }
+};
+
+std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
+                                                cudaStream_t st) {
+    // Validate every window first (apply_window / measure_window checks, gates.hpp:149-165,
+    // measure.hpp:385-398) so no device state is touched by a schedule that would throw.
+    std::vector<uint32_t> stamp(n, 0);
+    const uint64_t W = s.num_windows();
+    for (uint64_t w = 0; w < W; ++w)
+        validate_window(n, s.gates.data() + s.offsets[w], s.offsets[w + 1] - s.offsets[w],
+                        s.is_meas[w] != 0, stamp, uint32_t(w + 1));
+    auto ds = std::make_unique<DeviceSchedule>();
+    ds->device = device;
+    ds->offsets = s.offsets;
+    ds->is_meas = s.is_meas;
+    ds->mqubits.resize(W);
+    for (uint64_t w = 0; w < W; ++w) {
+        if (!s.is_meas[w]) {
+            ds->unitary_count += s.offsets[w + 1] - s.offsets[w];
+            continue;
+        }
+        for (uint64_t i = s.offsets[w]; i < s.offsets[w + 1]; ++i)
+            ds->mqubits[w].push_back(s.gates[i].q0);
+        ds->measure_count += ds->mqubits[w].size();
+    }
+    const uint64_t G = s.gates.size();
+    QSR_CUDA(cudaSetDevice(device));
+    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
+    if (G) {
+        // Pack + upload in 32 Mi-gate slabs through pinned staging.
+        const uint64_t slab = uint64_t(1) << 25;
+        uint64_t *pinned = nullptr;
+        QSR_CUDA(cudaMallocHost(&pinned, std::min(G, slab) * 8 * 2));
+        uint64_t *buf[2] = {pinned, pinned + std::min(G, slab)};
+        int cur = 0;
+        for (uint64_t b = 0; b < G; b += slab, cur ^= 1) {
+            uint64_t e = std::min(G, b + slab);
+            QSR_CUDA(cudaStreamSynchronize(st)); // previous use of buf[cur] finished
+            for (uint64_t i = b; i < e; ++i) buf[cur][i - b] = pack_gate(s.gates[i]);
+            QSR_CUDA(cudaMemcpyAsync(ds->d_gates + b, buf[cur], (e - b) * 8,
+                                     cudaMemcpyHostToDevice, st));
+        }
+        QSR_CUDA(cudaStreamSynchronize(st));
+        QSR_CUDA(cudaFreeHost(pinned));
+    }
+    return ds;
+}
+
+struct RunTimes {
+    double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
+    uint64_t gate_windows = 0;
+};
+
+// The single-shot driver on device-resident inputs (simulator.hpp:46-70). `record` is a
+// device array of measure_count entries.
+void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
+                qsr_record_entry *d_record, RunTimes &rt) {
+    cudaEvent_t e_start, e_end, a, b;
+    QSR_CUDA(cudaEventCreate(&e_start));
+    QSR_CUDA(cudaEventCreate(&e_end));
+    QSR_CUDA(cudaEventCreate(&a));
+    QSR_CUDA(cudaEventCreate(&b));
+    QSR_CUDA(cudaEventRecord(e_start, t.stream));
+    launch_zero_state(t, nullptr);
+    QSR_CUDA(cudaMemsetAsync(t.ms.coin_index, 0, 8, t.stream));
+    const uint64_t W = ds.is_meas.size();
+    uint64_t rec_off = 0;
+    std::vector<uint8_t> flags;
+    uint64_t w = 0;
+    while (w < W) {
+        if (!ds.is_meas[w]) {
+            // A maximal run of unitary windows, bracketed by one event pair (TO bucket).
+            QSR_CUDA(cudaEventRecord(a, t.stream));
+            for (; w < W && !ds.is_meas[w]; ++w) {
+                launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+                ++rt.gate_windows;
+            }
+            QSR_CUDA(cudaEventRecord(b, t.stream));
+            QSR_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            QSR_CUDA(cudaEventElapsedTime(&ms, a, b));
+            rt.to_ms += ms;
+            continue;
+        }
+        const auto &mq = ds.mqubits[w];
+        const uint64_t m = mq.size();
+        t.ensure_window_cap(m);
+        QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
+        measure_window_device(t, m, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
+        QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, m * sizeof(qsr_record_entry),
+                                 cudaMemcpyDeviceToDevice, t.stream));
+        rec_off += m;
+        ++w;
+    }
+    QSR_CUDA(cudaEventRecord(e_end, t.stream));
+    QSR_CUDA(cudaEventSynchronize(e_end));
+    float total = 0;
+    QSR_CUDA(cudaEventElapsedTime(&total, e_start, e_end));
+    rt.total_ms = total;
+    for (auto e : {e_start, e_end, a, b}) cudaEventDestroy(e);
+    if (read_error_flag(t))
+        fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+}
+
+void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
+                 const std::vector<qsr_record_entry> &record, double total_s) {
+    if (!rep) return;
+    rep->timers.to_seconds = rt.to_ms * 1e-3;
+    rep->timers.t_seconds = rt.t_ms * 1e-3;
+    rep->timers.cmp_seconds = rt.cmp_ms * 1e-3;
+    rep->timers.ge_seconds = rt.ge_ms * 1e-3;
+    rep->gate_count = ds.unitary_count;
+    rep->measure_count = ds.measure_count;
+    rep->window_count = ds.is_meas.size();
+    rep->probabilistic_count = 0;
+    for (const auto &e : record) rep->probabilistic_count += e.deterministic ? 0 : 1;
+    rep->total_seconds = total_s;
+}
+
+// Host reference-layout <-> device layout conversion.
+void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout) {
+    if (layout == QSR_COLUMN_MAJOR) {
+        if (t.layout != QSR_COLUMN_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
+        QSR_CUDA(cudaMemcpy2DAsync(t.x, t.cm_pitch * 8, x, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
+                                   cudaMemcpyHostToDevice, t.stream));
+        QSR_CUDA(cudaMemcpy2DAsync(t.z, t.cm_pitch * 8, z, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
+                                   cudaMemcpyHostToDevice, t.stream));
+        t.layout = QSR_COLUMN_MAJOR;
+    } else {
+        if (t.layout != QSR_ROW_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
+        // Reference RM: word (i, col) at i*2n_pad + col  ->  internal row col, word i.
+        const uint64_t R = 2 * t.n_pad, K = t.k;
+        std::vector<uint64_t> tmp(R * K);
+        for (int plane = 0; plane < 2; ++plane) {
+            const uint64_t *src = plane ? z : x;
+            for (uint64_t i = 0; i < K; ++i)
+                for (uint64_t c = 0; c < R; ++c) tmp[c * K + i] = src[i * R + c];
+            QSR_CUDA(cudaMemcpy2DAsync(plane ? t.z : t.x, t.rm_pitch * 8, tmp.data(), K * 8, K * 8,
+                                       R, cudaMemcpyHostToDevice, t.stream));
+            QSR_CUDA(cudaStreamSynchronize(t.stream));
+        }
+        t.layout = QSR_ROW_MAJOR;
+    }
+}
+
+void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z) {
+    if (t.layout == QSR_COLUMN_MAJOR) {
+        if (x) QSR_CUDA(cudaMemcpy2DAsync(x, 2 * t.k * 8, t.x, t.cm_pitch * 8, 2 * t.k * 8, t.n_pad,
+                                          cudaMemcpyDeviceToHost, t.stream));
+        if (z) QSR_CUDA(cudaMemcpy2DAsync(z, 2 * t.k * 8, t.z, t.cm_pitch * 8, 2 * t.k * 8, t.n_pad,
+                                          cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        return;
+    }
+    const uint64_t R = 2 * t.n_pad, K = t.k;
+    std::vector<uint64_t> tmp(R * K);
+    for (int plane = 0; plane < 2; ++plane) {
+        uint64_t *dst = plane ? z : x;
+        if (!dst) continue;
+        QSR_CUDA(cudaMemcpy2DAsync(tmp.data(), K * 8, plane ? t.z : t.x, t.rm_pitch * 8, K * 8, R,
+                                   cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        for (uint64_t c = 0; c < R; ++c)
+            for (uint64_t i = 0; i < K; ++i) dst[i * R + c] = tmp[c * K + i];
+    }
+}
+
+std::vector<uint64_t> download_signs(DeviceTableau &t) {
+    std::vector<uint64_t> s(2 * t.k);
+    QSR_CUDA(cudaMemcpyAsync(s.data(), t.s, 2 * t.k * 8, cudaMemcpyDeviceToHost, t.stream));
+    t.sync();
+    return s;
+}
+
+// One RM word of the X plane (row r, qubit-word i).
+uint64_t rm_word_x(DeviceTableau &t, uint64_t r, uint64_t i) {
+    uint64_t v = 0;
+    QSR_CUDA(cudaMemcpyAsync(&v, t.x + r * t.rm_pitch + i, 8, cudaMemcpyDeviceToHost, t.stream));
+    t.sync();
+    return v;
+}
+
+} // namespace
+
+// ================================ C ABI ===============================================
+
+extern "C" {
+
+const char *qsr_last_error(void) { return g_err.c_str(); }
+int qsr_abi_version(void) { return QSR_ABI_VERSION; }
+uint64_t qsr_launch_count(void) { return g_launches; }
+
+qsr_status qsr_host_alloc(uint64_t bytes, void **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        QSR_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+    });
+}
+void qsr_host_free(void *p) {
+    if (p) cudaFreeHost(p);
+}
+
+qsr_status qsr_device_count(int *count) {
+    return guard([&] {
+        REQUIRE_PTR(count);
+        QSR_CUDA(cudaGetDeviceCount(count));
+    });
+}
+
+void qsr_philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    philox_block(ctr, key, out);
+}
+uint64_t qsr_philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t index) {
+    return philox_word(seed, stream, ctx, index);
+}
+
+// ---- circuits ---------------------------------------------------------------------
+qsr_status qsr_circuit_create(uint32_t num_qubits, const qsr_gate *gates, uint64_t ngates,
+                              qsr_circuit **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        if (ngates) REQUIRE_PTR(gates);
+        auto c = std::make_unique<qsr_circuit>();
+        c->num_qubits = num_qubits;
+        c->gates.assign(gates, gates + ngates);
+        c->check_valid();
+        *out = c.release();
+    });
+}
+
+qsr_status qsr_generate_random(uint32_t n, uint32_t depth, uint64_t seed, double p,
+                               qsr_circuit **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        auto c = std::make_unique<qsr_circuit>();
+        static_cast<Circuit &>(*c) = generate_random(n, depth, seed, p);
+        *out = c.release();
+    });
+}
+
+qsr_status qsr_circuit_info(const qsr_circuit *c, uint32_t *nq, uint64_t *ng, uint64_t *nm) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        if (nq) *nq = c->num_qubits;
+        if (ng) *ng = c->gates.size();
+        if (nm) *nm = c->measure_count();
+    });
+}
+const qsr_gate *qsr_circuit_gates(const qsr_circuit *c) { return c ? c->gates.data() : nullptr; }
+void qsr_circuit_destroy(qsr_circuit *c) { delete c; }
+
+// ---- schedules --------------------------------------------------------------------
+qsr_status qsr_schedule_windows(const qsr_circuit *c, int mode, qsr_schedule **out) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        REQUIRE_PTR(out);
+        auto s = std::make_unique<qsr_schedule>();
+        static_cast<Schedule &>(*s) = schedule_windows(*c, mode);
+        *out = s.release();
+    });
+}
+
+qsr_status qsr_schedule_create(const qsr_gate *gates, const uint64_t *offsets,
+                               const uint8_t *is_meas, uint64_t nwin, int mode,
+                               qsr_schedule **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        REQUIRE_PTR(offsets);
+        if (nwin) REQUIRE_PTR(is_meas);
+        auto s = std::make_unique<qsr_schedule>();
+        s->mode = mode;
+        s->offsets.assign(offsets, offsets + nwin + 1);
+        if (s->offsets[0] != 0) fail(QSR_INVALID_ARGUMENT, "schedule offsets must start at 0");
+        for (uint64_t w = 0; w < nwin; ++w)
+            if (s->offsets[w + 1] < s->offsets[w])
+                fail(QSR_INVALID_ARGUMENT, "schedule offsets must be non-decreasing");
+        s->is_meas.assign(is_meas, is_meas + nwin);
+        uint64_t G = s->offsets[nwin];
+        if (G) REQUIRE_PTR(gates);
+        s->gates.assign(gates, gates + G);
+        *out = s.release();
+    });
+}
+
+qsr_status qsr_schedule_info(const qsr_schedule *s, uint64_t *nwin, uint64_t *ng, int *mode) {
+    return guard([&] {
+        REQUIRE_PTR(s);
+        if (nwin) *nwin = s->num_windows();
+        if (ng) *ng = s->gates.size();
+        if (mode) *mode = s->mode;
+    });
+}
+const qsr_gate *qsr_schedule_gates(const qsr_schedule *s) { return s ? s->gates.data() : nullptr; }
+const uint64_t *qsr_schedule_offsets(const qsr_schedule *s) { return s ? s->offsets.data() : nullptr; }
+const uint8_t *qsr_schedule_is_measurement(const qsr_schedule *s) {
+    return s ? s->is_meas.data() : nullptr;
+}
+void qsr_schedule_destroy(qsr_schedule *s) { delete s; }
+
+// ---- tableau ----------------------------------------------------------------------
+qsr_status qsr_tableau_create(uint64_t n, int device, qsr_tableau **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        auto h = std::make_unique<qsr_tableau>();
+        h->t = std::make_unique<DeviceTableau>(n, device);
+        *out = h.release();
+    });
+}
+
+qsr_status qsr_tableau_basis_state(qsr_tableau *h, const uint8_t *init) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        if (t.layout != QSR_COLUMN_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
+        uint8_t *d_init = nullptr;
+        if (init) {
+            QSR_CUDA(cudaMalloc(&d_init, t.n));
+            QSR_CUDA(cudaMemcpyAsync(d_init, init, t.n, cudaMemcpyHostToDevice, t.stream));
+        }
+        launch_zero_state(t, d_init);
+        t.sync();
+        if (d_init) cudaFree(d_init);
+    });
+}
+
+qsr_status qsr_tableau_info(const qsr_tableau *h, uint64_t *n, uint64_t *k, uint64_t *n_pad,
+                            int *layout) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        if (n) *n = h->t->n;
+        if (k) *k = h->t->k;
+        if (n_pad) *n_pad = h->t->n_pad;
+        if (layout) *layout = h->t->layout;
+    });
+}
+
+qsr_status qsr_tableau_upload(qsr_tableau *h, const uint64_t *x, const uint64_t *z,
+                              const uint64_t *s, int layout) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(x); REQUIRE_PTR(z); REQUIRE_PTR(s);
+        if (layout != QSR_COLUMN_MAJOR && layout != QSR_ROW_MAJOR)
+            fail(QSR_INVALID_ARGUMENT, "unknown layout");
+        DeviceTableau &t = *h->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        upload_planes(t, x, z, layout);
+        QSR_CUDA(cudaMemcpyAsync(t.s, s, 2 * t.k * 8, cudaMemcpyHostToDevice, t.stream));
+        t.sync();
+    });
+}
+
+qsr_status qsr_tableau_download(const qsr_tableau *h, uint64_t *x, uint64_t *z, uint64_t *s) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        download_planes(t, x, z);
+        if (s) {
+            auto sv = download_signs(t);
+            std::memcpy(s, sv.data(), sv.size() * 8);
+        }
+    });
+}
+
+qsr_status qsr_tableau_clone(const qsr_tableau *h, qsr_tableau **out) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(out);
+        const DeviceTableau &t = *h->t;
+        auto c = std::make_unique<qsr_tableau>();
+        c->t = std::make_unique<DeviceTableau>(t.n, t.device);
+        DeviceTableau &d = *c->t;
+        QSR_CUDA(cudaMemcpyAsync(d.x, t.x, t.plane_words * 8, cudaMemcpyDeviceToDevice, d.stream));
+        QSR_CUDA(cudaMemcpyAsync(d.z, t.z, t.plane_words * 8, cudaMemcpyDeviceToDevice, d.stream));
+        QSR_CUDA(cudaMemcpyAsync(d.x2, t.x2, t.plane_words * 8, cudaMemcpyDeviceToDevice, d.stream));
+        QSR_CUDA(cudaMemcpyAsync(d.z2, t.z2, t.plane_words * 8, cudaMemcpyDeviceToDevice, d.stream));
+        QSR_CUDA(cudaMemcpyAsync(d.s, t.s, t.cm_pitch * 8, cudaMemcpyDeviceToDevice, d.stream));
+        d.layout = t.layout;
+        d.sync();
+        *out = c.release();
+    });
+}
+
+void qsr_tableau_destroy(qsr_tableau *h) { delete h; }
+
+qsr_status qsr_transpose_in_place(qsr_tableau *h) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        if (t.layout == QSR_COLUMN_MAJOR) transpose_to_rm(t);
+        else transpose_to_cm(t);
+        t.sync();
+    });
+}
+
+qsr_status qsr_apply_window(qsr_tableau *h, const qsr_gate *gates, uint64_t ng) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        if (ng) REQUIRE_PTR(gates);
+        DeviceTableau &t = *h->t;
+        check_cm(t, "apply_window");
+        std::vector<uint32_t> stamp;
+        validate_window(t.n, gates, ng, false, stamp, 1);
+        QSR_CUDA(cudaSetDevice(t.device));
+        auto packed = pack(gates, ng);
+        t.ensure_gate_buf(ng);
+        QSR_CUDA(cudaMemcpyAsync(t.gate_buf, packed.data(), ng * 8, cudaMemcpyHostToDevice, t.stream));
+        launch_gate_window(t, t.gate_buf, ng);
+        t.sync();
+    });
+}
+
+qsr_status qsr_find_probabilistic(qsr_tableau *h, const qsr_gate *gates, uint64_t ng, int64_t *out) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        if (ng) { REQUIRE_PTR(gates); REQUIRE_PTR(out); }
+        DeviceTableau &t = *h->t;
+        check_rm(t, "find_probabilistic");
+        std::vector<uint32_t> qs(ng);
+        for (uint64_t i = 0; i < ng; ++i) {
+            if (gates[i].q0 >= t.n) fail(QSR_OUT_OF_RANGE, "find_probabilistic: qubit out of range");
+            qs[i] = gates[i].q0;
+        }
+        QSR_CUDA(cudaSetDevice(t.device));
+        std::vector<int64_t> res;
+        rm_find_probabilistic(t, qs, res);
+        std::memcpy(out, res.data(), ng * 8);
+    });
+}
+
+qsr_status qsr_find_and_compact_pivots(qsr_tableau *h, uint64_t q, int64_t *entries,
+                                       uint64_t *count) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(entries); REQUIRE_PTR(count);
+        DeviceTableau &t = *h->t;
+        check_rm(t, "find_and_compact_pivots");
+        if (q >= t.n) fail(QSR_OUT_OF_RANGE, "find_and_compact_pivots: qubit out of range");
+        QSR_CUDA(cudaSetDevice(t.device));
+        std::vector<int64_t> e;
+        rm_find_pivots(t, q, e, *count);
+        std::memcpy(entries, e.data(), t.n * 8);
+    });
+}
+
+qsr_status qsr_parallel_ge(qsr_tableau *h, const int64_t *entries, uint64_t count,
+                           uint64_t block_targets) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        check_rm(t, "parallel_ge");
+        if (count == 0) fail(QSR_INVALID_ARGUMENT, "parallel_ge: empty pivot list");
+        if (block_targets < 1) fail(QSR_INVALID_ARGUMENT, "parallel_ge: block size must be >= 1");
+        REQUIRE_PTR(entries);
+        std::vector<int64_t> piv(entries, entries + count);
+        for (int64_t p : piv)
+            if (p < 0 || uint64_t(p) >= t.n) fail(QSR_OUT_OF_RANGE, "parallel_ge: pivot out of range");
+        QSR_CUDA(cudaSetDevice(t.device));
+        // The result is independent of block_targets by construction (the reference's
+        // three-pass scan reproduces the ordered sequential product for any block size).
+        rm_parallel_ge(t, piv);
+        t.sync();
+    });
+}
+
+qsr_status qsr_swap_anti_commuting(qsr_tableau *h, uint64_t p, uint64_t q) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        check_rm(t, "swap_anti_commuting");
+        if (p >= t.n || q >= t.n) fail(QSR_OUT_OF_RANGE, "swap_anti_commuting: index out of range");
+        QSR_CUDA(cudaSetDevice(t.device));
+        uint64_t w = rm_word_x(t, t.n_pad + p, q / 64);
+        if (!((w >> (q % 64)) & 1))
+            fail(QSR_INVALID_ARGUMENT, "swap_anti_commuting: stabilizer p commutes with Z_q");
+        rm_swap_anti_commuting(t, p, q);
+        if (read_error_flag(t))
+            fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+    });
+}
+
+qsr_status qsr_inject_x(qsr_tableau *h, uint64_t p) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        if (p >= t.n) fail(QSR_OUT_OF_RANGE, "inject_x: index out of range");
+        QSR_CUDA(cudaSetDevice(t.device));
+        flip_sign_bit(t, t.k + p / 64, p % 64);
+        t.sync();
+    });
+}
+
+qsr_status qsr_deterministic_outcome(qsr_tableau *h, uint64_t q, uint8_t *outcome) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(outcome);
+        DeviceTableau &t = *h->t;
+        check_rm(t, "deterministic_outcome");
+        if (q >= t.n) fail(QSR_OUT_OF_RANGE, "deterministic_outcome: qubit out of range");
+        QSR_CUDA(cudaSetDevice(t.device));
+        *outcome = rm_deterministic_outcome(t, q) ? 1 : 0;
+    });
+}
+
+qsr_status qsr_measure_window(qsr_tableau *h, const qsr_gate *gates, uint64_t ng, uint64_t seed,
+                              uint64_t *coin_index, qsr_record_entry *out,
+                              qsr_phase_timers *timers) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(coin_index);
+        if (ng) { REQUIRE_PTR(gates); REQUIRE_PTR(out); }
+        DeviceTableau &t = *h->t;
+        check_cm(t, "measure_window");
+        std::vector<uint32_t> stamp;
+        validate_window(t.n, gates, ng, true, stamp, 1);
+        QSR_CUDA(cudaSetDevice(t.device));
+        std::vector<uint32_t> qs(ng);
+        for (uint64_t i = 0; i < ng; ++i) qs[i] = gates[i].q0;
+        t.ensure_window_cap(ng);
+        QSR_CUDA(cudaMemcpyAsync(t.ms.coin_index, coin_index, 8, cudaMemcpyHostToDevice, t.stream));
+        if (ng)
+            QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, qs.data(), ng * 4, cudaMemcpyHostToDevice, t.stream));
+        std::vector<uint8_t> flags;
+        double t_ms = 0, ge_ms = 0, cmp_ms = 0;
+        measure_window_device(t, ng, seed, qs, flags, timers != nullptr, &t_ms, &ge_ms, &cmp_ms);
+        if (ng)
+            QSR_CUDA(cudaMemcpyAsync(out, t.ms.out, ng * sizeof(qsr_record_entry),
+                                     cudaMemcpyDeviceToHost, t.stream));
+        QSR_CUDA(cudaMemcpyAsync(coin_index, t.ms.coin_index, 8, cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        if (read_error_flag(t))
+            fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+        if (timers) {
+            timers->t_seconds += t_ms * 1e-3;
+            timers->ge_seconds += ge_ms * 1e-3;
+            timers->cmp_seconds += cmp_ms * 1e-3;
+        }
+    });
+}
+
+qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint64_t seed,
+                               int device, qsr_tableau **out_tableau, qsr_record_entry *record,
+                               qsr_run_report *report) {
+    return guard([&] {
+        auto wall0 = std::chrono::steady_clock::now();
+        REQUIRE_PTR(c);
+        Schedule own;
+        if (!s) own = schedule_windows(*c, QSR_SINGLE_SHOT);
+        const Schedule &sched = s ? static_cast<const Schedule &>(*s) : own;
+        const uint64_t nm = c->measure_count();
+        if (nm) REQUIRE_PTR(record);
+        auto h = std::make_unique<qsr_tableau>();
+        h->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
+        DeviceTableau &t = *h->t;
+        auto ds = upload_schedule(t.n, sched, device, t.stream);
+        if (ds->measure_count != nm)
+            fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
+        qsr_record_entry *d_rec = nullptr;
+        QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
+        RunTimes rt;
+        try {
+            run_device(t, *ds, seed, d_rec, rt);
+        } catch (...) {
+            cudaFree(d_rec);
+            throw;
+        }
+        std::vector<qsr_record_entry> host_rec(nm);
+        if (nm)
+            QSR_CUDA(cudaMemcpyAsync(host_rec.data(), d_rec, nm * sizeof(qsr_record_entry),
+                                     cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        cudaFree(d_rec);
+        if (nm) std::memcpy(record, host_rec.data(), nm * sizeof(qsr_record_entry));
+        double wall =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+        fill_report(report, rt, *ds, host_rec, wall);
+        if (out_tableau) *out_tableau = h.release();
+    });
+}
+
+// ---- resident engine --------------------------------------------------------------
+struct qsr_engine {
+    std::unique_ptr<DeviceTableau> t;
+    std::unique_ptr<DeviceSchedule> ds;
+    qsr_record_entry *d_rec = nullptr;
+    RunTimes last;
+    uint64_t launches = 0;
+    ~qsr_engine() {
+        if (d_rec) cudaFree(d_rec);
+    }
+};
+
+qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int device,
+                             qsr_engine **out) {
+    return guard([&] {
+        REQUIRE_PTR(c); REQUIRE_PTR(out);
+        Schedule own;
+        if (!s) own = schedule_windows(*c, QSR_SINGLE_SHOT);
+        const Schedule &sched = s ? static_cast<const Schedule &>(*s) : own;
+        auto e = std::make_unique<qsr_engine>();
+        e->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
+        e->ds = upload_schedule(e->t->n, sched, device, e->t->stream);
+        QSR_CUDA(cudaMalloc(&e->d_rec,
+                            std::max<uint64_t>(e->ds->measure_count, 1) * sizeof(qsr_record_entry)));
+        *out = e.release();
+    });
+}
+
+qsr_status qsr_engine_run(qsr_engine *e, uint64_t seed, double *device_ms) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        QSR_CUDA(cudaSetDevice(e->t->device));
+        uint64_t l0 = g_launches;
+        e->last = RunTimes{};
+        run_device(*e->t, *e->ds, seed, e->d_rec, e->last);
+        e->launches = g_launches - l0;
+        if (device_ms) *device_ms = e->last.total_ms;
+    });
+}
+
+qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate_launches,
+                            double *transpose_ms, double *measure_ms, uint64_t *launches) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        if (gate_ms) *gate_ms = e->last.to_ms;
+        if (gate_launches) *gate_launches = e->last.gate_windows;
+        if (transpose_ms) *transpose_ms = e->last.t_ms;
+        if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
+        if (launches) *launches = e->launches;
+    });
+}
+
+qsr_status qsr_engine_record(const qsr_engine *e, qsr_record_entry *record) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        uint64_t nm = e->ds->measure_count;
+        if (nm) {
+            REQUIRE_PTR(record);
+            QSR_CUDA(cudaMemcpyAsync(record, e->d_rec, nm * sizeof(qsr_record_entry),
+                                     cudaMemcpyDeviceToHost, e->t->stream));
+        }
+        e->t->sync();
+    });
+}
+
+qsr_status qsr_engine_tableau(const qsr_engine *e, uint64_t *x, uint64_t *z, uint64_t *s) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        DeviceTableau &t = *e->t;
+        download_planes(t, x, z);
+        if (s) {
+            auto sv = download_signs(t);
+            std::memcpy(s, sv.data(), sv.size() * 8);
+        }
+    });
+}
+
+void qsr_engine_destroy(qsr_engine *e) { delete e; }
+
+// ---- frames -----------------------------------------------------------------------
+struct qsr_frames {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int num_sms = 148;
+    uint64_t n = 0, shots = 0, kf = 0, pitch = 0;
+    uint64_t *xf = nullptr, *zf = nullptr;
+    uint64_t *rec = nullptr;  // record rows [cap][pitch]
+    uint64_t rec_cap = 0;
+    std::vector<uint32_t> measured;
+    std::vector<int64_t> row_of; // qubit -> record row
+    uint64_t *gate_buf = nullptr;
+    uint64_t gate_cap = 0;
+    uint32_t *d_idx = nullptr;   // qubits + rows staging
+    uint64_t idx_cap = 0;
+    ~qsr_frames() {
+        cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
+        for (void *p : {(void *)xf, (void *)zf, (void *)rec, (void *)gate_buf, (void *)d_idx})
+            if (p) cudaFree(p);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    void ensure_rows(uint64_t rows) {
+        if (rows <= rec_cap) return;
+        uint64_t cap = std::max<uint64_t>(rows, std::min<uint64_t>(n, std::max<uint64_t>(rec_cap * 2, 64)));
+        uint64_t *nr = nullptr;
+        QSR_CUDA(cudaMalloc(&nr, cap * pitch * 8));
+        QSR_CUDA(cudaMemsetAsync(nr, 0, cap * pitch * 8, stream));
+        if (rec) {
+            QSR_CUDA(cudaMemcpyAsync(nr, rec, rec_cap * pitch * 8, cudaMemcpyDeviceToDevice, stream));
+            QSR_CUDA(cudaStreamSynchronize(stream));
+            QSR_CUDA(cudaFree(rec));
+        }
+        rec = nr;
+        rec_cap = cap;
+    }
+    void ensure_idx(uint64_t m) {
+        if (m <= idx_cap) return;
+        if (d_idx) QSR_CUDA(cudaFree(d_idx));
+        idx_cap = std::max<uint64_t>(m, 64);
+        QSR_CUDA(cudaMalloc(&d_idx, idx_cap * 2 * 4));
+    }
+};
+
+namespace {
+
+std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device) {
+    if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
+    if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "init_frames: n exceeds the supported maximum");
+    auto f = std::make_unique<qsr_frames>();
+    f->device = device;
+    QSR_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    QSR_CUDA(cudaGetDeviceProperties(&prop, device));
+    f->num_sms = prop.multiProcessorCount;
+    QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    f->n = n;
+    f->shots = shots;
+    f->kf = (shots + 63) / 64;
+    f->pitch = round_up(f->kf, 16);
+    uint64_t words = std::max<uint64_t>(n, 1) * f->pitch;
+    QSR_CUDA(cudaMalloc(&f->xf, words * 8));
+    QSR_CUDA(cudaMalloc(&f->zf, words * 8));
+    QSR_CUDA(cudaMemsetAsync(f->xf, 0, words * 8, f->stream));
+    QSR_CUDA(cudaMemsetAsync(f->zf, 0, words * 8, f->stream));
+    f->row_of.assign(n, -1);
+    if (n) launch_frames_init(f->zf, n, f->kf, f->pitch, shots, seed, 0, nullptr, f->stream);
+    return f;
+}
+
+void frames_window(qsr_frames &f, const uint64_t *d_gates, uint64_t ng) {
+    launch_frame_window(f.xf, f.zf, f.pitch, d_gates, ng, f.num_sms, f.stream);
+}
+
+void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t seed,
+                    uint32_t epoch) {
+    std::vector<uint32_t> idx(2 * ng);
+    for (uint64_t i = 0; i < ng; ++i) {
+        uint32_t q = gates[i].q0;
+        if (f.row_of[q] < 0) {
+            f.row_of[q] = int64_t(f.measured.size());
+            f.measured.push_back(q);
+        }
+        idx[i] = q;
+        idx[ng + i] = uint32_t(f.row_of[q]);
+    }
+    f.ensure_rows(f.measured.size());
+    f.ensure_idx(ng);
+    QSR_CUDA(cudaMemcpyAsync(f.d_idx, idx.data(), 2 * ng * 4, cudaMemcpyHostToDevice, f.stream));
+    launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
+                          seed, epoch, f.stream);
+    QSR_CUDA(cudaStreamSynchronize(f.stream)); // idx staging reused next call
+}
+
+void validate_frames_window(const qsr_frames &f, const qsr_gate *gates, uint64_t ng, bool meas,
+                            const char *who) {
+    std::vector<uint32_t> stamp;
+    if (meas) {
+        stamp.assign(f.n, 0);
+        for (uint64_t i = 0; i < ng; ++i) {
+            if (gates[i].q0 >= f.n) fail(QSR_OUT_OF_RANGE, std::string(who) + ": qubit out of range");
+            if (stamp[gates[i].q0])
+                fail(QSR_INVALID_ARGUMENT, "measure_sample: qubit measured twice in window");
+            stamp[gates[i].q0] = 1;
+        }
+        return;
+    }
+    validate_window(f.n, gates, ng, false, stamp, 1);
+}
+
+} // namespace
+
+qsr_status qsr_init_frames(uint64_t n, uint64_t shots, uint64_t seed, int device, qsr_frames **out) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        auto f = make_frames(n, shots, seed, device);
+        QSR_CUDA(cudaStreamSynchronize(f->stream));
+        *out = f.release();
+    });
+}
+
+qsr_status qsr_frames_info(const qsr_frames *f, uint64_t *n, uint64_t *shots, uint64_t *kf) {
+    return guard([&] {
+        REQUIRE_PTR(f);
+        if (n) *n = f->n;
+        if (shots) *shots = f->shots;
+        if (kf) *kf = f->kf;
+    });
+}
+
+qsr_status qsr_frames_download(const qsr_frames *f, uint64_t *xf, uint64_t *zf) {
+    return guard([&] {
+        REQUIRE_PTR(f);
+        QSR_CUDA(cudaSetDevice(f->device));
+        if (f->n == 0) return;
+        if (xf) QSR_CUDA(cudaMemcpy2DAsync(xf, f->kf * 8, f->xf, f->pitch * 8, f->kf * 8, f->n,
+                                           cudaMemcpyDeviceToHost, f->stream));
+        if (zf) QSR_CUDA(cudaMemcpy2DAsync(zf, f->kf * 8, f->zf, f->pitch * 8, f->kf * 8, f->n,
+                                           cudaMemcpyDeviceToHost, f->stream));
+        QSR_CUDA(cudaStreamSynchronize(f->stream));
+    });
+}
+
+qsr_status qsr_frames_upload(qsr_frames *f, const uint64_t *xf, const uint64_t *zf) {
+    return guard([&] {
+        REQUIRE_PTR(f); REQUIRE_PTR(xf); REQUIRE_PTR(zf);
+        QSR_CUDA(cudaSetDevice(f->device));
+        if (f->n == 0) return;
+        QSR_CUDA(cudaMemcpy2DAsync(f->xf, f->pitch * 8, xf, f->kf * 8, f->kf * 8, f->n,
+                                   cudaMemcpyHostToDevice, f->stream));
+        QSR_CUDA(cudaMemcpy2DAsync(f->zf, f->pitch * 8, zf, f->kf * 8, f->kf * 8, f->n,
+                                   cudaMemcpyHostToDevice, f->stream));
+        QSR_CUDA(cudaStreamSynchronize(f->stream));
+    });
+}
+
+qsr_status qsr_apply_window_frames(qsr_frames *f, const qsr_gate *gates, uint64_t ng, int is_meas) {
+    return guard([&] {
+        REQUIRE_PTR(f);
+        if (ng) REQUIRE_PTR(gates);
+        if (is_meas) fail(QSR_INVALID_ARGUMENT, "apply_window_frames: measurement window");
+        validate_frames_window(*f, gates, ng, false, "apply_window_frames");
+        QSR_CUDA(cudaSetDevice(f->device));
+        if (ng > f->gate_cap) {
+            if (f->gate_buf) QSR_CUDA(cudaFree(f->gate_buf));
+            f->gate_cap = std::max<uint64_t>(ng, 1024);
+            QSR_CUDA(cudaMalloc(&f->gate_buf, f->gate_cap * 8));
+        }
+        auto packed = pack(gates, ng);
+        QSR_CUDA(cudaMemcpyAsync(f->gate_buf, packed.data(), ng * 8, cudaMemcpyHostToDevice, f->stream));
+        frames_window(*f, f->gate_buf, ng);
+        QSR_CUDA(cudaStreamSynchronize(f->stream));
+    });
+}
+
+qsr_status qsr_measure_sample(qsr_frames *f, const qsr_gate *gates, uint64_t ng, int is_meas,
+                              uint64_t seed, uint32_t epoch) {
+    return guard([&] {
+        REQUIRE_PTR(f);
+        if (ng) REQUIRE_PTR(gates);
+        if (!is_meas) fail(QSR_INVALID_ARGUMENT, "measure_sample: not a measurement window");
+        validate_frames_window(*f, gates, ng, true, "measure_sample");
+        QSR_CUDA(cudaSetDevice(f->device));
+        frames_measure(*f, gates, ng, seed, epoch);
+    });
+}
+
+qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *measured,
+                             uint64_t *words) {
+    return guard([&] {
+        REQUIRE_PTR(f); REQUIRE_PTR(nrows);
+        *nrows = f->measured.size();
+        if (measured) std::memcpy(measured, f->measured.data(), f->measured.size() * 4);
+        if (words && !f->measured.empty()) {
+            QSR_CUDA(cudaSetDevice(f->device));
+            QSR_CUDA(cudaMemcpy2DAsync(words, f->kf * 8, f->rec, f->pitch * 8, f->kf * 8,
+                                       f->measured.size(), cudaMemcpyDeviceToHost, f->stream));
+            QSR_CUDA(cudaStreamSynchronize(f->stream));
+        }
+    });
+}
+
+void qsr_frames_destroy(qsr_frames *f) { delete f; }
+
+qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
+                      qsr_frames **out, qsr_run_report *report) {
+    return guard([&] {
+        auto wall0 = std::chrono::steady_clock::now();
+        REQUIRE_PTR(c); REQUIRE_PTR(out);
+        Schedule sched = schedule_windows(*c, QSR_SAMPLING);
+        // Reference shot (frames.hpp:167): the full single-shot pipeline on the device.
+        DeviceTableau t(c->num_qubits, device);
+        auto ds = upload_schedule(t.n, sched, device, t.stream);
+        const uint64_t nm = ds->measure_count;
+        qsr_record_entry *d_rec = nullptr;
+        QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
+        RunTimes rt;
+        std::vector<qsr_record_entry> ref(nm);
+        try {
+            run_device(t, *ds, seed, d_rec, rt);
+            if (nm)
+                QSR_CUDA(cudaMemcpyAsync(ref.data(), d_rec, nm * sizeof(qsr_record_entry),
+                                         cudaMemcpyDeviceToHost, t.stream));
+            t.sync();
+        } catch (...) {
+            cudaFree(d_rec);
+            throw;
+        }
+        cudaFree(d_rec);
+        if (report) {
+            double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+            fill_report(report, rt, *ds, ref, wall);
+        }
+        // Frames over the same device-resident schedule (frames.hpp:171-181).
+        auto f = make_frames(c->num_qubits, shots, seed, device);
+        QSR_CUDA(cudaStreamSynchronize(t.stream));
+        uint32_t epoch = 1;
+        for (uint64_t w = 0; w < ds->is_meas.size(); ++w) {
+            const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
+            if (ds->is_meas[w]) frames_measure(*f, sched.gates.data() + b, e - b, seed, epoch++);
+            else frames_window(*f, ds->d_gates + b, e - b);
+        }
+        // Fold in the reference outcomes: per_qubit() = last outcome per qubit
+        // (measure.hpp:50-64, frames.hpp:183-202).
+        std::vector<int8_t> last(c->num_qubits, -1);
+        for (const auto &e : ref) last[e.qubit] = int8_t(e.outcome ? 1 : 0);
+        std::vector<uint32_t> flip_rows;
+        for (uint64_t r = 0; r < f->measured.size(); ++r)
+            if (last[f->measured[r]] == 1) flip_rows.push_back(uint32_t(r));
+        if (!flip_rows.empty()) {
+            f->ensure_idx(flip_rows.size());
+            QSR_CUDA(cudaMemcpyAsync(f->d_idx, flip_rows.data(), flip_rows.size() * 4,
+                                     cudaMemcpyHostToDevice, f->stream));
+            launch_record_fold(f->rec, f->pitch, f->kf, f->shots, f->d_idx, flip_rows.size(),
+                               f->stream);
+        }
+        QSR_CUDA(cudaStreamSynchronize(f->stream));
+        *out = f.release();
+    });
+}
+
+} // extern "C"

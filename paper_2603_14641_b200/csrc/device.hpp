@@ -1,0 +1,115 @@
+// Device object model and kernel launchers of libqsr (sm_100a).
+//
+// HBM layout:
+//   CM plane  : word (q, j) at q*cm_pitch + j, q in [0, n_pad), j in [0, 2k); cm_pitch =
+//               round_up(2k, 16) so every qubit row starts on a 128-byte line.
+//   RM plane  : generator-major; row r = j*64 + b (r < n_pad destabilizer g = r, else
+//               stabilizer g = r - n_pad), word i = qubit-word; at r*rm_pitch + i,
+//               rm_pitch = round_up(k, 16). A generator's k words are contiguous, so the
+//               measurement row products stream exactly the bytes they need.
+//   signs     : 2k words (+ padding to cm_pitch), generator-indexed in both layouts.
+// The reference's RowMajor (i-major, tableau.hpp:91-94) is produced only when a caller
+// downloads a transposed tableau through the API-parity path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "host.hpp"
+
+namespace qsr {
+
+void cuda_check(cudaError_t e, const char *what);
+#define QSR_CUDA(call) ::qsr::cuda_check((call), #call)
+
+extern uint64_t g_launches; // kernel launches issued by the library
+inline void count_launch(uint64_t n = 1) { g_launches += n; }
+
+inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
+
+// Scratch used by the measurement pipeline; sized for one tableau.
+struct MeasureScratch {
+    uint64_t *mask = nullptr;       // 2k mask words (column bits of all rows)
+    uint32_t *rows = nullptr;       // compacted row list (<= 2*n_pad)
+    uint32_t *ctl = nullptr;        // control block (see k_measure.cu)
+    uint64_t *partial_x = nullptr;  // deterministic-product partials [kDetChunks][rm_pitch]
+    uint64_t *partial_z = nullptr;
+    int64_t *partial_e = nullptr;   // [kDetChunks]
+    uint8_t *flags = nullptr;       // per-measurement flags of the current window
+    qsr_record_entry *out = nullptr;// per-window outcomes
+    uint32_t *mqubits = nullptr;    // per-window measured qubits
+    uint64_t *coin_index = nullptr; // device coin counter
+    int *err = nullptr;             // odd-phase detector
+    uint64_t window_cap = 0;
+};
+
+struct DeviceTableau {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    uint64_t n = 0, k = 0, n_pad = 0;
+    uint64_t cm_pitch = 0, rm_pitch = 0;
+    uint64_t plane_words = 0;        // max(n_pad*cm_pitch, 2*n_pad*rm_pitch)
+    uint64_t *x = nullptr, *z = nullptr;   // current planes
+    uint64_t *x2 = nullptr, *z2 = nullptr; // transpose targets
+    uint64_t *s = nullptr;                 // signs (cm_pitch words)
+    int layout = QSR_COLUMN_MAJOR;
+    // gate-window sign partials
+    uint64_t *sign_partials = nullptr;
+    uint64_t sign_partial_chunks = 0;
+    uint32_t *tile_counters = nullptr;
+    uint64_t *gate_buf = nullptr;          // staging for single-window API calls
+    uint64_t gate_buf_cap = 0;
+    MeasureScratch ms;
+    int num_sms = 148;
+
+    DeviceTableau(uint64_t n, int device);
+    ~DeviceTableau();
+    void ensure_gate_buf(uint64_t ngates);
+    void ensure_window_cap(uint64_t m);
+    void sync();
+};
+
+// ---- launchers --------------------------------------------------------------------
+// Gate window on a CM tableau: `gates` is a device array of packed gate words.
+void launch_gate_window(DeviceTableau &t, const uint64_t *gates, uint64_t ngates);
+// Frames: same rules, no signs.
+void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *gates,
+                         uint64_t ngates, int num_sms, cudaStream_t st);
+// CM <-> internal RM transposes (swap t.x/t.x2 etc).
+void transpose_to_rm(DeviceTableau &t);
+void transpose_to_cm(DeviceTableau &t);
+void launch_zero_state(DeviceTableau &t, const uint8_t *d_init /* nullable */);
+
+// Measurement window on a CM tableau (fused recipe, measure.hpp:381-442 semantics).
+// `mq` = device array of measured qubits (m entries) already uploaded to t.ms.mqubits.
+struct MeasureTimes { cudaEvent_t t0, t1, t2, t3; };
+void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
+                           const std::vector<uint32_t> &qubits, std::vector<uint8_t> &flags_host,
+                           bool timed, double *t_ms, double *ge_ms, double *cmp_ms);
+
+void configure_measure_kernels(DeviceTableau &t);
+// API-parity kernels on an RM tableau.
+void rm_column_mask(DeviceTableau &t, uint64_t q);          // fills t.ms.mask
+void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries, uint64_t &count);
+void rm_parallel_ge(DeviceTableau &t, const std::vector<int64_t> &pivots);
+void rm_swap_anti_commuting(DeviceTableau &t, uint64_t p, uint64_t q);
+bool rm_deterministic_outcome(DeviceTableau &t, uint64_t q);
+void rm_find_probabilistic(DeviceTableau &t, const std::vector<uint32_t> &qubits,
+                           std::vector<int64_t> &out);
+void flip_sign_bit(DeviceTableau &t, uint64_t word, uint64_t bit);
+int read_error_flag(DeviceTableau &t); // syncs; returns and clears
+
+// Frames kernels.
+void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t pitch, uint64_t shots,
+                        uint64_t seed, uint32_t epoch, const uint32_t *qubits /*nullable*/,
+                        cudaStream_t st);
+void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf,
+                           uint64_t shots, uint64_t *rec, const uint32_t *qubits,
+                           const uint32_t *rows, uint64_t m, uint64_t seed, uint32_t epoch,
+                           cudaStream_t st);
+void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t shots,
+                        const uint32_t *flip_rows, uint64_t nflip, cudaStream_t st);
+
+} // namespace qsr

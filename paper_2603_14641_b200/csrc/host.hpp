@@ -1,0 +1,65 @@
+// Host-side runtime of libqsr: circuits, the O(G) window scheduler, error plumbing and
+// the device object model. Kernel launchers are declared in device.hpp.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qsr.h"
+
+namespace qsr {
+
+// Error carrying a qsr_status; thrown inside the library, converted at the C boundary.
+struct Error : std::runtime_error {
+    qsr_status status;
+    Error(qsr_status s, const std::string &m) : std::runtime_error(m), status(s) {}
+};
+[[noreturn]] inline void fail(qsr_status s, const std::string &m) { throw Error(s, m); }
+
+inline int gate_arity(uint8_t kind) {
+    return (kind == QSR_CX || kind == QSR_CY || kind == QSR_CZ || kind == QSR_SWAP ||
+            kind == QSR_ISWAP)
+               ? 2
+               : 1;
+}
+
+// Packed device gate word: bits [0,28) q0, [28,32) kind, [32,64) q1. 8 bytes per gate so
+// a whole c5 schedule (124 M gates) is ~1 GB of HBM, read by every gate-window CTA.
+inline uint64_t pack_gate(const qsr_gate &g) {
+    return uint64_t(g.q0 & 0x0FFFFFFFu) | (uint64_t(g.kind & 0xF) << 28) | (uint64_t(g.q1) << 32);
+}
+constexpr uint64_t kMaxQubits = (uint64_t(1) << 28) - 1;
+
+// Philox-4x32-10 (reference rng.hpp:28-55), host side.
+void philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+uint64_t philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t index);
+
+struct Circuit {
+    uint32_t num_qubits = 0;
+    std::vector<qsr_gate> gates;
+    uint64_t measure_count() const;
+    void check_valid() const; // circuit.hpp:108-115
+};
+
+// generate_random (circuit.hpp:132-173): same Philox stream, same draw order.
+Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measure_prob);
+
+struct Schedule {
+    int mode = QSR_SINGLE_SHOT;
+    std::vector<qsr_gate> gates;     // flattened, schedule order
+    std::vector<uint64_t> offsets;   // nwindows + 1
+    std::vector<uint8_t> is_meas;    // nwindows
+    uint64_t num_windows() const { return is_meas.size(); }
+};
+
+// schedule_windows (schedule.hpp:51-137) via the one-pass round closed form.
+Schedule schedule_windows(const Circuit &c, int mode);
+
+// Validates a schedule window by window exactly as apply_window / measure_window do
+// (gates.hpp:149-165, measure.hpp:385-398), before anything touches the device.
+void validate_window(uint64_t n, const qsr_gate *gates, uint64_t ngates, bool is_measurement,
+                     std::vector<uint32_t> &stamp, uint32_t stamp_id);
+
+} // namespace qsr
