@@ -82,8 +82,8 @@ constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTileWords = 64;
 
-template <bool kSigns, int U>
-__global__ void __launch_bounds__(kThreads)
+template <bool kSigns, int U, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
 k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
               const uint64_t *__restrict__ gates, uint32_t ngates, uint32_t chunk,
               uint64_t *__restrict__ partials, uint32_t *__restrict__ counters,
@@ -197,35 +197,45 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
     }
 }
 
-struct Occ {
-    int sign_blocks = 0, frame_blocks = 0;
-};
-Occ &occ_cache() {
-    static Occ o;
-    return o;
+// Kernel variants (unroll U, min resident CTAs): 0 = <2,3>, 1 = <1,4>, 2 = <2,4>.
+// QSR_GATE_VARIANT selects one for tuning runs; the default is the measured best
+// (profiles/r01_gate_tune.log: <2,3> 6.37 TB/s at c5, <1,4> 6.31, <2,4> 6.07 with spills).
+int gate_variant() {
+    static int v = [] {
+        const char *e = getenv("QSR_GATE_VARIANT");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
 }
 
-template <bool kSigns>
-void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uint64_t ngates,
-            int num_sms, cudaStream_t st, uint64_t **partials, uint64_t *partial_chunks,
-            uint32_t *counters, uint64_t *s) {
-    if (ngates == 0)
-        return;
-    constexpr int U = 2;
-    int &bps = kSigns ? occ_cache().sign_blocks : occ_cache().frame_blocks;
+template <bool kSigns, int U, int B>
+void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates,
+                    uint64_t ngates, int num_sms, cudaStream_t st, uint64_t **partials,
+                    uint64_t *partial_chunks, uint32_t *counters, uint64_t *s) {
+    static int bps = 0;
     if (bps == 0) {
         QSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &bps, k_gate_window<kSigns, U>, kThreads, 0));
+            &bps, k_gate_window<kSigns, U, B>, kThreads, 0));
         if (bps < 1)
             bps = 1;
     }
     const uint64_t tiles = (pitch + kTileWords - 1) / kTileWords;
-    const uint64_t target = uint64_t(num_sms) * uint64_t(bps);
-    // At least 8 gates per warp per chunk so the XOR tree and fold stay negligible.
-    uint64_t max_chunks = (ngates + kWarps * 8 - 1) / (kWarps * 8);
-    uint64_t chunks = (target + tiles - 1) / tiles;
-    if (chunks > max_chunks) chunks = max_chunks;
-    if (chunks < 1) chunks = 1;
+    const uint64_t slots = uint64_t(num_sms) * uint64_t(bps);
+    // Every CTA does the same work, so the grid should be a whole number of waves: pick the
+    // chunk count (>= ~4 waves when the window is big enough) whose tiles x chunks leaves the
+    // smallest partial last wave. At least 16 gates per warp per chunk keep the XOR tree and
+    // the tile fold negligible.
+    const uint64_t max_chunks = std::max<uint64_t>(1, ngates / (kWarps * 16));
+    uint64_t c_min = std::max<uint64_t>(1, (4 * slots + tiles - 1) / tiles);
+    if (c_min > max_chunks) c_min = max_chunks;
+    uint64_t chunks = c_min;
+    double best = 1e30;
+    for (uint64_t c = c_min; c <= std::min<uint64_t>(max_chunks, 4 * c_min); ++c) {
+        const uint64_t ctas = tiles * c;
+        const uint64_t waves = (ctas + slots - 1) / slots;
+        const double eff_time = double(waves) / double(c); // per-CTA work ~ 1/c
+        if (eff_time < best * 0.999) { best = eff_time; chunks = c; }
+    }
     if (chunks > 65535) chunks = 65535;
     uint64_t chunk = (ngates + chunks - 1) / chunks;
     chunks = (ngates + chunk - 1) / chunk;
@@ -236,11 +246,33 @@ void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uin
         *partial_chunks = chunks;
     }
     dim3 grid{unsigned(tiles), unsigned(chunks)};
-    k_gate_window<kSigns, U><<<grid, kThreads, 0, st>>>(
+    k_gate_window<kSigns, U, B><<<grid, kThreads, 0, st>>>(
         x, z, pitch, gates, uint32_t(ngates), uint32_t(chunk), kSigns ? *partials : nullptr,
         counters, s);
     QSR_CUDA(cudaGetLastError());
     count_launch();
+}
+
+template <bool kSigns>
+void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uint64_t ngates,
+            int num_sms, cudaStream_t st, uint64_t **partials, uint64_t *partial_chunks,
+            uint32_t *counters, uint64_t *s) {
+    if (ngates == 0)
+        return;
+    switch (gate_variant()) {
+    case 0:
+        launch_variant<kSigns, 2, 3>(x, z, pitch, gates, ngates, num_sms, st, partials,
+                                     partial_chunks, counters, s);
+        break;
+    case 2:
+        launch_variant<kSigns, 2, 4>(x, z, pitch, gates, ngates, num_sms, st, partials,
+                                     partial_chunks, counters, s);
+        break;
+    default:
+        launch_variant<kSigns, 1, 4>(x, z, pitch, gates, ngates, num_sms, st, partials,
+                                     partial_chunks, counters, s);
+        break;
+    }
 }
 
 } // namespace
