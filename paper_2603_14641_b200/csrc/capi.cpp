@@ -63,6 +63,11 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
     QSR_CUDA(cudaMemsetAsync(ms.coin_index, 0, 8, stream));
     QSR_CUDA(cudaMalloc(&ms.err, 4));
     QSR_CUDA(cudaMemsetAsync(ms.err, 0, 4, stream));
+    QSR_CUDA(cudaMalloc(&ms.colbits, 2 * n_pad * 4));
+    alloc(&ms.Vx, uint64_t(kMaxBatch) * rm_pitch);
+    alloc(&ms.Vz, uint64_t(kMaxBatch) * rm_pitch);
+    QSR_CUDA(cudaMalloc(&ms.vinfo, 3 * kMaxBatch * 4));
+    QSR_CUDA(cudaMalloc(&ms.bctl, 16));
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
 }
@@ -74,7 +79,9 @@ DeviceTableau::~DeviceTableau() {
                     (void *)tile_counters, (void *)gate_buf, (void *)ms.mask, (void *)ms.rows,
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
-                    (void *)ms.coin_index, (void *)ms.err})
+                    (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits, (void *)ms.Vx,
+                    (void *)ms.Vz, (void *)ms.vinfo, (void *)ms.bctl, (void *)ms.fq,
+                    (void *)ms.fidx})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -91,10 +98,14 @@ void DeviceTableau::ensure_window_cap(uint64_t m) {
     if (ms.flags) QSR_CUDA(cudaFree(ms.flags));
     if (ms.out) QSR_CUDA(cudaFree(ms.out));
     if (ms.mqubits) QSR_CUDA(cudaFree(ms.mqubits));
+    if (ms.fq) QSR_CUDA(cudaFree(ms.fq));
+    if (ms.fidx) QSR_CUDA(cudaFree(ms.fidx));
     ms.window_cap = std::max<uint64_t>(m, 64);
     QSR_CUDA(cudaMalloc(&ms.flags, ms.window_cap));
     QSR_CUDA(cudaMalloc(&ms.out, ms.window_cap * sizeof(qsr_record_entry)));
     QSR_CUDA(cudaMalloc(&ms.mqubits, ms.window_cap * 4));
+    QSR_CUDA(cudaMalloc(&ms.fq, ms.window_cap * 4));
+    QSR_CUDA(cudaMalloc(&ms.fidx, ms.window_cap * 4));
 }
 
 void DeviceTableau::sync() { QSR_CUDA(cudaStreamSynchronize(stream)); }
@@ -205,6 +216,41 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
         }
         QSR_CUDA(cudaStreamSynchronize(st));
         QSR_CUDA(cudaFreeHost(pinned));
+    }
+    return ds;
+}
+
+// Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
+// parallel stable scatter straight into packed device words, then one upload. Windows built
+// by the plan are operand-disjoint by construction; the only error the reference would raise
+// later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
+std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st) {
+    WindowPlan p = plan_windows(c);
+    if (p.duplicate_measure)
+        fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
+    const uint64_t G = c.gates.size();
+    std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
+    scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
+    auto ds = std::make_unique<DeviceSchedule>();
+    ds->device = device;
+    ds->offsets = std::move(p.offsets);
+    ds->is_meas = std::move(p.is_meas);
+    const uint64_t W = ds->is_meas.size();
+    ds->mqubits.resize(W);
+    for (uint64_t w = 0; w < W; ++w) {
+        const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
+        if (!ds->is_meas[w]) {
+            ds->unitary_count += e - b;
+            continue;
+        }
+        for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(uint32_t(packed[i] & 0x0FFFFFFFu));
+        ds->measure_count += e - b;
+    }
+    QSR_CUDA(cudaSetDevice(device));
+    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
+    if (G) {
+        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
+        QSR_CUDA(cudaStreamSynchronize(st));
     }
     return ds;
 }
@@ -704,15 +750,12 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
     return guard([&] {
         auto wall0 = std::chrono::steady_clock::now();
         REQUIRE_PTR(c);
-        Schedule own;
-        if (!s) own = schedule_windows(*c, QSR_SINGLE_SHOT);
-        const Schedule &sched = s ? static_cast<const Schedule &>(*s) : own;
         const uint64_t nm = c->measure_count();
         if (nm) REQUIRE_PTR(record);
         auto h = std::make_unique<qsr_tableau>();
         h->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
         DeviceTableau &t = *h->t;
-        auto ds = upload_schedule(t.n, sched, device, t.stream);
+        auto ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream);
         if (ds->measure_count != nm)
             fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
         qsr_record_entry *d_rec = nullptr;
@@ -754,12 +797,10 @@ qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int de
                              qsr_engine **out) {
     return guard([&] {
         REQUIRE_PTR(c); REQUIRE_PTR(out);
-        Schedule own;
-        if (!s) own = schedule_windows(*c, QSR_SINGLE_SHOT);
-        const Schedule &sched = s ? static_cast<const Schedule &>(*s) : own;
         auto e = std::make_unique<qsr_engine>();
         e->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
-        e->ds = upload_schedule(e->t->n, sched, device, e->t->stream);
+        e->ds = s ? upload_schedule(e->t->n, *s, device, e->t->stream)
+                  : upload_circuit(*c, device, e->t->stream);
         QSR_CUDA(cudaMalloc(&e->d_rec,
                             std::max<uint64_t>(e->ds->measure_count, 1) * sizeof(qsr_record_entry)));
         *out = e.release();

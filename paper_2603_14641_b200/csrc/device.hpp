@@ -43,7 +43,15 @@ struct MeasureScratch {
     uint64_t *coin_index = nullptr; // device coin counter
     int *err = nullptr;             // odd-phase detector
     uint64_t window_cap = 0;
+    // batched collapses (k_batch.cu)
+    uint32_t *colbits = nullptr;    // [2*n_pad] column bits at the batch's qubits
+    uint64_t *Vx = nullptr, *Vz = nullptr; // [kMaxBatch][rm_pitch] pivot rows
+    uint32_t *vinfo = nullptr;      // [3*kMaxBatch]
+    uint32_t *bctl = nullptr;       // [4]
+    uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
 };
+
+constexpr int kMaxBatch = 16; // collapses per batched pass (k_batch.cu)
 
 struct DeviceTableau {
     int device = 0;
@@ -90,6 +98,10 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
                            bool timed, double *t_ms, double *ge_ms, double *cmp_ms);
 
 void configure_measure_kernels(DeviceTableau &t);
+// Up to kMaxBatch flagged collapses in one pass; returns how many were collapsed and whether
+// the batch stopped at a measurement that became deterministic (k_batch.cu).
+void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
+                   uint64_t seed, uint32_t &done, bool &det);
 // API-parity kernels on an RM tableau.
 void rm_column_mask(DeviceTableau &t, uint64_t q);          // fills t.ms.mask
 void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries, uint64_t &count);

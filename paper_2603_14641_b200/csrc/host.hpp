@@ -5,6 +5,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/qsr.h"
@@ -53,6 +54,35 @@ struct Schedule {
     std::vector<uint8_t> is_meas;    // nwindows
     uint64_t num_windows() const { return is_meas.size(); }
 };
+
+// Window plan of the O(G) scheduler: key = 2*round + is_measure per gate, the window
+// boundaries, and per-thread stable scatter offsets (see host_circuit.cpp).
+struct WindowPlan {
+    std::vector<uint32_t> key;
+    uint64_t nkeys = 0;
+    unsigned threads = 1;
+    std::vector<uint64_t> chunk_offsets; // [threads][nkeys]
+    std::vector<uint64_t> offsets;       // nwindows + 1
+    std::vector<uint8_t> is_meas;        // nwindows
+    bool duplicate_measure = false;      // some measurement window repeats a qubit
+};
+WindowPlan plan_windows(const Circuit &c);
+
+// Stable parallel scatter of the circuit's gates into schedule order, converted per gate
+// (qsr_gate for the API Schedule, packed device words for the engine).
+template <typename T, typename F>
+void scatter_windows(const Circuit &c, WindowPlan &p, T *out, F convert) {
+    const uint64_t G = c.gates.size();
+    const unsigned nt = p.threads;
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            uint64_t *off = p.chunk_offsets.data() + uint64_t(t) * p.nkeys;
+            for (uint64_t i = G * t / nt; i < G * (t + 1) / nt; ++i)
+                out[off[p.key[i]]++] = convert(c.gates[i]);
+        });
+    for (auto &x : th) x.join();
+}
 
 // schedule_windows (schedule.hpp:51-137) via the one-pass round closed form.
 Schedule schedule_windows(const Circuit &c, int mode);

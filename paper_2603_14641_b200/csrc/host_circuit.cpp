@@ -15,6 +15,7 @@
 // later makes measure_window reject the window is therefore preserved).
 #include <algorithm>
 #include <cstring>
+#include <thread>
 
 #include "host.hpp"
 
@@ -135,51 +136,80 @@ Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measur
     return c;
 }
 
-Schedule schedule_windows(const Circuit &c, int mode) {
-    c.check_valid();
+WindowPlan plan_windows(const Circuit &c) {
     const uint64_t G = c.gates.size();
+    const uint32_t n = c.num_qubits;
+    WindowPlan p;
+    p.key.resize(G);
+    // wire state = round << 1 | (last gate on the wire was a MEASURE)
+    std::vector<uint32_t> wire(n, 0);
+    uint32_t max_round = 0, dup = 0;
+    const qsr_gate *gates = c.gates.data();
+    uint32_t *key = p.key.data();
+    for (uint64_t i = 0; i < G; ++i) {
+        const qsr_gate g = gates[i];
+        const uint32_t kind = g.kind;
+        // check_valid (circuit.hpp:108-115), fused into the same pass
+        if (kind > QSR_MEASURE) fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
+        const bool two = kind >= QSR_CX && kind <= QSR_ISWAP;
+        const uint32_t q0 = g.q0, q1 = two ? g.q1 : g.q0;
+        if (q0 >= n || q1 >= n) fail(QSR_OUT_OF_RANGE, "gate operand out of range");
+        if (two && q0 == q1) fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
+        const uint32_t w0 = wire[q0], w1 = wire[q1];
+        const uint32_t r0 = w0 >> 1, r1 = w1 >> 1;
+        const uint32_t meas = kind == QSR_MEASURE;
+        const uint32_t r = meas ? (r0 > 1 ? r0 : 1) : 1 + (r0 > r1 ? r0 : r1);
+        // A measurement chained behind another on the same wire lands in the same window;
+        // the reference's measure_window then rejects it (measure.hpp:394-395).
+        dup |= meas & w0 & 1u;
+        wire[q0] = (r << 1) | meas;
+        wire[q1] = (r << 1) | meas;
+        key[i] = 2 * r + meas;
+        max_round = r > max_round ? r : max_round;
+    }
+    p.duplicate_measure = dup != 0;
+    p.nkeys = 2 * uint64_t(max_round) + 2;
+    // Per-thread key histograms over contiguous gate chunks -> stable scatter offsets
+    // (key-major, chunk-minor), so the parallel scatter keeps circuit index order per window.
+    const unsigned T = p.threads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                                     unsigned(G / (1 << 16)) + 1));
+    p.chunk_offsets.assign(uint64_t(T) * p.nkeys, 0);
+    {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < T; ++t)
+            th.emplace_back([&, t] {
+                uint64_t *h = p.chunk_offsets.data() + uint64_t(t) * p.nkeys;
+                for (uint64_t i = G * t / T; i < G * (t + 1) / T; ++i) ++h[p.key[i]];
+            });
+        for (auto &x : th) x.join();
+    }
+    uint64_t pos = 0;
+    p.offsets.push_back(0);
+    for (uint64_t key = 0; key < p.nkeys; ++key) {
+        uint64_t total = 0;
+        for (unsigned t = 0; t < T; ++t) {
+            uint64_t &h = p.chunk_offsets[uint64_t(t) * p.nkeys + key];
+            uint64_t cnt = h;
+            h = pos + total;
+            total += cnt;
+        }
+        if (total) {
+            pos += total;
+            p.offsets.push_back(pos);
+            p.is_meas.push_back(uint8_t(key & 1));
+        }
+    }
+    return p;
+}
+
+Schedule schedule_windows(const Circuit &c, int mode) {
+    WindowPlan p = plan_windows(c);
     Schedule s;
     s.mode = mode;
-    std::vector<uint32_t> wire_round(c.num_qubits, 0);
-    std::vector<uint32_t> round(G);
-    uint32_t max_round = 0;
-    for (uint64_t i = 0; i < G; ++i) {
-        const qsr_gate &g = c.gates[i];
-        uint32_t r;
-        if (g.kind == QSR_MEASURE) {
-            r = std::max<uint32_t>(1, wire_round[g.q0]);
-            wire_round[g.q0] = r;
-        } else if (gate_arity(g.kind) == 2) {
-            r = 1 + std::max(wire_round[g.q0], wire_round[g.q1]);
-            wire_round[g.q0] = r;
-            wire_round[g.q1] = r;
-        } else {
-            r = 1 + wire_round[g.q0];
-            wire_round[g.q0] = r;
-        }
-        round[i] = r;
-        max_round = std::max(max_round, r);
-    }
-    // Stable counting sort on the key 2*round + is_measure (unitary window first).
-    const uint64_t nkeys = 2 * uint64_t(max_round) + 2;
-    std::vector<uint64_t> count(nkeys + 1, 0);
-    for (uint64_t i = 0; i < G; ++i)
-        ++count[2 * uint64_t(round[i]) + (c.gates[i].kind == QSR_MEASURE) + 1];
-    for (uint64_t key = 0; key < nkeys; ++key)
-        count[key + 1] += count[key];
-    s.gates.resize(G);
-    s.offsets.reserve(nkeys + 1);
-    s.offsets.push_back(0);
-    for (uint64_t key = 2; key < nkeys; ++key) {
-        if (count[key + 1] > count[key]) {
-            s.offsets.push_back(count[key + 1]);
-            s.is_meas.push_back(uint8_t(key & 1));
-        }
-    }
-    for (uint64_t i = 0; i < G; ++i) {
-        uint64_t key = 2 * uint64_t(round[i]) + (c.gates[i].kind == QSR_MEASURE);
-        s.gates[count[key]++] = c.gates[i];
-    }
+    s.gates.resize(c.gates.size());
+    scatter_windows(c, p, s.gates.data(), [](const qsr_gate &g) { return g; });
+    s.offsets = std::move(p.offsets);
+    s.is_meas = std::move(p.is_meas);
     return s;
 }
 

@@ -352,9 +352,14 @@ void finish(DeviceTableau &t, uint64_t seed, qsr_record_entry *out) {
     count_launch();
 }
 
-struct EventPair {
-    cudaEvent_t a = nullptr, b = nullptr;
-};
+// QSR_MEASURE_BATCH=0 selects the one-collapse-per-pass path (differential testing / A-B).
+bool batch_collapses() {
+    static bool on = [] {
+        const char *e = getenv("QSR_MEASURE_BATCH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 } // namespace
 
@@ -390,14 +395,41 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
     QSR_CUDA(cudaStreamSynchronize(t.stream)); // flags_host ready
     // Sequential collapse loop in window order (measure.hpp:409-431); device-resident
     // decisions (pivot, coin, deterministic fallback).
-    for (uint64_t i = 0; i < m; ++i) {
-        if (!flags_host[i]) continue;
-        set_ctl(t, MODE_COLLAPSE, 0, qubits[i]);
-        column_mask(t, qubits[i]);
-        compact(t, nullptr);
-        rowmul(t, 1u << MODE_COLLAPSE, 1);
-        det_partial(t);
-        finish(t, seed, t.ms.out + i);
+    if (batch_collapses()) {
+        // Batched: up to kMaxBatch consecutive flagged collapses per streaming pass.
+        std::vector<uint32_t> fq, fidx;
+        for (uint64_t i = 0; i < m; ++i)
+            if (flags_host[i]) { fq.push_back(qubits[i]); fidx.push_back(uint32_t(i)); }
+        if (!fq.empty()) {
+            QSR_CUDA(cudaMemcpyAsync(t.ms.fq, fq.data(), fq.size() * 4, cudaMemcpyHostToDevice, t.stream));
+            QSR_CUDA(cudaMemcpyAsync(t.ms.fidx, fidx.data(), fidx.size() * 4, cudaMemcpyHostToDevice,
+                                     t.stream));
+        }
+        size_t pos = 0;
+        while (pos < fq.size()) {
+            uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - pos)), done = 0;
+            bool det = false;
+            measure_batch(t, t.ms.fq + pos, t.ms.fidx + pos, b, seed, done, det);
+            pos += done;
+            if (det) { // flagged at window start, deterministic now (measure.hpp:417-421)
+                set_ctl(t, MODE_DET, 0, fq[pos]);
+                column_mask(t, fq[pos]);
+                compact(t, nullptr);
+                det_partial(t);
+                finish(t, seed, t.ms.out + fidx[pos]);
+                ++pos;
+            }
+        }
+    } else {
+        for (uint64_t i = 0; i < m; ++i) {
+            if (!flags_host[i]) continue;
+            set_ctl(t, MODE_COLLAPSE, 0, qubits[i]);
+            column_mask(t, qubits[i]);
+            compact(t, nullptr);
+            rowmul(t, 1u << MODE_COLLAPSE, 1);
+            det_partial(t);
+            finish(t, seed, t.ms.out + i);
+        }
     }
     // Deterministic outcomes of the unflagged measurements (measure.hpp:432-438).
     for (uint64_t i = 0; i < m; ++i) {

@@ -242,3 +242,59 @@ def test_engine_matches_run_single_shot(q, oracle):
     # second run on the same resident inputs is identical (state reset per run)
     e.run(9)
     np.testing.assert_array_equal(e.record(), rec)
+
+
+@pytest.mark.parametrize("n", [3, 64, 200])
+def test_ghz_chain_deterministic_breaks(q, oracle, n):
+    """All qubits flagged at window start, all but the first become deterministic mid-window
+    (exercises the batched path's deterministic break, measure.hpp:417-421)."""
+    G = q.GateKind
+    gates = [(G.H, 0)] + [(G.CX, i, i + 1) for i in range(n - 1)] + [(G.MEASURE, i) for i in range(n)]
+    c = q.Circuit(n, gates)
+    for seed in range(3):
+        r = q.run_single_shot(c, seed)
+        x, z, s, rec, _ = oracle.run_single_shot(n, c.gate_array, seed)
+        assert_same(r.tableau, x, z, s)
+        np.testing.assert_array_equal(r.record_array, rec)
+        assert rec["deterministic"].tolist() == [0] + [1] * (n - 1)
+
+
+def test_mixed_bell_and_random(q, oracle):
+    G = q.GateKind
+    n = 150
+    g = list(q.generate_random(n, 30, 77, 0.0).gate_array)
+    g = [(int(a["kind"]), int(a["q0"]), int(a["q1"])) for a in q.generate_random(n, 30, 77, 0.0).gate_array]
+    g += [(G.H, 0), (G.CX, 0, 1)] + [(G.MEASURE, i) for i in range(0, n, 2)]
+    g += [(int(a["kind"]), int(a["q0"]), int(a["q1"])) for a in q.generate_random(n, 10, 78, 1.0).gate_array]
+    c = q.Circuit(n, g)
+    r = q.run_single_shot(c, 11)
+    x, z, s, rec, _ = oracle.run_single_shot(n, c.gate_array, 11)
+    assert_same(r.tableau, x, z, s)
+    np.testing.assert_array_equal(r.record_array, rec)
+
+
+def test_single_collapse_path_matches(q):
+    """QSR_MEASURE_BATCH=0 (one collapse per pass) must agree with the batched default."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_2603_14641_b200 import quasar as q\n"
+        "from oracle.oracle import best_available\n"
+        "o = best_available()\n"
+        "for seed in range(4):\n"
+        "    n = 40 + 37 * seed\n"
+        "    c = q.generate_random(n, 30, seed, 1.0)\n"
+        "    r = q.run_single_shot(c, seed)\n"
+        "    x, z, s, rec, _ = o.run_single_shot(n, c.gate_array, seed)\n"
+        "    gx, gz, gs = r.tableau.planes()\n"
+        "    assert np.array_equal(gx, x) and np.array_equal(gz, z) and np.array_equal(gs, s)\n"
+        "    assert np.array_equal(r.record_array, rec)\n"
+        "print('ok')\n")
+    import os
+    env = dict(os.environ, QSR_MEASURE_BATCH="0")
+    root = __import__("pathlib").Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout
