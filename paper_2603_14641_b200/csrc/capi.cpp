@@ -66,7 +66,7 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
     QSR_CUDA(cudaMalloc(&ms.colbits, 2 * n_pad * 4));
     alloc(&ms.Vx, uint64_t(kMaxBatch) * rm_pitch);
     alloc(&ms.Vz, uint64_t(kMaxBatch) * rm_pitch);
-    QSR_CUDA(cudaMalloc(&ms.vinfo, 3 * kMaxBatch * 4));
+    QSR_CUDA(cudaMalloc(&ms.vinfo, 4 * kMaxBatch * 4));
     QSR_CUDA(cudaMalloc(&ms.bctl, 16));
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
@@ -528,6 +528,7 @@ qsr_status qsr_tableau_basis_state(qsr_tableau *h, const uint8_t *init) {
             QSR_CUDA(cudaMemcpyAsync(d_init, init, t.n, cudaMemcpyHostToDevice, t.stream));
         }
         launch_zero_state(t, d_init);
+        t.trusted = true;
         t.sync();
         if (d_init) cudaFree(d_init);
     });
@@ -553,6 +554,7 @@ qsr_status qsr_tableau_upload(qsr_tableau *h, const uint64_t *x, const uint64_t 
         DeviceTableau &t = *h->t;
         QSR_CUDA(cudaSetDevice(t.device));
         upload_planes(t, x, z, layout);
+        t.trusted = false;
         QSR_CUDA(cudaMemcpyAsync(t.s, s, 2 * t.k * 8, cudaMemcpyHostToDevice, t.stream));
         t.sync();
     });

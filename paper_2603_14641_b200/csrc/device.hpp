@@ -51,7 +51,7 @@ struct MeasureScratch {
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
 };
 
-constexpr int kMaxBatch = 16; // collapses per batched pass (k_batch.cu)
+constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
 
 struct DeviceTableau {
     int device = 0;
@@ -63,6 +63,10 @@ struct DeviceTableau {
     uint64_t *x2 = nullptr, *z2 = nullptr; // transpose targets
     uint64_t *s = nullptr;                 // signs (cm_pitch words)
     int layout = QSR_COLUMN_MAJOR;
+    // Built only from basis states, gates and measurements (a valid tableau). Uploaded
+    // tableaux may be corrupt and are measured on the per-collapse path, which checks the
+    // phase of every single product (measure.hpp:373-374, tableau.hpp:345-350).
+    bool trusted = true;
     // gate-window sign partials
     uint64_t *sign_partials = nullptr;
     uint64_t sign_partial_chunks = 0;

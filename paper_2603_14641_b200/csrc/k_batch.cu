@@ -1,25 +1,33 @@
-// Batched projective measurement: B consecutive probabilistic collapses of a measurement
-// window applied in ONE streaming pass over the RM tableau (bit-identical to applying them one
-// by one with the fused recipe of k_measure.cu, which is itself bit-identical to the
+// Batched projective measurement: up to kMaxBatch consecutive probabilistic collapses of a
+// measurement window applied in ONE streaming pass over the RM tableau, bit-identical to
+// applying them one by one with the fused recipe of k_measure.cu (itself bit-identical to the
 // reference's parallel_ge + swap_anti_commuting + inject_x, measure.hpp:409-431).
 //
-// Why it is exact. Collapse m multiplies every row of R_m = {rows != S_c, D_c with X[q_m]} by
-// V_m = S_{c_m} as it stands at time m, then D_{c_m} <- V_m, S_{c_m} <- +/-Z_{q_m}. A row's
-// membership in R_m depends only on its X bit at q_m at time m, which is its bit at batch
-// start XORed with the X bits at q_m of the V's it absorbed earlier. So with
+// Why batching is exact. Collapse m multiplies every row of R_m = {rows other than S_c, D_c
+// with X[q_m] set} by V_m = S_{c_m} as it stands at time m, then D_{c_m} <- V_m and
+// S_{c_m} <- +/-Z_{q_m}. A row's membership in R_m depends only on its X bit at q_m at time m,
+// i.e. its bit at batch start XOR the X bits at q_m of the V's it absorbed before. With
 //   colbits_r[m] = X_r[q_m] at batch start            (phase A, a column gather)
 //   vb[m'][m]    = X bit of V_{m'} at q_m              (phase B)
-// the membership vector of every row follows from the recurrence
-//   member_r[m] = colbits_r[m] ^ parity(member_r[<m] & VBcol[m]),
-// and the row's final value and sign are r ^ sum V_m, s_r ^ sum (s(V_m) ^ flip_m), with the
-// mod-4 phase of each product taken against the row as it stands just before it (phase C).
-// Only the pivot rows need sequential treatment (phase B, one CTA): c_m is the smallest
-// stabilizer whose current X bit at q_m is set, V_m is S_{c_m} after its own earlier
-// memberships, and the coin is Philox(seed, 0, 0, coin_index++) & 1.
+// every row's membership vector follows from  member[m] = colbits[m] ^ parity(member[<m] &
+// VBcol[m]). Only the pivot rows need sequential treatment (phase B, one CTA): c_m is the
+// smallest stabilizer whose current X bit at q_m is set, V_m is S_{c_m} after its own earlier
+// memberships, the coin is Philox(seed, 0, 0, coin_index++) & 1.
 //
-// Traffic: one read + write of the touched rows per batch instead of per collapse
-// (B x fewer HBM bytes); the pivot rows V_m are staged through shared memory in 64-word
-// slices.
+// Why the phase is cheap. For Hermitian Paulis P(a)P(b) = i^g P(a^b) with, summed over qubits,
+//   g(a, b) = beta(a) + beta(b) + 2|a_z & b_x| - beta(a^b)   (mod 4),  beta(p) = |p_x & p_z|,
+// which is exactly product_phase_counts' (plus - minus) (tableau.hpp:336-342). Absorbing
+// V_1..V_k in order (V on the left, as the reference's control*target) therefore telescopes:
+//   E = beta(r_start) - beta(r_end) + sum_j beta(V_j) + 2 sum_j |V_jz & cur_{j-1,x}|  (mod 4).
+// Every single product of a valid tableau has even phase, so the XOR of the per-product flips
+// equals bit 1 of E, and the row's sign becomes s_r ^ XOR_j s(V_j) ^ ((E >> 1) & 1). Per
+// absorbed word this costs one AND-XOR into a parity accumulator plus the two row XORs.
+// (An odd E flags a corrupted tableau; uploaded, possibly corrupt tableaux are measured on the
+// per-collapse path, which checks every product exactly.)
+//
+// Traffic: one read + write of the touched rows per batch instead of per collapse; the pivot
+// rows are staged through shared memory (cp.async, double-buffered 64-word slices) and each
+// staged word is reused by the 4 rows a warp carries.
 #include "common.cuh"
 #include "device.hpp"
 
@@ -27,8 +35,11 @@ namespace qsr {
 
 namespace {
 
-constexpr int kB = kMaxBatch;       // collapses per batch (<= 32: u32 membership masks)
+using u64 = unsigned long long;
+constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
 enum : uint32_t { BL_LEN = 0, BL_DET = 1 };
+// vinfo layout (u32 [4*kB]): vb | sign of V_m | c_m | beta(V_m) mod 4
+enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB };
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
 
@@ -42,6 +53,20 @@ __device__ __forceinline__ uint32_t membership(uint32_t cb, const uint32_t *vbco
         M |= bit << m;
     }
     return M;
+}
+
+__device__ __forceinline__ int block_sum(int v, int *red /* >= 32 ints */) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    int t = 0;
+    if (threadIdx.x < 32) {
+        t = threadIdx.x < (blockDim.x + 31) / 32 ? red[threadIdx.x] : 0;
+        t = warp_sum(t);
+    }
+    return t; // valid in warp 0
 }
 
 // ---- phase A: column bits of all rows at the batch's measured qubits ----------------
@@ -62,8 +87,6 @@ __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64
 }
 
 // ---- phase B: pivots, pivot rows, coins (one CTA) --------------------------------------
-// vinfo layout: [0,kB) vb (X bits of V_m at q_0..q_{b-1}), [kB,2kB) sign of V_m,
-//               [2kB,3kB) c_m (stabilizer index).
 __global__ void __launch_bounds__(1024)
 k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t k,
                uint64_t n, uint64_t n_pad, uint64_t *__restrict__ s,
@@ -72,11 +95,11 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                uint64_t *__restrict__ Vz, uint32_t *__restrict__ vinfo, uint32_t *__restrict__ bctl,
                uint64_t seed, uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
                int *__restrict__ err) {
-    __shared__ uint32_t s_vb[kB], s_vsign[kB], s_c[kB], s_q[kB], s_vbcol[kB];
-    __shared__ uint32_t s_min;
-    __shared__ int s_red[32][kB];
-    __shared__ uint32_t s_len;
-    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x;
+    __shared__ uint32_t s_vb[kB], s_vsign[kB], s_c[kB], s_q[kB], s_vbcol[kB], s_beta[kB];
+    __shared__ uint32_t s_min, s_len;
+    __shared__ int s_red[32];
+    __shared__ uint32_t s_bits[kB];
+    const uint32_t tid = threadIdx.x, nthr = blockDim.x;
     if (tid < b) s_q[tid] = fq[tid];
     if (tid == 0) s_len = b;
     __syncthreads();
@@ -117,41 +140,41 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         }
         const uint32_t c = found;
         const uint32_t Mc = membership(colbits[n_pad + c], s_vbcol, 0, m);
-        // V_m = S_c after its memberships (ordered products with mod-4 phase per product).
-        int ph[kB];
-#pragma unroll
-        for (int j = 0; j < kB; ++j) ph[j] = 0;
+        // V_m = S_c after its memberships; phase by the telescoped formula (file header).
         const uint64_t rs = n_pad + c;
+        int e_part = 0, beta_part = 0;
+        u64 acc = 0;
         for (uint64_t i = tid; i < k; i += nthr) {
-            uint64_t cx = x[rs * pitch + i], cz = z[rs * pitch + i];
-#pragma unroll
-            for (int j = 0; j < kB; ++j) {
-                if ((Mc >> j) & 1u) {
-                    const uint64_t vx = Vx[uint64_t(j) * pitch + i], vz = Vz[uint64_t(j) * pitch + i];
-                    ph[j] += phase_delta(vx, vz, cx, cz);
-                    cx ^= vx;
-                    cz ^= vz;
-                }
+            u64 cx = x[rs * pitch + i], cz = z[rs * pitch + i];
+            e_part += __popcll(cx & cz);
+            for (uint32_t U = Mc; U; U &= U - 1) {
+                const uint32_t j = __ffs(U) - 1;
+                const u64 vx = Vx[uint64_t(j) * pitch + i], vz = Vz[uint64_t(j) * pitch + i];
+                acc ^= vz & cx;
+                cx ^= vx;
+                cz ^= vz;
             }
+            const int bend = __popcll(cx & cz);
+            e_part -= bend;
+            beta_part += bend;
             Vx[uint64_t(m) * pitch + i] = cx;
             Vz[uint64_t(m) * pitch + i] = cz;
         }
-#pragma unroll
-        for (int j = 0; j < kB; ++j) {
-            int v = warp_sum(ph[j]);
-            if (lane == 0) s_red[warp][j] = v;
-        }
-        __syncthreads();
+        e_part += 2 * (__popcll(acc) & 1);
+        const int e_tot = block_sum(e_part, s_red);
+        const int b_tot = block_sum(beta_part, s_red);
         if (tid == 0) {
+            int E = e_tot;
             uint32_t sign = uint32_t((s[rs >> 6] >> (rs & 63)) & 1u);
-            for (uint32_t j = 0; j < m; ++j) {
-                if (!((Mc >> j) & 1u)) continue;
-                int tot = 0;
-                for (uint32_t w = 0; w < (nthr + 31) / 32; ++w) tot += s_red[w][j];
-                if (tot & 1) atomicExch(err, 1);
-                sign ^= s_vsign[j] ^ ((uint32_t(tot) >> 1) & 1u);
+            for (uint32_t U = Mc; U; U &= U - 1) {
+                const uint32_t j = __ffs(U) - 1;
+                E += int(s_beta[j]);
+                sign ^= s_vsign[j];
             }
+            if (E & 1) atomicExch(err, 1);
+            sign ^= (uint32_t(E) >> 1) & 1u;
             s_vsign[m] = sign;
+            s_beta[m] = uint32_t(b_tot) & 3u;
             s_c[m] = c;
             const uint64_t idx = *coin_index;
             const uint32_t coin = uint32_t(d_philox_word(seed, 0, 0, idx) & 1u);
@@ -162,15 +185,15 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             s[rd >> 6] = (s[rd >> 6] & ~(1ull << (rd & 63))) | (uint64_t(sign) << (rd & 63));
             s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (uint64_t(coin) << (rs & 63));
         }
-        __syncthreads(); // V_m visible to the block
+        __syncthreads(); // V_m (global) and the shared pivot bookkeeping visible to the block
         if (tid < b) {
             const uint32_t qj = s_q[tid];
-            s_red[0][tid] = uint32_t((Vx[uint64_t(m) * pitch + (qj >> 6)] >> (qj & 63)) & 1u);
+            s_bits[tid] = uint32_t((Vx[uint64_t(m) * pitch + (qj >> 6)] >> (qj & 63)) & 1u);
         }
         __syncthreads();
         if (tid == 0) {
             uint32_t vb = 0;
-            for (uint32_t j = 0; j < b; ++j) vb |= uint32_t(s_red[0][j]) << j;
+            for (uint32_t j = 0; j < b; ++j) vb |= s_bits[j] << j;
             s_vb[m] = vb;
         }
         // Special rows: D_c <- V_m (bits), S_c <- Z_{q_m}.
@@ -186,34 +209,23 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
     }
     __syncthreads();
     if (tid < kB) {
-        vinfo[tid] = tid < s_len ? s_vb[tid] : 0u;
-        vinfo[kB + tid] = tid < s_len ? s_vsign[tid] : 0u;
-        vinfo[2 * kB + tid] = tid < s_len ? s_c[tid] : 0xFFFFFFFFu;
+        const bool v = tid < s_len;
+        vinfo[VI_VB + tid] = v ? s_vb[tid] : 0u;
+        vinfo[VI_SIGN + tid] = v ? s_vsign[tid] : 0u;
+        vinfo[VI_C + tid] = v ? s_c[tid] : 0xFFFFFFFFu;
+        vinfo[VI_BETA + tid] = v ? s_beta[tid] : 0u;
     }
     if (tid == 0) bctl[BL_LEN] = s_len;
 }
 
 // ---- phase C: every other row absorbs its V's in one pass --------------------------
-// One warp per row; the CTA's rows share each 128-word slice of the V's staged in shared
-// memory. Per absorbed V the mod-4 product phase is kept in a bit-sliced 2-bit counter per bit
-// position (c1 = ones, c2 = twos), flushed with two popcounts per slice:
-//   x1z2 = vx & cz ; anti = (cx & vz) ^ x1z2 ; (cx, cz) ^= (vx, vz)
-//   c2 ^= (c1 ^ cx ^ cz ^ x1z2) & anti ; c1 ^= anti
-// which adds +1 (mod 4) for each bit where V*cur picks up +i and -1 where it picks up -i —
-// the same count as product_phase_counts (tableau.hpp:336-342), in ~8 logic ops per word.
-constexpr int kCThreads = 512;
+constexpr int kCThreads = 256;
 constexpr int kCWarps = kCThreads / 32;
-constexpr int kSlice = 128; // words per staged V slice (4 per lane)
-
-using u64 = unsigned long long;
-__device__ __forceinline__ void absorb(u64 vx, u64 vz, u64 &cx, u64 &cz, u64 &c1, u64 &c2) {
-    const u64 x1z2 = vx & cz;
-    const u64 anti = (cx & vz) ^ x1z2;
-    cx ^= vx;
-    cz ^= vz;
-    c2 ^= (c1 ^ cx ^ cz ^ x1z2) & anti;
-    c1 ^= anti;
-}
+constexpr int kRowsPerWarp = 4;
+constexpr int kGroupRows = kCWarps * kRowsPerWarp; // 32 consecutive rows per CTA iteration
+constexpr int kSlice = 64;                          // words per staged V slice (2 per lane)
+constexpr size_t kSliceWords = size_t(kB) * 2 * kSlice;
+constexpr size_t kApplySmem = 2 * kSliceWords * sizeof(u64); // double buffer
 
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const unsigned sa = unsigned(__cvta_generic_to_shared(smem));
@@ -222,17 +234,16 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-// Stage words [w0, w0+kSlice) of V_0..V_{len-1} (x and z) into buf[j][plane][word]
-// asynchronously (cp.async, 16 bytes per op; pitch % 16 == 0 so slices past k read zeros).
-__device__ __forceinline__ void stage_slice(u64 (*buf)[2][kSlice], const uint64_t *Vx,
-                                            const uint64_t *Vz, uint64_t pitch, uint64_t w0,
-                                            uint32_t len, uint32_t tid) {
+// Stage words [w0, w0+kSlice) of V_0..V_{len-1} (x and z) into buf[(j*2+plane)*kSlice + w]
+// with cp.async (16 bytes per op; pitch % 16 == 0, so past k it reads the zero padding).
+__device__ __forceinline__ void stage_slice(u64 *buf, const uint64_t *Vx, const uint64_t *Vz,
+                                            uint64_t pitch, uint64_t w0, uint32_t len) {
     const uint32_t pairs = len * 2 * (kSlice / 2);
-    for (uint32_t e = tid; e < pairs; e += kCThreads) {
+    for (uint32_t e = threadIdx.x; e < pairs; e += kCThreads) {
         const uint32_t w = 2 * (e & (kSlice / 2 - 1)), jp = e / (kSlice / 2);
         const uint32_t j = jp >> 1, plane = jp & 1;
         const uint64_t gw = w0 + w;
-        u64 *dst = &buf[j][plane][w];
+        u64 *dst = buf + size_t(jp) * kSlice + w;
         if (gw < pitch) cp_async16(dst, (plane ? Vz : Vx) + uint64_t(j) * pitch + gw);
         else { dst[0] = 0; dst[1] = 0; }
     }
@@ -245,112 +256,120 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
               const uint32_t *__restrict__ colbits, const uint64_t *__restrict__ Vx,
               const uint64_t *__restrict__ Vz, const uint32_t *__restrict__ vinfo,
               const uint32_t *__restrict__ bctl, int *__restrict__ err) {
-    __shared__ uint32_t s_vbcol[kB], s_vsign[kB], s_c[kB], s_vb[kB];
-    extern __shared__ __align__(16) u64 sv_raw[]; // [2 buffers][kB][2 planes][kSlice]
-    u64 (*sv[2])[2][kSlice] = {reinterpret_cast<u64 (*)[2][kSlice]>(sv_raw),
-                               reinterpret_cast<u64 (*)[2][kSlice]>(sv_raw + kB * 2 * kSlice)};
+    __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
+    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask;
+    extern __shared__ __align__(16) u64 sv_raw[];
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < kB) {
-        s_vb[tid] = vinfo[tid];
-        s_vsign[tid] = vinfo[kB + tid];
-        s_c[tid] = vinfo[2 * kB + tid];
+        s_vb[tid] = vinfo[VI_VB + tid];
+        s_c[tid] = vinfo[VI_C + tid];
+    }
+    if (tid == 0) {
+        uint32_t vs = 0, b0 = 0, b1 = 0;
+        for (uint32_t j = 0; j < len; ++j) {
+            vs |= (vinfo[VI_SIGN + j] & 1u) << j;
+            b0 |= (vinfo[VI_BETA + j] & 1u) << j;
+            b1 |= ((vinfo[VI_BETA + j] >> 1) & 1u) << j;
+        }
+        s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
     }
     __syncthreads();
     if (tid < kB) {
         uint32_t col = 0;
-        for (uint32_t mp = 0; mp < len; ++mp)
-            if (mp < tid) col |= ((s_vb[mp] >> tid) & 1u) << mp;
+        for (uint32_t mp = 0; mp < len && mp < tid; ++mp) col |= ((s_vb[mp] >> tid) & 1u) << mp;
         s_vbcol[tid] = col;
     }
     __syncthreads();
-    const uint64_t groups = nrows / kCWarps;
+    const uint64_t groups = nrows / kGroupRows;
     const uint32_t nslices = uint32_t((k + kSlice - 1) / kSlice);
     for (uint64_t grp = blockIdx.x; grp < groups; grp += gridDim.x) {
-        const uint64_t r = grp * kCWarps + warp;
-        // Membership: pivot stabilizers are final already; replaced destabilizers restart
-        // from V_m at collapse m+1; every other row starts from its batch-start column bits.
-        uint32_t M;
-        {
+        const uint64_t r0 = grp * kGroupRows + warp * kRowsPerWarp;
+        // Membership per row: pivot stabilizers are final already; replaced destabilizers
+        // restart from V_m after collapse m; every other row starts from its column bits.
+        uint32_t M[kRowsPerWarp];
+#pragma unroll
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            const uint64_t r = r0 + q;
             uint32_t cb = colbits[r], start = 0;
             bool skip = false;
             for (uint32_t j = 0; j < len; ++j) {
                 if (r == n_pad + s_c[j]) skip = true;
                 if (r == s_c[j]) { cb = s_vb[j]; start = j + 1; }
             }
-            M = skip ? 0u : membership(cb, s_vbcol, start, len);
+            M[q] = skip ? 0u : membership(cb, s_vbcol, start, len);
         }
-        int ph[kB];
+        const uint32_t U = M[0] | M[1] | M[2] | M[3];
+        u64 acc[kRowsPerWarp];
+        int bd[kRowsPerWarp];
 #pragma unroll
-        for (int j = 0; j < kB; ++j) ph[j] = 0;
-        uint64_t *xr = x + r * pitch, *zr = z + r * pitch;
-        stage_slice(sv[0], Vx, Vz, pitch, 0, len, tid);
+        for (int q = 0; q < kRowsPerWarp; ++q) acc[q] = 0, bd[q] = 0;
+        stage_slice(sv_raw, Vx, Vz, pitch, 0, len);
         for (uint32_t sl = 0; sl < nslices; ++sl) {
             cp_async_wait_all();
-            __syncthreads(); // slice sl staged; everyone is done with slice sl-1's buffer
+            __syncthreads(); // slice sl staged; everyone is done with the other buffer
             if (sl + 1 < nslices)
-                stage_slice(sv[(sl + 1) & 1], Vx, Vz, pitch, uint64_t(sl + 1) * kSlice, len, tid);
-            if (M == 0) continue;
-            u64 (*buf)[2][kSlice] = sv[sl & 1];
-            // lane words: [w0 + 2*lane, +1] and [w0 + 64 + 2*lane, +1] (two 512-byte warp runs)
-            const uint64_t w0 = uint64_t(sl) * kSlice;
-            const uint64_t i0 = w0 + 2 * lane, i1 = i0 + 64;
-            const bool a0 = i0 < pitch, a1 = i1 < pitch;
-            ulonglong2 xa = make_ulonglong2(0ull, 0ull), za = xa, xb = xa, zb = xa;
-            if (a0) {
-                xa = __ldcs(reinterpret_cast<const ulonglong2 *>(xr + i0));
-                za = __ldcs(reinterpret_cast<const ulonglong2 *>(zr + i0));
-            }
-            if (a1) {
-                xb = __ldcs(reinterpret_cast<const ulonglong2 *>(xr + i1));
-                zb = __ldcs(reinterpret_cast<const ulonglong2 *>(zr + i1));
-            }
+                stage_slice(sv_raw + ((sl + 1) & 1) * kSliceWords, Vx, Vz, pitch,
+                            uint64_t(sl + 1) * kSlice, len);
+            if (U == 0) continue;
+            const u64 *buf = sv_raw + (sl & 1) * kSliceWords;
+            const uint64_t i = uint64_t(sl) * kSlice + 2 * lane;
+            const bool act = i < pitch;
+            ulonglong2 cx[kRowsPerWarp], cz[kRowsPerWarp];
 #pragma unroll
-            for (int j = 0; j < kB; ++j) {
-                if ((M >> j) & 1u) {
-                    const ulonglong2 vxa = *reinterpret_cast<const ulonglong2 *>(&buf[j][0][2 * lane]);
-                    const ulonglong2 vza = *reinterpret_cast<const ulonglong2 *>(&buf[j][1][2 * lane]);
-                    const ulonglong2 vxb = *reinterpret_cast<const ulonglong2 *>(&buf[j][0][64 + 2 * lane]);
-                    const ulonglong2 vzb = *reinterpret_cast<const ulonglong2 *>(&buf[j][1][64 + 2 * lane]);
-                    u64 c1 = 0, c2 = 0;
-                    absorb(vxa.x, vza.x, xa.x, za.x, c1, c2);
-                    absorb(vxa.y, vza.y, xa.y, za.y, c1, c2);
-                    absorb(vxb.x, vzb.x, xb.x, zb.x, c1, c2);
-                    absorb(vxb.y, vzb.y, xb.y, zb.y, c1, c2);
-                    ph[j] += __popcll(c1) + 2 * __popcll(c2);
+            for (int q = 0; q < kRowsPerWarp; ++q) {
+                cx[q] = make_ulonglong2(0ull, 0ull);
+                cz[q] = cx[q];
+                if (M[q] && act) {
+                    cx[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(x + (r0 + q) * pitch + i));
+                    cz[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(z + (r0 + q) * pitch + i));
+                    bd[q] += __popcll(cx[q].x & cz[q].x) + __popcll(cx[q].y & cz[q].y);
                 }
             }
-            if (a0) {
-                __stcs(reinterpret_cast<ulonglong2 *>(xr + i0), xa);
-                __stcs(reinterpret_cast<ulonglong2 *>(zr + i0), za);
+            for (uint32_t W = U; W; W &= W - 1) {
+                const uint32_t j = __ffs(W) - 1;
+                const ulonglong2 vx = *reinterpret_cast<const ulonglong2 *>(buf + (2 * j) * kSlice + 2 * lane);
+                const ulonglong2 vz = *reinterpret_cast<const ulonglong2 *>(buf + (2 * j + 1) * kSlice + 2 * lane);
+#pragma unroll
+                for (int q = 0; q < kRowsPerWarp; ++q) {
+                    if ((M[q] >> j) & 1u) {
+                        acc[q] ^= (vz.x & cx[q].x) ^ (vz.y & cx[q].y);
+                        cx[q].x ^= vx.x; cx[q].y ^= vx.y;
+                        cz[q].x ^= vz.x; cz[q].y ^= vz.y;
+                    }
+                }
             }
-            if (a1) {
-                __stcs(reinterpret_cast<ulonglong2 *>(xr + i1), xb);
-                __stcs(reinterpret_cast<ulonglong2 *>(zr + i1), zb);
+#pragma unroll
+            for (int q = 0; q < kRowsPerWarp; ++q) {
+                if (M[q] && act) {
+                    bd[q] -= __popcll(cx[q].x & cz[q].x) + __popcll(cx[q].y & cz[q].y);
+                    __stcs(reinterpret_cast<ulonglong2 *>(x + (r0 + q) * pitch + i), cx[q]);
+                    __stcs(reinterpret_cast<ulonglong2 *>(z + (r0 + q) * pitch + i), cz[q]);
+                }
             }
         }
         cp_async_wait_all();
         __syncthreads(); // buffers free before the next row group stages into them
-        if (M == 0) continue;
-        uint32_t dsign = 0;
+        if (U == 0) continue;
+        uint64_t flips = 0;
+        bool odd = false;
 #pragma unroll
-        for (int j = 0; j < kB; ++j) {
-            if ((M >> j) & 1u) {
-                const int tot = warp_sum(ph[j]);
-                if (tot & 1) dsign |= 0x80000000u; // odd phase: corrupted tableau
-                dsign ^= s_vsign[j] ^ ((uint32_t(tot) >> 1) & 1u);
+        for (int q = 0; q < kRowsPerWarp; ++q) {
+            const int tot = warp_sum(bd[q] + 2 * (__popcll(acc[q]) & 1));
+            if (M[q]) {
+                const int E = tot + __popc(M[q] & s_b0_mask) + 2 * __popc(M[q] & s_b1_mask);
+                odd |= (E & 1) != 0;
+                const uint32_t f = parity32(M[q] & s_vs_mask) ^ ((uint32_t(E) >> 1) & 1u);
+                flips |= uint64_t(f) << ((r0 + q) & 63);
             }
         }
         if (lane == 0) {
-            if (dsign & 0x80000000u) atomicExch(err, 1);
-            if (dsign & 1u)
-                atomicXor(reinterpret_cast<unsigned long long *>(s + (r >> 6)), 1ull << (r & 63));
+            if (odd) atomicExch(err, 1);
+            if (flips) atomicXor(reinterpret_cast<unsigned long long *>(s + (r0 >> 6)), flips);
         }
     }
 }
-
-constexpr size_t kApplySmem = size_t(2) * kB * 2 * kSlice * sizeof(u64);
 
 } // namespace
 

@@ -127,6 +127,7 @@ void launch_zero_state(DeviceTableau &t, const uint8_t *d_init) {
     QSR_CUDA(cudaGetLastError());
     count_launch();
     t.layout = QSR_COLUMN_MAJOR;
+    t.trusted = true;
 }
 
 } // namespace qsr

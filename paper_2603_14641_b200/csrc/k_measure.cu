@@ -395,7 +395,7 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
     QSR_CUDA(cudaStreamSynchronize(t.stream)); // flags_host ready
     // Sequential collapse loop in window order (measure.hpp:409-431); device-resident
     // decisions (pivot, coin, deterministic fallback).
-    if (batch_collapses()) {
+    if (batch_collapses() && t.trusted) {
         // Batched: up to kMaxBatch consecutive flagged collapses per streaming pass.
         std::vector<uint32_t> fq, fidx;
         for (uint64_t i = 0; i < m; ++i)
