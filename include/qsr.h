@@ -166,6 +166,13 @@ qsr_status qsr_deterministic_outcome(qsr_tableau *t, uint64_t q, uint8_t *outcom
 qsr_status qsr_measure_window(qsr_tableau *t, const qsr_gate *gates, uint64_t ngates,
                               uint64_t seed, uint64_t *coin_index, qsr_record_entry *out,
                               qsr_phase_timers *timers);
+/* Same, with the coins supplied by the caller: coins[i] & 1 is the i-th coin the window may
+ * consume (the caller draws them from its own RandomStream, any stream / context; at most
+ * ngates are used, ncoins >= ngates). *used receives how many were consumed, so the caller
+ * advances its stream by exactly that many draws (measure.hpp:427). */
+qsr_status qsr_measure_window_coins(qsr_tableau *t, const qsr_gate *gates, uint64_t ngates,
+                                    const uint8_t *coins, uint64_t ncoins, uint64_t *used,
+                                    qsr_record_entry *out, qsr_phase_timers *timers);
 
 /* run_single_shot<uint64_t>(circuit, schedule, seed) (simulator.hpp:46-76).
  * schedule == NULL -> schedule_windows(circuit, single_shot). `record` must hold

@@ -1,0 +1,255 @@
+// quasar_gpu.hpp — header-only C++ drop-in for the reference's hot-path API
+// (proj/include/quasar) on the B200 engine (libqsr.so, C ABI in qsr.h).
+//
+// A reference user keeps their types (quasar::Circuit, Schedule, Window, Tableau<uint64_t>,
+// MeasurementRecord, RandomStream, ShotRecord<uint64_t>, RunReport) and swaps the namespace:
+//
+//     #include "quasar/simulator.hpp"     // reference headers (types)
+//     #include "quasar_gpu.hpp"           // this file
+//     auto r = quasar::gpu::run_single_shot<uint64_t>(circuit, seed);   // was quasar::
+//
+// Signatures, results (bit-exact) and exception types are the reference's: the C ABI status
+// is rethrown as std::invalid_argument / std::out_of_range / std::logic_error. Only the word
+// type uint64_t (the reference default) is provided. Host Tableau<uint64_t> arguments are
+// uploaded, processed on the GPU and downloaded in the reference's own storage layout.
+#ifndef QUASAR_GPU_HPP_
+#define QUASAR_GPU_HPP_
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "qsr.h"
+#include "quasar/frames.hpp"
+#include "quasar/measure.hpp"
+#include "quasar/simulator.hpp"
+
+namespace quasar::gpu {
+
+static_assert(sizeof(Gate) == sizeof(qsr_gate), "quasar::Gate must match qsr_gate (12 bytes)");
+static_assert(sizeof(MeasurementRecord::Entry) == sizeof(qsr_record_entry),
+              "MeasurementRecord::Entry must match qsr_record_entry (8 bytes)");
+
+inline void check(qsr_status st) {
+    switch (st) {
+    case QSR_OK: return;
+    case QSR_INVALID_ARGUMENT: throw std::invalid_argument(qsr_last_error());
+    case QSR_OUT_OF_RANGE: throw std::out_of_range(qsr_last_error());
+    case QSR_LOGIC_ERROR: throw std::logic_error(qsr_last_error());
+    default: throw std::runtime_error(std::string("libqsr: ") + qsr_last_error());
+    }
+}
+
+inline int& device() { // CUDA device used by the free functions below
+    static int d = 0;
+    return d;
+}
+
+namespace detail {
+struct CircuitDel { void operator()(qsr_circuit *c) const { qsr_circuit_destroy(c); } };
+struct ScheduleDel { void operator()(qsr_schedule *s) const { qsr_schedule_destroy(s); } };
+struct TableauDel { void operator()(qsr_tableau *t) const { qsr_tableau_destroy(t); } };
+struct FramesDel { void operator()(qsr_frames *f) const { qsr_frames_destroy(f); } };
+using CircuitPtr = std::unique_ptr<qsr_circuit, CircuitDel>;
+using SchedulePtr = std::unique_ptr<qsr_schedule, ScheduleDel>;
+using TableauPtr = std::unique_ptr<qsr_tableau, TableauDel>;
+using FramesPtr = std::unique_ptr<qsr_frames, FramesDel>;
+
+inline const qsr_gate *gates(const std::vector<Gate> &g) {
+    return reinterpret_cast<const qsr_gate *>(g.data());
+}
+
+inline CircuitPtr circuit(const Circuit &c) {
+    qsr_circuit *h = nullptr;
+    check(qsr_circuit_create(c.num_qubits, gates(c.gates), c.gates.size(), &h));
+    return CircuitPtr(h);
+}
+
+inline SchedulePtr schedule(const Schedule &s) {
+    std::vector<Gate> flat;
+    std::vector<uint64_t> off{0};
+    std::vector<uint8_t> meas;
+    for (const Window &w : s.windows) {
+        flat.insert(flat.end(), w.gates.begin(), w.gates.end());
+        off.push_back(flat.size());
+        meas.push_back(w.is_measurement ? 1 : 0);
+    }
+    qsr_schedule *h = nullptr;
+    check(qsr_schedule_create(gates(flat), off.data(), meas.data(), meas.size(),
+                              s.mode == ScheduleMode::sampling ? QSR_SAMPLING : QSR_SINGLE_SHOT, &h));
+    return SchedulePtr(h);
+}
+
+inline TableauPtr upload(const Tableau<uint64_t> &t) {
+    qsr_tableau *h = nullptr;
+    check(qsr_tableau_create(t.num_qubits(), device(), &h));
+    TableauPtr p(h);
+    check(qsr_tableau_upload(h, t.x_plane().data(), t.z_plane().data(), t.signs().data(),
+                             t.layout() == Layout::RowMajor ? QSR_ROW_MAJOR : QSR_COLUMN_MAJOR));
+    return p;
+}
+
+// Download into a reference Tableau (ColumnMajor results only, which is every result of the
+// functions below: run_single_shot, apply_window and measure_window all end ColumnMajor).
+inline void download(qsr_tableau *h, Tableau<uint64_t> &t) {
+    int layout = 0;
+    check(qsr_tableau_info(h, nullptr, nullptr, nullptr, &layout));
+    if (layout != QSR_COLUMN_MAJOR || t.layout() != Layout::ColumnMajor)
+        throw std::logic_error("quasar::gpu: only ColumnMajor tableaux are downloaded");
+    check(qsr_tableau_download(h, t.x_plane().data(), t.z_plane().data(), t.signs().data()));
+}
+
+inline RunReport report(const qsr_run_report &r) {
+    RunReport o;
+    o.timers.to_seconds = r.timers.to_seconds;
+    o.timers.t_seconds = r.timers.t_seconds;
+    o.timers.cmp_seconds = r.timers.cmp_seconds;
+    o.timers.ge_seconds = r.timers.ge_seconds;
+    o.gate_count = r.gate_count;
+    o.measure_count = r.measure_count;
+    o.probabilistic_count = r.probabilistic_count;
+    o.window_count = r.window_count;
+    o.total_seconds = r.total_seconds;
+    return o;
+}
+
+inline SingleShotResult<uint64_t> run(const Circuit &c, const Schedule *s, uint64_t seed) {
+    auto ch = circuit(c);
+    SchedulePtr sh;
+    if (s) sh = schedule(*s);
+    std::vector<MeasurementRecord::Entry> rec(c.measure_count());
+    qsr_run_report rep{};
+    qsr_tableau *th = nullptr;
+    check(qsr_run_single_shot(ch.get(), sh.get(), seed, device(), &th,
+                              reinterpret_cast<qsr_record_entry *>(rec.data()), &rep));
+    TableauPtr tp(th);
+    SingleShotResult<uint64_t> out{Tableau<uint64_t>(c.num_qubits), {}, {}};
+    download(th, out.tableau);
+    out.record.entries = std::move(rec);
+    out.report = report(rep);
+    return out;
+}
+} // namespace detail
+
+// run_single_shot<uint64_t>(circuit, schedule, seed)   (simulator.hpp:46-70)
+template <Word W>
+SingleShotResult<W> run_single_shot(const Circuit &circuit, const Schedule &schedule,
+                                    uint64_t seed) {
+    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
+    return detail::run(circuit, &schedule, seed);
+}
+
+// run_single_shot<uint64_t>(circuit, seed)   (simulator.hpp:72-76)
+template <Word W>
+SingleShotResult<W> run_single_shot(const Circuit &circuit, uint64_t seed) {
+    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
+    return detail::run(circuit, nullptr, seed);
+}
+
+// schedule_windows(circuit, mode)   (schedule.hpp:51-137)
+inline Schedule schedule_windows(const Circuit &circuit, ScheduleMode mode) {
+    auto ch = detail::circuit(circuit);
+    qsr_schedule *sh = nullptr;
+    check(qsr_schedule_windows(ch.get(), mode == ScheduleMode::sampling ? QSR_SAMPLING : QSR_SINGLE_SHOT, &sh));
+    detail::SchedulePtr sp(sh);
+    uint64_t nwin = 0, ng = 0;
+    check(qsr_schedule_info(sh, &nwin, &ng, nullptr));
+    const qsr_gate *g = qsr_schedule_gates(sh);
+    const uint64_t *off = qsr_schedule_offsets(sh);
+    const uint8_t *meas = qsr_schedule_is_measurement(sh);
+    Schedule s;
+    s.mode = mode;
+    s.windows.resize(nwin);
+    for (uint64_t w = 0; w < nwin; ++w) {
+        s.windows[w].is_measurement = meas[w] != 0;
+        const Gate *b = reinterpret_cast<const Gate *>(g + off[w]);
+        s.windows[w].gates.assign(b, b + (off[w + 1] - off[w]));
+    }
+    return s;
+}
+
+// generate_random(n, depth, seed, measure_prob)   (circuit.hpp:132-173)
+inline Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measure_prob) {
+    qsr_circuit *h = nullptr;
+    check(qsr_generate_random(n, depth, seed, measure_prob, &h));
+    detail::CircuitPtr p(h);
+    uint32_t nq = 0;
+    uint64_t ng = 0;
+    check(qsr_circuit_info(h, &nq, &ng, nullptr));
+    Circuit c;
+    c.num_qubits = nq;
+    c.num_clbits = nq;
+    const Gate *g = reinterpret_cast<const Gate *>(qsr_circuit_gates(h));
+    c.gates.assign(g, g + ng);
+    return c;
+}
+
+// apply_window(tableau, window)   (gates.hpp:147-197)
+inline void apply_window(Tableau<uint64_t> &t, const Window &window) {
+    if (window.is_measurement)
+        throw std::invalid_argument("apply_window: window contains measurements");
+    if (t.layout() != Layout::ColumnMajor)
+        throw std::invalid_argument("apply_window: tableau must be ColumnMajor");
+    auto h = detail::upload(t);
+    check(qsr_apply_window(h.get(), detail::gates(window.gates), window.gates.size()));
+    detail::download(h.get(), t);
+}
+
+// measure_window(t, window, rng, record, scratch, timers)   (measure.hpp:381-442). The coins
+// are drawn from the caller's RandomStream (any stream/context) and it is advanced by exactly
+// the number of probabilistic collapses, as in the reference.
+inline void measure_window(Tableau<uint64_t> &t, const Window &window, RandomStream &rng,
+                           MeasurementRecord &record, MeasureScratch<uint64_t> &,
+                           PhaseTimers *timers = nullptr) {
+    if (t.layout() != Layout::ColumnMajor)
+        throw std::invalid_argument("measure_window: tableau must be ColumnMajor");
+    if (!window.is_measurement)
+        throw std::invalid_argument("measure_window: not a measurement window");
+    RandomStream peek = rng;
+    std::vector<uint8_t> coins(window.gates.size());
+    for (auto &c : coins) c = uint8_t(peek.next_word() & 1);
+    auto h = detail::upload(t);
+    std::vector<MeasurementRecord::Entry> out(window.gates.size());
+    uint64_t used = 0;
+    qsr_phase_timers pt{};
+    check(qsr_measure_window_coins(h.get(), detail::gates(window.gates), window.gates.size(),
+                                   coins.data(), coins.size(), &used,
+                                   reinterpret_cast<qsr_record_entry *>(out.data()), &pt));
+    for (uint64_t i = 0; i < used; ++i) rng.next_word();
+    detail::download(h.get(), t);
+    record.entries.insert(record.entries.end(), out.begin(), out.end());
+    if (timers) {
+        timers->t_seconds += pt.t_seconds;
+        timers->cmp_seconds += pt.cmp_seconds;
+        timers->ge_seconds += pt.ge_seconds;
+    }
+}
+
+// sample<uint64_t>(circuit, shots, seed, report)   (frames.hpp:163-204)
+template <Word W>
+ShotRecord<W> sample(const Circuit &circuit, size_t shots, uint64_t seed, RunReport *report = nullptr) {
+    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
+    auto ch = detail::circuit(circuit);
+    qsr_frames *fh = nullptr;
+    qsr_run_report rep{};
+    check(qsr_sample(ch.get(), shots, seed, device(), &fh, &rep));
+    detail::FramesPtr fp(fh);
+    uint64_t nrows = 0, kf = 0;
+    check(qsr_frames_record(fh, &nrows, nullptr, nullptr));
+    check(qsr_frames_info(fh, nullptr, nullptr, &kf));
+    ShotRecord<uint64_t> r;
+    r.shots = shots;
+    r.kf = kf;
+    r.measured.resize(nrows);
+    r.words.resize(nrows * kf);
+    check(qsr_frames_record(fh, &nrows, r.measured.data(), r.words.data()));
+    if (report) *report = detail::report(rep);
+    return r;
+}
+
+} // namespace quasar::gpu
+
+#endif // QUASAR_GPU_HPP_

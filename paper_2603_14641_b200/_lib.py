@@ -113,6 +113,7 @@ SIGNATURES = {
     "qsr_inject_x": (i32, [P, u64]),
     "qsr_deterministic_outcome": (i32, [P, u64, pu8]),
     "qsr_measure_window": (i32, [P, P, u64, u64, pu64, P, C.POINTER(Timers_t)]),
+    "qsr_measure_window_coins": (i32, [P, P, u64, pu8, u64, pu64, P, C.POINTER(Timers_t)]),
     "qsr_run_single_shot": (i32, [P, P, u64, i32, C.POINTER(P), P, C.POINTER(Report_t)]),
     "qsr_engine_create": (i32, [P, P, i32, C.POINTER(P)]),
     "qsr_engine_run": (i32, [P, u64, pd]),

@@ -81,7 +81,7 @@ DeviceTableau::~DeviceTableau() {
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
                     (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits, (void *)ms.Vx,
                     (void *)ms.Vz, (void *)ms.vinfo, (void *)ms.bctl, (void *)ms.fq,
-                    (void *)ms.fidx})
+                    (void *)ms.fidx, (void *)ms.coin_buf})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
 }
@@ -100,7 +100,9 @@ void DeviceTableau::ensure_window_cap(uint64_t m) {
     if (ms.mqubits) QSR_CUDA(cudaFree(ms.mqubits));
     if (ms.fq) QSR_CUDA(cudaFree(ms.fq));
     if (ms.fidx) QSR_CUDA(cudaFree(ms.fidx));
+    if (ms.coin_buf) QSR_CUDA(cudaFree(ms.coin_buf));
     ms.window_cap = std::max<uint64_t>(m, 64);
+    QSR_CUDA(cudaMalloc(&ms.coin_buf, ms.window_cap));
     QSR_CUDA(cudaMalloc(&ms.flags, ms.window_cap));
     QSR_CUDA(cudaMalloc(&ms.out, ms.window_cap * sizeof(qsr_record_entry)));
     QSR_CUDA(cudaMalloc(&ms.mqubits, ms.window_cap * 4));
@@ -735,6 +737,54 @@ qsr_status qsr_measure_window(qsr_tableau *h, const qsr_gate *gates, uint64_t ng
             QSR_CUDA(cudaMemcpyAsync(out, t.ms.out, ng * sizeof(qsr_record_entry),
                                      cudaMemcpyDeviceToHost, t.stream));
         QSR_CUDA(cudaMemcpyAsync(coin_index, t.ms.coin_index, 8, cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        if (read_error_flag(t))
+            fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+        if (timers) {
+            timers->t_seconds += t_ms * 1e-3;
+            timers->ge_seconds += ge_ms * 1e-3;
+            timers->cmp_seconds += cmp_ms * 1e-3;
+        }
+    });
+}
+
+qsr_status qsr_measure_window_coins(qsr_tableau *h, const qsr_gate *gates, uint64_t ng,
+                                    const uint8_t *coins, uint64_t ncoins, uint64_t *used,
+                                    qsr_record_entry *out, qsr_phase_timers *timers) {
+    return guard([&] {
+        REQUIRE_PTR(h); REQUIRE_PTR(used);
+        if (ng) { REQUIRE_PTR(gates); REQUIRE_PTR(out); }
+        DeviceTableau &t = *h->t;
+        check_cm(t, "measure_window");
+        std::vector<uint32_t> stamp;
+        validate_window(t.n, gates, ng, true, stamp, 1);
+        // At most one coin per measurement of the window is ever drawn.
+        if (ncoins < ng) fail(QSR_INVALID_ARGUMENT, "measure_window: fewer coins than measurements");
+        if (ng) REQUIRE_PTR(coins);
+        QSR_CUDA(cudaSetDevice(t.device));
+        std::vector<uint32_t> qs(ng);
+        for (uint64_t i = 0; i < ng; ++i) qs[i] = gates[i].q0;
+        t.ensure_window_cap(ng);
+        const uint64_t zero = 0;
+        QSR_CUDA(cudaMemcpyAsync(t.ms.coin_index, &zero, 8, cudaMemcpyHostToDevice, t.stream));
+        if (ng) {
+            QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, qs.data(), ng * 4, cudaMemcpyHostToDevice, t.stream));
+            QSR_CUDA(cudaMemcpyAsync(t.ms.coin_buf, coins, ng, cudaMemcpyHostToDevice, t.stream));
+        }
+        t.ms.coin_table = t.ms.coin_buf;
+        std::vector<uint8_t> flags;
+        double t_ms = 0, ge_ms = 0, cmp_ms = 0;
+        try {
+            measure_window_device(t, ng, 0, qs, flags, timers != nullptr, &t_ms, &ge_ms, &cmp_ms);
+        } catch (...) {
+            t.ms.coin_table = nullptr;
+            throw;
+        }
+        t.ms.coin_table = nullptr;
+        if (ng)
+            QSR_CUDA(cudaMemcpyAsync(out, t.ms.out, ng * sizeof(qsr_record_entry),
+                                     cudaMemcpyDeviceToHost, t.stream));
+        QSR_CUDA(cudaMemcpyAsync(used, t.ms.coin_index, 8, cudaMemcpyDeviceToHost, t.stream));
         t.sync();
         if (read_error_flag(t))
             fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");

@@ -26,6 +26,13 @@ __device__ __forceinline__ uint64_t d_philox_word(uint64_t seed, uint32_t stream
     return (uint64_t(c1) << 32) | c0;
 }
 
+// Measurement coin number idx of the run: Philox(seed, kStreamMeasure, 0, idx) & 1
+// (measure.hpp:427, simulator.hpp:51), or bit 0 of a caller-supplied table (the C++ shim draws
+// the coins from the caller's own RandomStream, whatever its stream / context).
+__device__ __forceinline__ uint32_t draw_coin(uint64_t seed, uint64_t idx, const uint8_t *table) {
+    return table ? uint32_t(table[idx] & 1u) : uint32_t(d_philox_word(seed, 0, 0, idx) & 1u);
+}
+
 enum : uint32_t { K_X = 0, K_Y, K_Z, K_H, K_S, K_SDG, K_CX, K_CY, K_CZ, K_SWAP, K_ISWAP };
 
 __device__ __forceinline__ uint32_t gate_q0(uint64_t g) { return uint32_t(g) & 0x0FFFFFFFu; }

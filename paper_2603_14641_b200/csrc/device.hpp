@@ -49,6 +49,9 @@ struct MeasureScratch {
     uint32_t *vinfo = nullptr;      // [3*kMaxBatch]
     uint32_t *bctl = nullptr;       // [4]
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
+    // Caller-drawn coins for the current measurement window (nullptr = device Philox).
+    uint8_t *coin_table = nullptr;
+    uint8_t *coin_buf = nullptr;  // [window_cap]
 };
 
 constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)

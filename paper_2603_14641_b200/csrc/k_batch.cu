@@ -94,7 +94,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                const uint32_t *__restrict__ fidx, uint32_t b, uint64_t *__restrict__ Vx,
                uint64_t *__restrict__ Vz, uint32_t *__restrict__ vinfo, uint32_t *__restrict__ bctl,
                uint64_t seed, uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
-               int *__restrict__ err) {
+               int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
     __shared__ uint32_t s_vb[kB], s_vsign[kB], s_c[kB], s_q[kB], s_vbcol[kB], s_beta[kB];
     __shared__ uint32_t s_min, s_len;
     __shared__ int s_red[32];
@@ -177,7 +177,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             s_beta[m] = uint32_t(b_tot) & 3u;
             s_c[m] = c;
             const uint64_t idx = *coin_index;
-            const uint32_t coin = uint32_t(d_philox_word(seed, 0, 0, idx) & 1u);
+            const uint32_t coin = draw_coin(seed, idx, coin_table);
             *coin_index = idx + 1;
             out[fidx[m]] = qsr_record_entry{s_q[m], uint8_t(coin), 0};
             // signs of the replaced pair: D_c <- s(V_m), S_c <- coin
@@ -383,7 +383,7 @@ void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fid
     QSR_CUDA(cudaGetLastError());
     k_batch_pivots<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n, t.n_pad, t.s, ms.colbits,
                                              d_fq, d_fidx, b, ms.Vx, ms.Vz, ms.vinfo, ms.bctl, seed,
-                                             ms.coin_index, ms.out, ms.err);
+                                             ms.coin_index, ms.out, ms.err, ms.coin_table);
     QSR_CUDA(cudaGetLastError());
     static bool configured = false;
     if (!configured) {

@@ -214,7 +214,8 @@ k_finish(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
          uint64_t n_pad, uint64_t *__restrict__ s, uint32_t *__restrict__ ctl,
          const uint64_t *__restrict__ px, const uint64_t *__restrict__ pz,
          int64_t *__restrict__ pe, uint64_t seed, uint64_t *__restrict__ coin_index,
-         qsr_record_entry *__restrict__ out, int *__restrict__ err) {
+         qsr_record_entry *__restrict__ out, int *__restrict__ err,
+         const uint8_t *__restrict__ coin_table) {
     const uint32_t mode = ctl[CTL_MODE];
     const uint32_t q = ctl[CTL_Q];
     const uint32_t tid = threadIdx.x;
@@ -266,7 +267,7 @@ k_finish(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
         uint64_t coin = 0;
         if (mode == MODE_COLLAPSE) {
             uint64_t idx = *coin_index;
-            coin = d_philox_word(seed, 0, 0, idx) & 1;
+            coin = draw_coin(seed, idx, coin_table);
             *coin_index = idx + 1;
         }
         s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (coin << (rs & 63));
@@ -347,7 +348,7 @@ void det_partial(DeviceTableau &t) {
 void finish(DeviceTableau &t, uint64_t seed, qsr_record_entry *out) {
     k_finish<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_pad, t.s, t.ms.ctl,
                                        t.ms.partial_x, t.ms.partial_z, t.ms.partial_e, seed,
-                                       t.ms.coin_index, out, t.ms.err);
+                                       t.ms.coin_index, out, t.ms.err, t.ms.coin_table);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -573,14 +573,20 @@ def measure_window(t: Tableau, window: Window, rng: RandomStream, record: Measur
     arr, is_meas = _window_gates(window)
     if not is_meas:
         raise InvalidArgument("measure_window: not a measurement window")
-    if rng.stream != kStreamMeasure or rng.ctx != 0:
-        raise InvalidArgument("measure_window: coins must come from stream kStreamMeasure, ctx 0")
     out = np.zeros(len(arr), dtype=ENTRY_DTYPE)
-    idx = C.c_uint64(rng.index)
     ct = _lib.Timers_t() if timers is not None else None
-    check(lib.qsr_measure_window(t._h, ptr(arr), len(arr), rng.seed(), C.byref(idx), ptr(out),
-                                 C.byref(ct) if ct is not None else None))
-    rng.index = idx.value
+    if rng.stream == kStreamMeasure and rng.ctx == 0:
+        idx = C.c_uint64(rng.index)  # coins drawn on the device at the stream's position
+        check(lib.qsr_measure_window(t._h, ptr(arr), len(arr), rng.seed(), C.byref(idx), ptr(out),
+                                     C.byref(ct) if ct is not None else None))
+        rng.index = idx.value
+    else:  # any other stream: draw the window's coins here, consume exactly what was used
+        coins = np.array([Philox.word_at(rng.seed(), rng.stream, rng.ctx, rng.index + i) & 1
+                          for i in range(len(arr))], dtype=np.uint8)
+        used = C.c_uint64(0)
+        check(lib.qsr_measure_window_coins(t._h, ptr(arr), len(arr), ptr(coins, C.c_uint8), len(coins),
+                                           C.byref(used), ptr(out), C.byref(ct) if ct is not None else None))
+        rng.index += used.value
     record.entries.extend(MeasurementRecord.from_array(out).entries)
     if timers is not None:
         timers.t_seconds += ct.t_seconds
