@@ -5,11 +5,14 @@ wall-s for the 180k-qubit depth-1000 Clifford+measure circuit; HBM GB/s).
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl ours|reference]
 
 One step = one full run_single_shot of the configured circuit (every gate window, the
-transposes and every measurement collapse) on device-resident inputs. `value` is whole-job
-gates/s (all ranks), timed with CUDA events; `e2e` is the same metric through the C-ABI
-call with host buffers (schedule + upload + simulate + record and tableau download).
-N > 1 (torchrun): one process per GPU, each runs its own replica of the workload (weak
-scaling, no data-path collective); the generator-row-sharded engine is future work.
+transposes and every measurement collapse) on device-resident inputs. `value` is the circuit's
+gates/s, timed with CUDA events (max over ranks); `e2e` is the same metric through the public
+API with host buffers (schedule + upload + simulate + record and tableau download).
+N > 1 (torchrun): one process per GPU drives one generator-word shard of the SAME tableau
+(strong scaling): gate windows run shard-local, measurement windows exchange pivot blocks and
+partial products over NCCL inside libqsr (csrc/shard.cpp, csrc/exchange.cu).
+--local-shards S (N = 1): the sharded engine with all S shards on the one GPU (the
+multi-GPU protocol's overhead, measured on one device).
 """
 from __future__ import annotations
 
@@ -106,28 +109,6 @@ def gate_bytes(circuit, k: int, gate_windows: int) -> float:
     return 8.0 * 2 * k * words + 16.0 * 2 * k * gate_windows
 
 
-def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        return world, rank, local, dist
-    return 1, 0, 0, None
-
-
-def dist_max(dist, v: float, local: int) -> float:
-    if dist is None:
-        return v
-    import torch
-    t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
-
-
 def barrier(dist):
     if dist is not None:
         dist.barrier()
@@ -165,7 +146,7 @@ def run_reference_arm(args, cfg, world, rank, dist):
               f"{args.warmup} untimed, {args.steps} timed; gates/s over the timed windows")
     line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "gates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": {"workload": DESCR[args.config], "step": "one gate window (bounded CPU sample)"},
             "cpu_baseline": {"value": rate, "unit": "gates/s", "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": rate, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -183,9 +164,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--cpu-windows", type=int, default=2, help="timed CPU-baseline windows (rank 0)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--local-shards", type=int, default=1,
+                    help="N = 1 only: run the sharded engine with this many shards on the one GPU")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    world, rank, local, dist = dist_setup()
+    from paper_2603_14641_b200 import dist as qd
+    world, rank, local, dist = qd.init_from_env("nccl")
     if args.impl == "reference":
         run_reference_arm(args, cfg, world, rank, dist)
         return
@@ -203,11 +187,24 @@ def main():
     _, offs, flags = sched.arrays()
     gate_windows = int((flags == 0).sum())
     log(f"[rank {rank}] scheduled {len(flags)} windows in {time.time() - t0:.2f}s")
-    eng = q.Engine(circ, sched, device=device)
     n = cfg["n"]
     k = (n + 63) // 64
     n_pad = 64 * k
-    run_seed = cfg["run_seed"] + rank
+    run_seed = cfg["run_seed"]
+    nccl_id = qd.share_nccl_id(dist, rank) if world > 1 else None
+    shards = world if world > 1 else args.local_shards
+
+    def make_engine():
+        if world > 1:
+            return q.ShardedEngine(circ, world, device=device, exchange="nccl", rank=rank, nccl_id=nccl_id)
+        if shards > 1:
+            return q.ShardedEngine(circ, shards, device=device, exchange="local")
+        return q.Engine(circ, sched, device=device)
+
+    t0 = time.time()
+    eng = make_engine()
+    log(f"[rank {rank}] engine ({'sharded x%d' % shards if shards > 1 else 'single'}) up in {time.time() - t0:.1f}s")
+    kg_local = q.shard_range(n, world, rank)[1] if world > 1 else k
 
     for i in range(args.warmup):
         ms = eng.run(run_seed)
@@ -226,13 +223,16 @@ def main():
             log(f"[rank {rank}] step {i}: {ms:.1f} ms  {st}")
     barrier(dist)
     launches = q.launch_count() - launches0
-    total_ms = dist_max(dist, float(np.sum(step_ms)), local)
+    total_ms = qd.max_over_ranks(dist, float(np.sum(step_ms)))
     ms_per_step = total_ms / args.steps
-    value = world * G * args.steps / (total_ms * 1e-3)
+    value = G * args.steps / (total_ms * 1e-3)
 
     # Roofline of the dominant kernel (gate window): algorithmic bytes per launch over the
     # average launch duration measured above with CUDA events on the engine's stream.
-    gb = gate_bytes(circ, k, gate_windows)
+    # Per launch: one window on this process's shard (2*kg_local generator-words per qubit).
+    gb = gate_bytes(circ, kg_local, gate_windows)
+    if world == 1 and shards > 1:
+        gb = gate_bytes(circ, k, gate_windows) / shards  # mean shard (launches count all shards)
     per_launch_bytes = gb / gate_windows
     per_launch_s = (gate_ms / gate_launch) * 1e-3
     achieved = per_launch_bytes / per_launch_s / 1e9
@@ -249,8 +249,10 @@ def main():
     st = eng.stats()
     del eng
 
-    # e2e through the C ABI with host buffers: run_single_shot (schedule, validation, packed
-    # gate upload, simulation, record download) + final tableau download into pinned memory.
+    # e2e through the public API with host buffers, every step: N = 1 -> qsr_run_single_shot
+    # (schedule, validation, packed gate upload, simulation, record download) + final tableau
+    # download into pinned memory; N > 1 -> ShardedEngine create (schedule + upload per rank),
+    # run, record download and this rank's tableau columns.
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     plane = n_pad * 2 * k
     px, pz = C.c_void_p(), C.c_void_p()
@@ -262,22 +264,30 @@ def main():
     barrier(dist)
     for i in range(e2e_steps):
         t1 = time.perf_counter()
-        rep = _lib.Report_t()
-        h = C.c_void_p()
-        _lib.check(_lib.lib.qsr_run_single_shot(circ._h, None, run_seed, device, C.byref(h), _lib.ptr(rec),
-                                                C.byref(rep)))
-        _lib.check(_lib.lib.qsr_tableau_download(h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
-                                                 _lib.ptr(ps, C.c_uint64)))
-        _lib.lib.qsr_tableau_destroy(h)
+        if world > 1 or shards > 1:
+            e = make_engine()
+            e.run(run_seed)
+            _lib.check(_lib.lib.qsr_sharded_record(e._h, _lib.ptr(rec)))
+            _lib.check(_lib.lib.qsr_sharded_tableau(e._h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
+                                                    _lib.ptr(ps, C.c_uint64)))
+            del e
+        else:
+            rep = _lib.Report_t()
+            h = C.c_void_p()
+            _lib.check(_lib.lib.qsr_run_single_shot(circ._h, None, run_seed, device, C.byref(h), _lib.ptr(rec),
+                                                    C.byref(rep)))
+            _lib.check(_lib.lib.qsr_tableau_download(h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
+                                                     _lib.ptr(ps, C.c_uint64)))
+            _lib.lib.qsr_tableau_destroy(h)
         e2e_s.append(time.perf_counter() - t1)
-        log(f"[rank {rank}] e2e {i}: {e2e_s[-1]:.2f} s (device run {rep.total_seconds:.2f} s)")
+        log(f"[rank {rank}] e2e {i}: {e2e_s[-1]:.2f} s")
     barrier(dist)
     _lib.lib.qsr_host_free(px)
     _lib.lib.qsr_host_free(pz)
-    e2e_total = dist_max(dist, float(np.sum(e2e_s)), local) if e2e_steps else float("nan")
-    e2e_value = world * G * e2e_steps / e2e_total if e2e_steps else None
-    h2d = 8 * G + 4 * nm
-    d2h = 8 * nm + 2 * 8 * plane + 8 * 2 * k
+    e2e_total = qd.max_over_ranks(dist, float(np.sum(e2e_s))) if e2e_steps else float("nan")
+    e2e_value = G * e2e_steps / e2e_total if e2e_steps else None
+    h2d = world * (8 * G + 4 * nm)
+    d2h = world * 8 * nm + 2 * 8 * plane + 8 * 2 * k
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -295,11 +305,13 @@ def main():
         return
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
         "config": {"workload": DESCR[args.config], "qubits": n, "depth": cfg["depth"], "gates": G,
                    "measurements": nm, "windows": int(len(flags)), "gate_windows": gate_windows,
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"generator-row shards x{world} (NCCL)" if world > 1 else
+                                   f"generator-row shards x{shards} on one GPU (local exchange)"
+                                   if shards > 1 else "single GPU"),
                    "l2": "inputs larger than L2 (tableau 16.2 GB vs 126 MB L2); no flush needed"},
         "wall_s_per_step": ms_per_step / 1e3,
         "phase_ms_per_step": {"gate_windows": gate_ms / args.steps, "transpose": st["transpose_ms"],

@@ -219,6 +219,50 @@ void qsr_frames_destroy(qsr_frames *f);
  * frames object's ShotRecord. */
 qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
                       qsr_frames **out, qsr_run_report *report);
+/* sample<uint64_t> sharded by shot: this call computes shot-words
+ * [w0, w0+nw) of ceil(shots/64), w0 = kf*rank/world, on `device` (one process per GPU; no
+ * communication: the Philox key (q<<24)|j of frames.hpp:63 uses the global word j). The
+ * reference shot runs on every rank. The record rows hold nw words each; concatenating the
+ * ranks' rows word-wise gives sample()'s ShotRecord exactly. */
+qsr_status qsr_sample_shard(const qsr_circuit *c, uint64_t shots, uint64_t seed, int world,
+                            int rank, int device, qsr_frames **out, qsr_run_report *report);
+/* Global shot-word slice [j0, j0+nw) held by a frames object (j0 = 0, nw = kf unsharded). */
+qsr_status qsr_frames_shot_words(const qsr_frames *f, uint64_t *j0, uint64_t *nw);
+
+/* ---- generator-row-sharded engine (multi-GPU run_single_shot) ------
+ * The tableau is split by generator-words: shard r of `world` holds generator-words
+ * [j0, j0+kg) of both halves (destabilizers and stabilizers g = 64*j0 .. 64*(j0+kg)-1) for
+ * all qubits. Gate windows run shard-local with no communication; a measurement window
+ * exchanges a pivot-leader mask (all-gather of 4 B per shard), the batch's pivot rows
+ * (broadcast from the shard holding them), deterministic partial products (all-gather)
+ * and the window's flags / record (max-all-reduce). Results are bit-identical to
+ * run_single_shot<uint64_t> (simulator.hpp:46-76) for every world size. */
+enum { QSR_EXCHANGE_LOCAL = 0, QSR_EXCHANGE_NCCL = 1 };
+typedef struct qsr_shard_config {
+    int world;              /* number of shards (1 <= world <= ceil(n/64)) */
+    int rank;               /* NCCL: the shard this process drives; LOCAL: ignored */
+    int device;             /* CUDA device of this process's shard(s) */
+    int exchange;           /* QSR_EXCHANGE_LOCAL: all shards in this process on `device`;
+                               QSR_EXCHANGE_NCCL: one process per shard (collective create) */
+    const uint8_t *nccl_id; /* 128-byte ncclUniqueId shared by all ranks (NCCL only) */
+} qsr_shard_config;
+typedef struct qsr_sharded qsr_sharded;
+/* Shard r's generator-word range for n qubits (host only, no device needed). */
+qsr_status qsr_shard_range(uint64_t n, int world, int rank, uint64_t *j0, uint64_t *kg);
+/* ncclGetUniqueId (rank 0 creates it, the host rendezvous hands it to every rank). */
+qsr_status qsr_nccl_unique_id(uint8_t out[128]);
+qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
+                              const qsr_shard_config *cfg, qsr_sharded **out);
+/* One full single-shot pass (collective); *device_ms = CUDA-event time of this process. */
+qsr_status qsr_sharded_run(qsr_sharded *e, uint64_t seed, double *device_ms);
+qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *gate_launches,
+                             double *transpose_ms, double *measure_ms, uint64_t *launches);
+/* The full measurement record (identical on every rank). */
+qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record);
+/* Writes the generator-word columns of this process's shards into full-size reference-layout
+ * CM buffers (x, z: n_pad*2k words; s: 2k words); other columns are left untouched. */
+qsr_status qsr_sharded_tableau(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s);
+void qsr_sharded_destroy(qsr_sharded *e);
 
 #ifdef __cplusplus
 }

@@ -64,6 +64,13 @@ class Report_t(C.Structure):
                 ("total_seconds", C.c_double)]
 
 
+class ShardConfig_t(C.Structure):
+    _fields_ = [("world", C.c_int), ("rank", C.c_int), ("device", C.c_int), ("exchange", C.c_int),
+                ("nccl_id", C.POINTER(C.c_uint8))]
+
+
+EXCHANGE_LOCAL, EXCHANGE_NCCL = 0, 1
+
 GATE_DTYPE = np.dtype({"names": ["kind", "q0", "q1"], "formats": ["u1", "<u4", "<u4"],
                        "offsets": [0, 4, 8], "itemsize": 12})
 ENTRY_DTYPE = np.dtype({"names": ["qubit", "outcome", "deterministic"], "formats": ["<u4", "u1", "u1"],
@@ -130,6 +137,16 @@ SIGNATURES = {
     "qsr_frames_record": (i32, [P, pu64, pu32, pu64]),
     "qsr_frames_destroy": (None, [P]),
     "qsr_sample": (i32, [P, u64, u64, i32, C.POINTER(P), C.POINTER(Report_t)]),
+    "qsr_sample_shard": (i32, [P, u64, u64, i32, i32, i32, C.POINTER(P), C.POINTER(Report_t)]),
+    "qsr_frames_shot_words": (i32, [P, pu64, pu64]),
+    "qsr_shard_range": (i32, [u64, i32, i32, pu64, pu64]),
+    "qsr_nccl_unique_id": (i32, [pu8]),
+    "qsr_sharded_create": (i32, [P, P, C.POINTER(ShardConfig_t), C.POINTER(P)]),
+    "qsr_sharded_run": (i32, [P, u64, pd]),
+    "qsr_sharded_stats": (i32, [P, pd, pu64, pd, pd, pu64]),
+    "qsr_sharded_record": (i32, [P, P]),
+    "qsr_sharded_tableau": (i32, [P, pu64, pu64, pu64]),
+    "qsr_sharded_destroy": (None, [P]),
 }
 
 

@@ -8,16 +8,16 @@
 #include <string>
 #include <unordered_map>
 
-#include "device.hpp"
+#include "abi.hpp"
+#include "engine.hpp"
 
 using namespace qsr;
 
-struct qsr_circuit : Circuit {};
-struct qsr_schedule : Schedule {};
 
 namespace qsr {
 
 uint64_t g_launches = 0;
+thread_local std::string g_err;
 
 void cuda_check(cudaError_t e, const char *what) {
     if (e == cudaSuccess) return;
@@ -27,15 +27,20 @@ void cuda_check(cudaError_t e, const char *what) {
     fail(QSR_CUDA_ERROR, m);
 }
 
-DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
+DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : device(dev), n(n_) {
     if (n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "Tableau: n exceeds the supported maximum");
     QSR_CUDA(cudaSetDevice(device));
     k = (n + 63) / 64;
     n_pad = 64 * k;
-    cm_pitch = round_up(2 * k, 16);
+    kg = kg_ ? kg_ : k;
+    if (j0 + kg > k) fail(QSR_INVALID_ARGUMENT, "Tableau: generator shard out of range");
+    g0 = 64 * j0;
+    ng = 64 * kg;
+    n_gen = std::min<uint64_t>(ng, n > g0 ? n - g0 : 0);
+    cm_pitch = round_up(2 * kg, 16);
     rm_pitch = round_up(k, 16);
-    plane_words = std::max(n_pad * cm_pitch, 2 * n_pad * rm_pitch);
+    plane_words = std::max(n_pad * cm_pitch, 2 * ng * rm_pitch);
     cudaDeviceProp prop;
     QSR_CUDA(cudaGetDeviceProperties(&prop, device));
     num_sms = prop.multiProcessorCount;
@@ -51,8 +56,8 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
     alloc(&s, cm_pitch);
     QSR_CUDA(cudaMalloc(&tile_counters, (cm_pitch / 64 + 2) * 4));
     QSR_CUDA(cudaMemsetAsync(tile_counters, 0, (cm_pitch / 64 + 2) * 4, stream));
-    alloc(&ms.mask, 2 * k + 2);
-    QSR_CUDA(cudaMalloc(&ms.rows, 2 * n_pad * 4));
+    alloc(&ms.mask, 2 * kg + 2);
+    QSR_CUDA(cudaMalloc(&ms.rows, 2 * ng * 4));
     QSR_CUDA(cudaMalloc(&ms.ctl, 64));
     QSR_CUDA(cudaMemsetAsync(ms.ctl, 0, 64, stream));
     alloc(&ms.partial_x, 128 * rm_pitch);
@@ -63,11 +68,18 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev) : device(dev), n(n_) {
     QSR_CUDA(cudaMemsetAsync(ms.coin_index, 0, 8, stream));
     QSR_CUDA(cudaMalloc(&ms.err, 4));
     QSR_CUDA(cudaMemsetAsync(ms.err, 0, 4, stream));
-    QSR_CUDA(cudaMalloc(&ms.colbits, 2 * n_pad * 4));
-    alloc(&ms.Vx, uint64_t(kMaxBatch) * rm_pitch);
-    alloc(&ms.Vz, uint64_t(kMaxBatch) * rm_pitch);
-    QSR_CUDA(cudaMalloc(&ms.vinfo, 4 * kMaxBatch * 4));
-    QSR_CUDA(cudaMalloc(&ms.bctl, 16));
+    QSR_CUDA(cudaMalloc(&ms.colbits, 2 * ng * 4));
+    {
+        const uint64_t vwords = uint64_t(kMaxBatch) * 2 * rm_pitch;
+        const uint64_t info_words = (4 * kMaxBatch + 4) / 2;
+        ms.batch_block_bytes = (vwords + info_words) * 8;
+        alloc(&ms.batch_block, vwords + info_words);
+        ms.Vx = ms.batch_block;
+        ms.Vz = ms.batch_block + rm_pitch;
+        ms.vstride = 2 * rm_pitch;
+        ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
+        ms.bctl = ms.vinfo + 4 * kMaxBatch;
+    }
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
 }
@@ -79,8 +91,8 @@ DeviceTableau::~DeviceTableau() {
                     (void *)tile_counters, (void *)gate_buf, (void *)ms.mask, (void *)ms.rows,
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
-                    (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits, (void *)ms.Vx,
-                    (void *)ms.Vz, (void *)ms.vinfo, (void *)ms.bctl, (void *)ms.fq,
+                    (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits,
+                    (void *)ms.batch_block, (void *)ms.fq,
                     (void *)ms.fidx, (void *)ms.coin_buf})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -120,30 +132,6 @@ struct qsr_tableau {
 
 namespace {
 
-thread_local std::string g_err;
-
-template <typename F>
-qsr_status guard(F &&f) {
-    try {
-        f();
-        return QSR_OK;
-    } catch (const Error &e) {
-        g_err = e.what();
-        return e.status;
-    } catch (const std::bad_alloc &) {
-        g_err = "host allocation failed";
-        return QSR_OUT_OF_MEMORY;
-    } catch (const std::exception &e) {
-        g_err = e.what();
-        return QSR_INTERNAL;
-    }
-}
-
-#define REQUIRE_PTR(p)                                                                      \
-    do {                                                                                    \
-        if (!(p)) fail(QSR_INVALID_ARGUMENT, #p " must not be NULL");                       \
-    } while (0)
-
 void check_cm(const DeviceTableau &t, const char *who) {
     if (t.layout != QSR_COLUMN_MAJOR)
         fail(QSR_INVALID_ARGUMENT, std::string(who) + ": tableau must be ColumnMajor");
@@ -157,230 +145,6 @@ std::vector<uint64_t> pack(const qsr_gate *g, uint64_t n) {
     std::vector<uint64_t> v(n);
     for (uint64_t i = 0; i < n; ++i) v[i] = pack_gate(g[i]);
     return v;
-}
-
-uint64_t host_bit(const std::vector<uint64_t> &s, uint64_t word, uint64_t bit) {
-    return (s[word] >> bit) & 1;
-}
-
-// Device-resident schedule: packed gates + per-window measured qubits.
-struct DeviceSchedule {
-    int device = 0;
-    uint64_t *d_gates = nullptr;
-    std::vector<uint64_t> offsets;
-    std::vector<uint8_t> is_meas;
-    std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
-    uint64_t measure_count = 0, unitary_count = 0;
-    ~DeviceSchedule() {
-        if (d_gates) { cudaSetDevice(device); cudaFree(d_gates); }
-    }
-};
-
-std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
-                                                cudaStream_t st) {
-    // Validate every window first (apply_window / measure_window checks, gates.hpp:149-165,
-    // measure.hpp:385-398) so no device state is touched by a schedule that would throw.
-    std::vector<uint32_t> stamp(n, 0);
-    const uint64_t W = s.num_windows();
-    for (uint64_t w = 0; w < W; ++w)
-        validate_window(n, s.gates.data() + s.offsets[w], s.offsets[w + 1] - s.offsets[w],
-                        s.is_meas[w] != 0, stamp, uint32_t(w + 1));
-    auto ds = std::make_unique<DeviceSchedule>();
-    ds->device = device;
-    ds->offsets = s.offsets;
-    ds->is_meas = s.is_meas;
-    ds->mqubits.resize(W);
-    for (uint64_t w = 0; w < W; ++w) {
-        if (!s.is_meas[w]) {
-            ds->unitary_count += s.offsets[w + 1] - s.offsets[w];
-            continue;
-        }
-        for (uint64_t i = s.offsets[w]; i < s.offsets[w + 1]; ++i)
-            ds->mqubits[w].push_back(s.gates[i].q0);
-        ds->measure_count += ds->mqubits[w].size();
-    }
-    const uint64_t G = s.gates.size();
-    QSR_CUDA(cudaSetDevice(device));
-    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
-    if (G) {
-        // Pack + upload in 32 Mi-gate slabs through pinned staging.
-        const uint64_t slab = uint64_t(1) << 25;
-        uint64_t *pinned = nullptr;
-        QSR_CUDA(cudaMallocHost(&pinned, std::min(G, slab) * 8 * 2));
-        uint64_t *buf[2] = {pinned, pinned + std::min(G, slab)};
-        int cur = 0;
-        for (uint64_t b = 0; b < G; b += slab, cur ^= 1) {
-            uint64_t e = std::min(G, b + slab);
-            QSR_CUDA(cudaStreamSynchronize(st)); // previous use of buf[cur] finished
-            for (uint64_t i = b; i < e; ++i) buf[cur][i - b] = pack_gate(s.gates[i]);
-            QSR_CUDA(cudaMemcpyAsync(ds->d_gates + b, buf[cur], (e - b) * 8,
-                                     cudaMemcpyHostToDevice, st));
-        }
-        QSR_CUDA(cudaStreamSynchronize(st));
-        QSR_CUDA(cudaFreeHost(pinned));
-    }
-    return ds;
-}
-
-// Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
-// parallel stable scatter straight into packed device words, then one upload. Windows built
-// by the plan are operand-disjoint by construction; the only error the reference would raise
-// later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
-std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st) {
-    WindowPlan p = plan_windows(c);
-    if (p.duplicate_measure)
-        fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
-    const uint64_t G = c.gates.size();
-    std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
-    scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
-    auto ds = std::make_unique<DeviceSchedule>();
-    ds->device = device;
-    ds->offsets = std::move(p.offsets);
-    ds->is_meas = std::move(p.is_meas);
-    const uint64_t W = ds->is_meas.size();
-    ds->mqubits.resize(W);
-    for (uint64_t w = 0; w < W; ++w) {
-        const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
-        if (!ds->is_meas[w]) {
-            ds->unitary_count += e - b;
-            continue;
-        }
-        for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(uint32_t(packed[i] & 0x0FFFFFFFu));
-        ds->measure_count += e - b;
-    }
-    QSR_CUDA(cudaSetDevice(device));
-    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
-    if (G) {
-        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
-        QSR_CUDA(cudaStreamSynchronize(st));
-    }
-    return ds;
-}
-
-struct RunTimes {
-    double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
-    uint64_t gate_windows = 0;
-};
-
-// The single-shot driver on device-resident inputs (simulator.hpp:46-70). `record` is a
-// device array of measure_count entries.
-void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
-                qsr_record_entry *d_record, RunTimes &rt) {
-    cudaEvent_t e_start, e_end, a, b;
-    QSR_CUDA(cudaEventCreate(&e_start));
-    QSR_CUDA(cudaEventCreate(&e_end));
-    QSR_CUDA(cudaEventCreate(&a));
-    QSR_CUDA(cudaEventCreate(&b));
-    QSR_CUDA(cudaEventRecord(e_start, t.stream));
-    launch_zero_state(t, nullptr);
-    QSR_CUDA(cudaMemsetAsync(t.ms.coin_index, 0, 8, t.stream));
-    const uint64_t W = ds.is_meas.size();
-    uint64_t rec_off = 0;
-    std::vector<uint8_t> flags;
-    uint64_t w = 0;
-    while (w < W) {
-        if (!ds.is_meas[w]) {
-            // A maximal run of unitary windows, bracketed by one event pair (TO bucket).
-            QSR_CUDA(cudaEventRecord(a, t.stream));
-            for (; w < W && !ds.is_meas[w]; ++w) {
-                launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
-                ++rt.gate_windows;
-            }
-            QSR_CUDA(cudaEventRecord(b, t.stream));
-            QSR_CUDA(cudaEventSynchronize(b));
-            float ms = 0;
-            QSR_CUDA(cudaEventElapsedTime(&ms, a, b));
-            rt.to_ms += ms;
-            continue;
-        }
-        const auto &mq = ds.mqubits[w];
-        const uint64_t m = mq.size();
-        t.ensure_window_cap(m);
-        QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
-        measure_window_device(t, m, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
-        QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, m * sizeof(qsr_record_entry),
-                                 cudaMemcpyDeviceToDevice, t.stream));
-        rec_off += m;
-        ++w;
-    }
-    QSR_CUDA(cudaEventRecord(e_end, t.stream));
-    QSR_CUDA(cudaEventSynchronize(e_end));
-    float total = 0;
-    QSR_CUDA(cudaEventElapsedTime(&total, e_start, e_end));
-    rt.total_ms = total;
-    for (auto e : {e_start, e_end, a, b}) cudaEventDestroy(e);
-    if (read_error_flag(t))
-        fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
-}
-
-void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
-                 const std::vector<qsr_record_entry> &record, double total_s) {
-    if (!rep) return;
-    rep->timers.to_seconds = rt.to_ms * 1e-3;
-    rep->timers.t_seconds = rt.t_ms * 1e-3;
-    rep->timers.cmp_seconds = rt.cmp_ms * 1e-3;
-    rep->timers.ge_seconds = rt.ge_ms * 1e-3;
-    rep->gate_count = ds.unitary_count;
-    rep->measure_count = ds.measure_count;
-    rep->window_count = ds.is_meas.size();
-    rep->probabilistic_count = 0;
-    for (const auto &e : record) rep->probabilistic_count += e.deterministic ? 0 : 1;
-    rep->total_seconds = total_s;
-}
-
-// Host reference-layout <-> device layout conversion.
-void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout) {
-    if (layout == QSR_COLUMN_MAJOR) {
-        if (t.layout != QSR_COLUMN_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
-        QSR_CUDA(cudaMemcpy2DAsync(t.x, t.cm_pitch * 8, x, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
-                                   cudaMemcpyHostToDevice, t.stream));
-        QSR_CUDA(cudaMemcpy2DAsync(t.z, t.cm_pitch * 8, z, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
-                                   cudaMemcpyHostToDevice, t.stream));
-        t.layout = QSR_COLUMN_MAJOR;
-    } else {
-        if (t.layout != QSR_ROW_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
-        // Reference RM: word (i, col) at i*2n_pad + col  ->  internal row col, word i.
-        const uint64_t R = 2 * t.n_pad, K = t.k;
-        std::vector<uint64_t> tmp(R * K);
-        for (int plane = 0; plane < 2; ++plane) {
-            const uint64_t *src = plane ? z : x;
-            for (uint64_t i = 0; i < K; ++i)
-                for (uint64_t c = 0; c < R; ++c) tmp[c * K + i] = src[i * R + c];
-            QSR_CUDA(cudaMemcpy2DAsync(plane ? t.z : t.x, t.rm_pitch * 8, tmp.data(), K * 8, K * 8,
-                                       R, cudaMemcpyHostToDevice, t.stream));
-            QSR_CUDA(cudaStreamSynchronize(t.stream));
-        }
-        t.layout = QSR_ROW_MAJOR;
-    }
-}
-
-void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z) {
-    if (t.layout == QSR_COLUMN_MAJOR) {
-        if (x) QSR_CUDA(cudaMemcpy2DAsync(x, 2 * t.k * 8, t.x, t.cm_pitch * 8, 2 * t.k * 8, t.n_pad,
-                                          cudaMemcpyDeviceToHost, t.stream));
-        if (z) QSR_CUDA(cudaMemcpy2DAsync(z, 2 * t.k * 8, t.z, t.cm_pitch * 8, 2 * t.k * 8, t.n_pad,
-                                          cudaMemcpyDeviceToHost, t.stream));
-        t.sync();
-        return;
-    }
-    const uint64_t R = 2 * t.n_pad, K = t.k;
-    std::vector<uint64_t> tmp(R * K);
-    for (int plane = 0; plane < 2; ++plane) {
-        uint64_t *dst = plane ? z : x;
-        if (!dst) continue;
-        QSR_CUDA(cudaMemcpy2DAsync(tmp.data(), K * 8, plane ? t.z : t.x, t.rm_pitch * 8, K * 8, R,
-                                   cudaMemcpyDeviceToHost, t.stream));
-        t.sync();
-        for (uint64_t c = 0; c < R; ++c)
-            for (uint64_t i = 0; i < K; ++i) dst[i * R + c] = tmp[c * K + i];
-    }
-}
-
-std::vector<uint64_t> download_signs(DeviceTableau &t) {
-    std::vector<uint64_t> s(2 * t.k);
-    QSR_CUDA(cudaMemcpyAsync(s.data(), t.s, 2 * t.k * 8, cudaMemcpyDeviceToHost, t.stream));
-    t.sync();
-    return s;
 }
 
 // One RM word of the X plane (row r, qubit-word i).
@@ -682,7 +446,7 @@ qsr_status qsr_swap_anti_commuting(qsr_tableau *h, uint64_t p, uint64_t q) {
         check_rm(t, "swap_anti_commuting");
         if (p >= t.n || q >= t.n) fail(QSR_OUT_OF_RANGE, "swap_anti_commuting: index out of range");
         QSR_CUDA(cudaSetDevice(t.device));
-        uint64_t w = rm_word_x(t, t.n_pad + p, q / 64);
+        uint64_t w = rm_word_x(t, t.ng + p, q / 64);
         if (!((w >> (q % 64)) & 1))
             fail(QSR_INVALID_ARGUMENT, "swap_anti_commuting: stabilizer p commutes with Z_q");
         rm_swap_anti_commuting(t, p, q);
@@ -697,7 +461,7 @@ qsr_status qsr_inject_x(qsr_tableau *h, uint64_t p) {
         DeviceTableau &t = *h->t;
         if (p >= t.n) fail(QSR_OUT_OF_RANGE, "inject_x: index out of range");
         QSR_CUDA(cudaSetDevice(t.device));
-        flip_sign_bit(t, t.k + p / 64, p % 64);
+        flip_sign_bit(t, t.kg + p / 64, p % 64);
         t.sync();
     });
 }
@@ -915,7 +679,8 @@ struct qsr_frames {
     int device = 0;
     cudaStream_t stream = nullptr;
     int num_sms = 148;
-    uint64_t n = 0, shots = 0, kf = 0, pitch = 0;
+    uint64_t n = 0, shots = 0, kf = 0, pitch = 0; // kf: shot-words held here
+    uint64_t j0 = 0;                                // global index of the first one
     uint64_t *xf = nullptr, *zf = nullptr;
     uint64_t *rec = nullptr;  // record rows [cap][pitch]
     uint64_t rec_cap = 0;
@@ -956,7 +721,8 @@ struct qsr_frames {
 
 namespace {
 
-std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device) {
+std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
+                                        uint64_t j0 = 0, uint64_t nw = 0) {
     if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "init_frames: n exceeds the supported maximum");
     auto f = std::make_unique<qsr_frames>();
@@ -968,7 +734,9 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
     f->n = n;
     f->shots = shots;
-    f->kf = (shots + 63) / 64;
+    f->kf = nw ? nw : (shots + 63) / 64;
+    f->j0 = j0;
+    if (f->j0 + f->kf > (shots + 63) / 64) fail(QSR_INVALID_ARGUMENT, "init_frames: shot slice out of range");
     f->pitch = round_up(f->kf, 16);
     uint64_t words = std::max<uint64_t>(n, 1) * f->pitch;
     QSR_CUDA(cudaMalloc(&f->xf, words * 8));
@@ -976,7 +744,7 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     QSR_CUDA(cudaMemsetAsync(f->xf, 0, words * 8, f->stream));
     QSR_CUDA(cudaMemsetAsync(f->zf, 0, words * 8, f->stream));
     f->row_of.assign(n, -1);
-    if (n) launch_frames_init(f->zf, n, f->kf, f->pitch, shots, seed, 0, nullptr, f->stream);
+    if (n) launch_frames_init(f->zf, n, f->kf, f->j0, f->pitch, shots, seed, 0, f->stream);
     return f;
 }
 
@@ -999,7 +767,7 @@ void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t 
     f.ensure_rows(f.measured.size());
     f.ensure_idx(ng);
     QSR_CUDA(cudaMemcpyAsync(f.d_idx, idx.data(), 2 * ng * 4, cudaMemcpyHostToDevice, f.stream));
-    launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
+    launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.j0, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
                           seed, epoch, f.stream);
     QSR_CUDA(cudaStreamSynchronize(f.stream)); // idx staging reused next call
 }
@@ -1037,6 +805,14 @@ qsr_status qsr_frames_info(const qsr_frames *f, uint64_t *n, uint64_t *shots, ui
         if (n) *n = f->n;
         if (shots) *shots = f->shots;
         if (kf) *kf = f->kf;
+    });
+}
+
+qsr_status qsr_frames_shot_words(const qsr_frames *f, uint64_t *j0, uint64_t *nw) {
+    return guard([&] {
+        REQUIRE_PTR(f);
+        if (j0) *j0 = f->j0;
+        if (nw) *nw = f->kf;
     });
 }
 
@@ -1114,11 +890,17 @@ qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *mea
 
 void qsr_frames_destroy(qsr_frames *f) { delete f; }
 
-qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
-                      qsr_frames **out, qsr_run_report *report) {
+static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device, int world,
+                       int rank, qsr_frames **out, qsr_run_report *report) {
     return guard([&] {
         auto wall0 = std::chrono::steady_clock::now();
         REQUIRE_PTR(c); REQUIRE_PTR(out);
+        if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
+        const uint64_t kf_all = (shots + 63) / 64;
+        if (world < 1 || uint64_t(world) > kf_all || rank < 0 || rank >= world)
+            fail(QSR_INVALID_ARGUMENT, "sample: world must be in [1, ceil(shots/64)], 0 <= rank < world");
+        const uint64_t w0 = kf_all * uint64_t(rank) / uint64_t(world);
+        const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
         Schedule sched = schedule_windows(*c, QSR_SAMPLING);
         // Reference shot (frames.hpp:167): the full single-shot pipeline on the device.
         DeviceTableau t(c->num_qubits, device);
@@ -1144,7 +926,7 @@ qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int d
             fill_report(report, rt, *ds, ref, wall);
         }
         // Frames over the same device-resident schedule (frames.hpp:171-181).
-        auto f = make_frames(c->num_qubits, shots, seed, device);
+        auto f = make_frames(c->num_qubits, shots, seed, device, w0, nw);
         QSR_CUDA(cudaStreamSynchronize(t.stream));
         uint32_t epoch = 1;
         for (uint64_t w = 0; w < ds->is_meas.size(); ++w) {
@@ -1163,12 +945,22 @@ qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int d
             f->ensure_idx(flip_rows.size());
             QSR_CUDA(cudaMemcpyAsync(f->d_idx, flip_rows.data(), flip_rows.size() * 4,
                                      cudaMemcpyHostToDevice, f->stream));
-            launch_record_fold(f->rec, f->pitch, f->kf, f->shots, f->d_idx, flip_rows.size(),
+            launch_record_fold(f->rec, f->pitch, f->kf, f->j0, f->shots, f->d_idx, flip_rows.size(),
                                f->stream);
         }
         QSR_CUDA(cudaStreamSynchronize(f->stream));
         *out = f.release();
     });
+}
+
+qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
+                      qsr_frames **out, qsr_run_report *report) {
+    return sample_impl(c, shots, seed, device, 1, 0, out, report);
+}
+
+qsr_status qsr_sample_shard(const qsr_circuit *c, uint64_t shots, uint64_t seed, int world, int rank,
+                            int device, qsr_frames **out, qsr_run_report *report) {
+    return sample_impl(c, shots, seed, device, world, rank, out, report);
 }
 
 } // extern "C"

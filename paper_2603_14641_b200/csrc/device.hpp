@@ -29,6 +29,8 @@ inline void count_launch(uint64_t n = 1) { g_launches += n; }
 
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
+constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
+
 // Scratch used by the measurement pipeline; sized for one tableau.
 struct MeasureScratch {
     uint64_t *mask = nullptr;       // 2k mask words (column bits of all rows)
@@ -44,24 +46,37 @@ struct MeasureScratch {
     int *err = nullptr;             // odd-phase detector
     uint64_t window_cap = 0;
     // batched collapses (k_batch.cu)
-    uint32_t *colbits = nullptr;    // [2*n_pad] column bits at the batch's qubits
-    uint64_t *Vx = nullptr, *Vz = nullptr; // [kMaxBatch][rm_pitch] pivot rows
-    uint32_t *vinfo = nullptr;      // [3*kMaxBatch]
-    uint32_t *bctl = nullptr;       // [4]
+    uint32_t *colbits = nullptr;    // [2*ng] column bits at the batch's qubits
+    // One contiguous batch block (broadcast as a unit by the sharded engine):
+    //   V rows  [kMaxBatch][2][rm_pitch] (x words then z words of pivot row m)
+    //   vinfo   [4*kMaxBatch] u32, bctl [4] u32 (len, stopped, stabilizer OR-mask, -)
+    uint64_t *batch_block = nullptr;
+    uint64_t batch_block_bytes = 0;
+    uint64_t *Vx = nullptr, *Vz = nullptr; // views into batch_block, row stride vstride
+    uint64_t vstride = 0;
+    uint32_t *vinfo = nullptr;
+    uint32_t *bctl = nullptr;
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
     // Caller-drawn coins for the current measurement window (nullptr = device Philox).
     uint8_t *coin_table = nullptr;
     uint8_t *coin_buf = nullptr;  // [window_cap]
 };
 
-constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
 
+// One tableau, or one generator-word shard of it: the shard holds generator
+// words [j0, j0+kg) of both halves (destabilizers g and stabilizers g for the same g), for all
+// n_pad qubits. Unsharded: j0 = 0, kg = k. CM columns = 2kg local generator-words; RM rows =
+// 2ng local generator rows (ng = 64kg; stabilizer row offset ng), each k qubit-words long.
 struct DeviceTableau {
     int device = 0;
     cudaStream_t stream = nullptr;
-    uint64_t n = 0, k = 0, n_pad = 0;
+    uint64_t n = 0, k = 0, n_pad = 0; // qubits, qubit-words, CM rows (64k)
+    uint64_t kg = 0;                  // generator-words held (per half)
+    uint64_t g0 = 0;                  // global index of the first generator held (64*j0)
+    uint64_t ng = 0;                  // 64*kg generator rows per half
+    uint64_t n_gen = 0;               // valid generators held: clamp(n - g0, 0, ng)
     uint64_t cm_pitch = 0, rm_pitch = 0;
-    uint64_t plane_words = 0;        // max(n_pad*cm_pitch, 2*n_pad*rm_pitch)
+    uint64_t plane_words = 0;        // max(n_pad*cm_pitch, 2*ng*rm_pitch)
     uint64_t *x = nullptr, *z = nullptr;   // current planes
     uint64_t *x2 = nullptr, *z2 = nullptr; // transpose targets
     uint64_t *s = nullptr;                 // signs (cm_pitch words)
@@ -79,7 +94,7 @@ struct DeviceTableau {
     MeasureScratch ms;
     int num_sms = 148;
 
-    DeviceTableau(uint64_t n, int device);
+    DeviceTableau(uint64_t n, int device, uint64_t j0 = 0, uint64_t kg = 0);
     ~DeviceTableau();
     void ensure_gate_buf(uint64_t ngates);
     void ensure_window_cap(uint64_t m);
@@ -109,6 +124,24 @@ void configure_measure_kernels(DeviceTableau &t);
 // the batch stopped at a measurement that became deterministic (k_batch.cu).
 void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
                    uint64_t seed, uint32_t &done, bool &det);
+// The three phases of measure_batch, separately (the sharded engine exchanges between them):
+// column bits + stabilizer OR-mask (bctl[2]); pivots / V rows / coins / record (leader
+// shard only); every row absorbs its V's.
+void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b);
+void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
+                  uint64_t seed);
+void batch_apply(DeviceTableau &t);
+// Deterministic outcome of measuring q (measure.hpp:343-376), sharded form: this shard's
+// ordered partial product is written to `slot` ([x: rm_pitch][z: rm_pitch][e: 16 words]);
+// det_combine folds `nslots` slots (in shard order, stride det_slot_words) into the outcome,
+// written to *out (deterministic entry) and ctl.
+uint64_t det_slot_words(const DeviceTableau &t);
+void det_local_partial(DeviceTableau &t, uint64_t q, uint64_t *slot);
+void det_combine(DeviceTableau &t, uint64_t q, const uint64_t *slots, uint32_t nslots,
+                 qsr_record_entry *out);
+// Probabilistic flags of a measurement window on this tableau/shard (find_probabilistic,
+// measure.hpp:104-126) into t.ms.flags (device; m bytes).
+void flags_cm(DeviceTableau &t, uint64_t m);
 // API-parity kernels on an RM tableau.
 void rm_column_mask(DeviceTableau &t, uint64_t q);          // fills t.ms.mask
 void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries, uint64_t &count);
@@ -120,15 +153,15 @@ void rm_find_probabilistic(DeviceTableau &t, const std::vector<uint32_t> &qubits
 void flip_sign_bit(DeviceTableau &t, uint64_t word, uint64_t bit);
 int read_error_flag(DeviceTableau &t); // syncs; returns and clears
 
-// Frames kernels.
-void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t pitch, uint64_t shots,
-                        uint64_t seed, uint32_t epoch, const uint32_t *qubits /*nullable*/,
-                        cudaStream_t st);
-void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf,
+// Frames kernels. A frames object may hold a slice of the shot-words: kf words starting at
+// global word j0 (sampling sharded by shot); `shots` is the global count.
+void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t j0, uint64_t pitch,
+                        uint64_t shots, uint64_t seed, uint32_t epoch, cudaStream_t st);
+void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf, uint64_t j0,
                            uint64_t shots, uint64_t *rec, const uint32_t *qubits,
                            const uint32_t *rows, uint64_t m, uint64_t seed, uint32_t epoch,
                            cudaStream_t st);
-void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t shots,
+void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t j0, uint64_t shots,
                         const uint32_t *flip_rows, uint64_t nflip, cudaStream_t st);
 
 } // namespace qsr

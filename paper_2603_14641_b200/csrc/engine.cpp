@@ -1,0 +1,211 @@
+// Device-resident schedules, the single-shot driver and layout conversion (engine.hpp).
+#include "engine.hpp"
+
+#include <algorithm>
+
+namespace qsr {
+
+std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
+                                                cudaStream_t st) {
+    // Validate every window first (apply_window / measure_window checks, gates.hpp:149-165,
+    // measure.hpp:385-398) so no device state is touched by a schedule that would throw.
+    std::vector<uint32_t> stamp(n, 0);
+    const uint64_t W = s.num_windows();
+    for (uint64_t w = 0; w < W; ++w)
+        validate_window(n, s.gates.data() + s.offsets[w], s.offsets[w + 1] - s.offsets[w],
+                        s.is_meas[w] != 0, stamp, uint32_t(w + 1));
+    auto ds = std::make_unique<DeviceSchedule>();
+    ds->device = device;
+    ds->offsets = s.offsets;
+    ds->is_meas = s.is_meas;
+    ds->mqubits.resize(W);
+    for (uint64_t w = 0; w < W; ++w) {
+        if (!s.is_meas[w]) {
+            ds->unitary_count += s.offsets[w + 1] - s.offsets[w];
+            continue;
+        }
+        for (uint64_t i = s.offsets[w]; i < s.offsets[w + 1]; ++i)
+            ds->mqubits[w].push_back(s.gates[i].q0);
+        ds->measure_count += ds->mqubits[w].size();
+    }
+    const uint64_t G = s.gates.size();
+    QSR_CUDA(cudaSetDevice(device));
+    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
+    if (G) {
+        // Pack + upload in 32 Mi-gate slabs through pinned staging.
+        const uint64_t slab = uint64_t(1) << 25;
+        uint64_t *pinned = nullptr;
+        QSR_CUDA(cudaMallocHost(&pinned, std::min(G, slab) * 8 * 2));
+        uint64_t *buf[2] = {pinned, pinned + std::min(G, slab)};
+        int cur = 0;
+        for (uint64_t b = 0; b < G; b += slab, cur ^= 1) {
+            uint64_t e = std::min(G, b + slab);
+            QSR_CUDA(cudaStreamSynchronize(st)); // previous use of buf[cur] finished
+            for (uint64_t i = b; i < e; ++i) buf[cur][i - b] = pack_gate(s.gates[i]);
+            QSR_CUDA(cudaMemcpyAsync(ds->d_gates + b, buf[cur], (e - b) * 8,
+                                     cudaMemcpyHostToDevice, st));
+        }
+        QSR_CUDA(cudaStreamSynchronize(st));
+        QSR_CUDA(cudaFreeHost(pinned));
+    }
+    return ds;
+}
+
+// Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
+// parallel stable scatter straight into packed device words, then one upload. Windows built
+// by the plan are operand-disjoint by construction; the only error the reference would raise
+// later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
+std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st) {
+    WindowPlan p = plan_windows(c);
+    if (p.duplicate_measure)
+        fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
+    const uint64_t G = c.gates.size();
+    std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
+    scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
+    auto ds = std::make_unique<DeviceSchedule>();
+    ds->device = device;
+    ds->offsets = std::move(p.offsets);
+    ds->is_meas = std::move(p.is_meas);
+    const uint64_t W = ds->is_meas.size();
+    ds->mqubits.resize(W);
+    for (uint64_t w = 0; w < W; ++w) {
+        const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
+        if (!ds->is_meas[w]) {
+            ds->unitary_count += e - b;
+            continue;
+        }
+        for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(uint32_t(packed[i] & 0x0FFFFFFFu));
+        ds->measure_count += e - b;
+    }
+    QSR_CUDA(cudaSetDevice(device));
+    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
+    if (G) {
+        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
+        QSR_CUDA(cudaStreamSynchronize(st));
+    }
+    return ds;
+}
+
+// The single-shot driver on device-resident inputs (simulator.hpp:46-70). `record` is a
+// device array of measure_count entries.
+void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
+                qsr_record_entry *d_record, RunTimes &rt) {
+    cudaEvent_t e_start, e_end, a, b;
+    QSR_CUDA(cudaEventCreate(&e_start));
+    QSR_CUDA(cudaEventCreate(&e_end));
+    QSR_CUDA(cudaEventCreate(&a));
+    QSR_CUDA(cudaEventCreate(&b));
+    QSR_CUDA(cudaEventRecord(e_start, t.stream));
+    launch_zero_state(t, nullptr);
+    QSR_CUDA(cudaMemsetAsync(t.ms.coin_index, 0, 8, t.stream));
+    const uint64_t W = ds.is_meas.size();
+    uint64_t rec_off = 0;
+    std::vector<uint8_t> flags;
+    uint64_t w = 0;
+    while (w < W) {
+        if (!ds.is_meas[w]) {
+            // A maximal run of unitary windows, bracketed by one event pair (TO bucket).
+            QSR_CUDA(cudaEventRecord(a, t.stream));
+            for (; w < W && !ds.is_meas[w]; ++w) {
+                launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+                ++rt.gate_windows;
+            }
+            QSR_CUDA(cudaEventRecord(b, t.stream));
+            QSR_CUDA(cudaEventSynchronize(b));
+            float ms = 0;
+            QSR_CUDA(cudaEventElapsedTime(&ms, a, b));
+            rt.to_ms += ms;
+            continue;
+        }
+        const auto &mq = ds.mqubits[w];
+        const uint64_t m = mq.size();
+        t.ensure_window_cap(m);
+        QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
+        measure_window_device(t, m, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
+        QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, m * sizeof(qsr_record_entry),
+                                 cudaMemcpyDeviceToDevice, t.stream));
+        rec_off += m;
+        ++w;
+    }
+    QSR_CUDA(cudaEventRecord(e_end, t.stream));
+    QSR_CUDA(cudaEventSynchronize(e_end));
+    float total = 0;
+    QSR_CUDA(cudaEventElapsedTime(&total, e_start, e_end));
+    rt.total_ms = total;
+    for (auto e : {e_start, e_end, a, b}) cudaEventDestroy(e);
+    if (read_error_flag(t))
+        fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+}
+
+void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
+                 const std::vector<qsr_record_entry> &record, double total_s) {
+    if (!rep) return;
+    rep->timers.to_seconds = rt.to_ms * 1e-3;
+    rep->timers.t_seconds = rt.t_ms * 1e-3;
+    rep->timers.cmp_seconds = rt.cmp_ms * 1e-3;
+    rep->timers.ge_seconds = rt.ge_ms * 1e-3;
+    rep->gate_count = ds.unitary_count;
+    rep->measure_count = ds.measure_count;
+    rep->window_count = ds.is_meas.size();
+    rep->probabilistic_count = 0;
+    for (const auto &e : record) rep->probabilistic_count += e.deterministic ? 0 : 1;
+    rep->total_seconds = total_s;
+}
+
+// Host reference-layout <-> device layout conversion.
+void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout) {
+    if (layout == QSR_COLUMN_MAJOR) {
+        if (t.layout != QSR_COLUMN_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
+        QSR_CUDA(cudaMemcpy2DAsync(t.x, t.cm_pitch * 8, x, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
+                                   cudaMemcpyHostToDevice, t.stream));
+        QSR_CUDA(cudaMemcpy2DAsync(t.z, t.cm_pitch * 8, z, 2 * t.k * 8, 2 * t.k * 8, t.n_pad,
+                                   cudaMemcpyHostToDevice, t.stream));
+        t.layout = QSR_COLUMN_MAJOR;
+    } else {
+        if (t.layout != QSR_ROW_MAJOR) { std::swap(t.x, t.x2); std::swap(t.z, t.z2); }
+        // Reference RM: word (i, col) at i*2n_pad + col  ->  internal row col, word i.
+        const uint64_t R = 2 * t.n_pad, K = t.k;
+        std::vector<uint64_t> tmp(R * K);
+        for (int plane = 0; plane < 2; ++plane) {
+            const uint64_t *src = plane ? z : x;
+            for (uint64_t i = 0; i < K; ++i)
+                for (uint64_t c = 0; c < R; ++c) tmp[c * K + i] = src[i * R + c];
+            QSR_CUDA(cudaMemcpy2DAsync(plane ? t.z : t.x, t.rm_pitch * 8, tmp.data(), K * 8, K * 8,
+                                       R, cudaMemcpyHostToDevice, t.stream));
+            QSR_CUDA(cudaStreamSynchronize(t.stream));
+        }
+        t.layout = QSR_ROW_MAJOR;
+    }
+}
+
+void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z) {
+    if (t.layout == QSR_COLUMN_MAJOR) {
+        if (x) QSR_CUDA(cudaMemcpy2DAsync(x, 2 * t.kg * 8, t.x, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad,
+                                          cudaMemcpyDeviceToHost, t.stream));
+        if (z) QSR_CUDA(cudaMemcpy2DAsync(z, 2 * t.kg * 8, t.z, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad,
+                                          cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        return;
+    }
+    const uint64_t R = 2 * t.n_pad, K = t.k;
+    std::vector<uint64_t> tmp(R * K);
+    for (int plane = 0; plane < 2; ++plane) {
+        uint64_t *dst = plane ? z : x;
+        if (!dst) continue;
+        QSR_CUDA(cudaMemcpy2DAsync(tmp.data(), K * 8, plane ? t.z : t.x, t.rm_pitch * 8, K * 8, R,
+                                   cudaMemcpyDeviceToHost, t.stream));
+        t.sync();
+        for (uint64_t c = 0; c < R; ++c)
+            for (uint64_t i = 0; i < K; ++i) dst[i * R + c] = tmp[c * K + i];
+    }
+}
+
+std::vector<uint64_t> download_signs(DeviceTableau &t) {
+    std::vector<uint64_t> s(2 * t.kg);
+    QSR_CUDA(cudaMemcpyAsync(s.data(), t.s, 2 * t.kg * 8, cudaMemcpyDeviceToHost, t.stream));
+    t.sync();
+    return s;
+}
+
+
+} // namespace qsr

@@ -1,0 +1,47 @@
+// Device-resident schedules and the single-shot driver (reference simulator.hpp:46-76) on one
+// DeviceTableau, plus host <-> device layout conversion. Shared by the C ABI (capi.cpp) and the
+// generator-row-sharded engine (shard.cpp).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "device.hpp"
+
+namespace qsr {
+
+// Device-resident schedule: packed gates + per-window measured qubits.
+struct DeviceSchedule {
+    int device = 0;
+    uint64_t *d_gates = nullptr;
+    std::vector<uint64_t> offsets;
+    std::vector<uint8_t> is_meas;
+    std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
+    uint64_t measure_count = 0, unitary_count = 0;
+    ~DeviceSchedule() {
+        if (d_gates) { cudaSetDevice(device); cudaFree(d_gates); }
+    }
+};
+
+// Validates every window (apply_window / measure_window checks) and uploads the packed gates.
+std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
+                                                cudaStream_t st);
+// Circuit -> device schedule through the O(G) plan (no API Schedule materialised).
+std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st);
+
+struct RunTimes {
+    double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
+    uint64_t gate_windows = 0;
+};
+
+// The single-shot driver on device-resident inputs; `d_record` has measure_count entries.
+void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
+                qsr_record_entry *d_record, RunTimes &rt);
+void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
+                 const std::vector<qsr_record_entry> &record, double total_s);
+// Host reference-layout <-> device layout (CM: [n_pad][2kg] words; RM: reference i-major).
+void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout);
+void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z);
+std::vector<uint64_t> download_signs(DeviceTableau &t);
+
+} // namespace qsr

@@ -37,7 +37,7 @@ namespace {
 
 using u64 = unsigned long long;
 constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
-enum : uint32_t { BL_LEN = 0, BL_DET = 1 };
+enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2 };
 // vinfo layout (u32 [4*kB]): vb | sign of V_m | c_m | beta(V_m) mod 4
 enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB };
 
@@ -70,29 +70,36 @@ __device__ __forceinline__ int block_sum(int v, int *red /* >= 32 ints */) {
 }
 
 // ---- phase A: column bits of all rows at the batch's measured qubits ----------------
+// Also ORs the stabilizer rows' bits into *stab_or: bit m set iff some stabilizer held here has
+// X at q_m at batch start (the sharded leader protocol, shard.cpp).
 __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64_t nrows,
-                          const uint32_t *__restrict__ fq, uint32_t b, uint32_t *__restrict__ colbits) {
+                          uint64_t ng, const uint32_t *__restrict__ fq, uint32_t b,
+                          uint32_t *__restrict__ colbits, uint32_t *__restrict__ stab_or) {
     __shared__ uint32_t sq[kB];
     if (threadIdx.x < b) sq[threadIdx.x] = fq[threadIdx.x];
     __syncthreads();
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (r >= nrows) return;
-    const uint64_t *row = x + r * pitch;
     uint32_t bits = 0;
-    for (uint32_t m = 0; m < b; ++m) {
-        const uint32_t q = sq[m];
-        bits |= uint32_t((__ldcg(row + (q >> 6)) >> (q & 63)) & 1u) << m;
+    if (r < nrows) {
+        const uint64_t *row = x + r * pitch;
+        for (uint32_t m = 0; m < b; ++m) {
+            const uint32_t q = sq[m];
+            bits |= uint32_t((__ldcg(row + (q >> 6)) >> (q & 63)) & 1u) << m;
+        }
+        colbits[r] = bits;
     }
-    colbits[r] = bits;
+    const uint32_t any = __reduce_or_sync(0xffffffffu, r >= ng && r < nrows ? bits : 0u);
+    if ((threadIdx.x & 31) == 0 && any) atomicOr(stab_or, any);
 }
 
 // ---- phase B: pivots, pivot rows, coins (one CTA) --------------------------------------
 __global__ void __launch_bounds__(1024)
 k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t k,
-               uint64_t n, uint64_t n_pad, uint64_t *__restrict__ s,
+               uint64_t n, uint64_t ng, uint64_t g0, uint64_t *__restrict__ s,
                const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ fq,
                const uint32_t *__restrict__ fidx, uint32_t b, uint64_t *__restrict__ Vx,
-               uint64_t *__restrict__ Vz, uint32_t *__restrict__ vinfo, uint32_t *__restrict__ bctl,
+               uint64_t *__restrict__ Vz, uint64_t vstride, uint32_t *__restrict__ vinfo,
+               uint32_t *__restrict__ bctl,
                uint64_t seed, uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
                int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
     __shared__ uint32_t s_vb[kB], s_vsign[kB], s_c[kB], s_q[kB], s_vbcol[kB], s_beta[kB];
@@ -122,7 +129,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                 bool used = false;
                 for (uint32_t mp = 0; mp < m; ++mp) used |= s_c[mp] == uint32_t(g);
                 if (!used) {
-                    const uint32_t cb = colbits[n_pad + g];
+                    const uint32_t cb = colbits[ng + g];
                     const uint32_t M = membership(cb, s_vbcol, 0, m);
                     const uint32_t bit = ((cb >> m) ^ parity32(M & s_vbcol[m])) & 1u;
                     if (bit) atomicMin(&s_min, uint32_t(g));
@@ -139,9 +146,9 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             break;
         }
         const uint32_t c = found;
-        const uint32_t Mc = membership(colbits[n_pad + c], s_vbcol, 0, m);
+        const uint32_t Mc = membership(colbits[ng + c], s_vbcol, 0, m);
         // V_m = S_c after its memberships; phase by the telescoped formula (file header).
-        const uint64_t rs = n_pad + c;
+        const uint64_t rs = ng + c;
         int e_part = 0, beta_part = 0;
         u64 acc = 0;
         for (uint64_t i = tid; i < k; i += nthr) {
@@ -149,7 +156,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             e_part += __popcll(cx & cz);
             for (uint32_t U = Mc; U; U &= U - 1) {
                 const uint32_t j = __ffs(U) - 1;
-                const u64 vx = Vx[uint64_t(j) * pitch + i], vz = Vz[uint64_t(j) * pitch + i];
+                const u64 vx = Vx[uint64_t(j) * vstride + i], vz = Vz[uint64_t(j) * vstride + i];
                 acc ^= vz & cx;
                 cx ^= vx;
                 cz ^= vz;
@@ -157,8 +164,8 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             const int bend = __popcll(cx & cz);
             e_part -= bend;
             beta_part += bend;
-            Vx[uint64_t(m) * pitch + i] = cx;
-            Vz[uint64_t(m) * pitch + i] = cz;
+            Vx[uint64_t(m) * vstride + i] = cx;
+            Vz[uint64_t(m) * vstride + i] = cz;
         }
         e_part += 2 * (__popcll(acc) & 1);
         const int e_tot = block_sum(e_part, s_red);
@@ -188,7 +195,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         __syncthreads(); // V_m (global) and the shared pivot bookkeeping visible to the block
         if (tid < b) {
             const uint32_t qj = s_q[tid];
-            s_bits[tid] = uint32_t((Vx[uint64_t(m) * pitch + (qj >> 6)] >> (qj & 63)) & 1u);
+            s_bits[tid] = uint32_t((Vx[uint64_t(m) * vstride + (qj >> 6)] >> (qj & 63)) & 1u);
         }
         __syncthreads();
         if (tid == 0) {
@@ -200,8 +207,8 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         const uint32_t qm = s_q[m];
         for (uint64_t i = tid; i < pitch; i += nthr) {
             const bool valid = i < k;
-            x[uint64_t(c) * pitch + i] = valid ? Vx[uint64_t(m) * pitch + i] : 0ull;
-            z[uint64_t(c) * pitch + i] = valid ? Vz[uint64_t(m) * pitch + i] : 0ull;
+            x[uint64_t(c) * pitch + i] = valid ? Vx[uint64_t(m) * vstride + i] : 0ull;
+            z[uint64_t(c) * pitch + i] = valid ? Vz[uint64_t(m) * vstride + i] : 0ull;
             x[rs * pitch + i] = 0ull;
             z[rs * pitch + i] = i == (qm >> 6) ? (1ull << (qm & 63)) : 0ull;
         }
@@ -212,7 +219,7 @@ k_batch_pivots(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         const bool v = tid < s_len;
         vinfo[VI_VB + tid] = v ? s_vb[tid] : 0u;
         vinfo[VI_SIGN + tid] = v ? s_vsign[tid] : 0u;
-        vinfo[VI_C + tid] = v ? s_c[tid] : 0xFFFFFFFFu;
+        vinfo[VI_C + tid] = v ? uint32_t(g0 + s_c[tid]) : 0xFFFFFFFFu; // global generator
         vinfo[VI_BETA + tid] = v ? s_beta[tid] : 0u;
     }
     if (tid == 0) bctl[BL_LEN] = s_len;
@@ -237,14 +244,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Stage words [w0, w0+kSlice) of V_0..V_{len-1} (x and z) into buf[(j*2+plane)*kSlice + w]
 // with cp.async (16 bytes per op; pitch % 16 == 0, so past k it reads the zero padding).
 __device__ __forceinline__ void stage_slice(u64 *buf, const uint64_t *Vx, const uint64_t *Vz,
-                                            uint64_t pitch, uint64_t w0, uint32_t len) {
+                                            uint64_t pitch, uint64_t vstride, uint64_t w0,
+                                            uint32_t len) {
     const uint32_t pairs = len * 2 * (kSlice / 2);
     for (uint32_t e = threadIdx.x; e < pairs; e += kCThreads) {
         const uint32_t w = 2 * (e & (kSlice / 2 - 1)), jp = e / (kSlice / 2);
         const uint32_t j = jp >> 1, plane = jp & 1;
         const uint64_t gw = w0 + w;
         u64 *dst = buf + size_t(jp) * kSlice + w;
-        if (gw < pitch) cp_async16(dst, (plane ? Vz : Vx) + uint64_t(j) * pitch + gw);
+        if (gw < pitch) cp_async16(dst, (plane ? Vz : Vx) + uint64_t(j) * vstride + gw);
         else { dst[0] = 0; dst[1] = 0; }
     }
     cp_async_commit();
@@ -252,9 +260,9 @@ __device__ __forceinline__ void stage_slice(u64 *buf, const uint64_t *Vx, const 
 
 __global__ void __launch_bounds__(kCThreads, 2)
 k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t k,
-              uint64_t nrows, uint64_t n_pad, uint64_t *__restrict__ s,
+              uint64_t nrows, uint64_t ng, uint64_t g0, uint64_t *__restrict__ s,
               const uint32_t *__restrict__ colbits, const uint64_t *__restrict__ Vx,
-              const uint64_t *__restrict__ Vz, const uint32_t *__restrict__ vinfo,
+              const uint64_t *__restrict__ Vz, uint64_t vstride, const uint32_t *__restrict__ vinfo,
               const uint32_t *__restrict__ bctl, int *__restrict__ err) {
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
     __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask;
@@ -264,7 +272,10 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid < kB) {
         s_vb[tid] = vinfo[VI_VB + tid];
-        s_c[tid] = vinfo[VI_C + tid];
+        // Pivot generator (global) -> local generator index, or none if another shard holds it.
+        const uint32_t cg = vinfo[VI_C + tid];
+        s_c[tid] = (cg != 0xFFFFFFFFu && cg >= g0 && cg < g0 + ng) ? uint32_t(cg - g0)
+                                                                       : 0xFFFFFFFFu;
     }
     if (tid == 0) {
         uint32_t vs = 0, b0 = 0, b1 = 0;
@@ -295,7 +306,8 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
             uint32_t cb = colbits[r], start = 0;
             bool skip = false;
             for (uint32_t j = 0; j < len; ++j) {
-                if (r == n_pad + s_c[j]) skip = true;
+                if (s_c[j] == 0xFFFFFFFFu) continue;
+                if (r == ng + s_c[j]) skip = true;
                 if (r == s_c[j]) { cb = s_vb[j]; start = j + 1; }
             }
             M[q] = skip ? 0u : membership(cb, s_vbcol, start, len);
@@ -305,12 +317,12 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
         int bd[kRowsPerWarp];
 #pragma unroll
         for (int q = 0; q < kRowsPerWarp; ++q) acc[q] = 0, bd[q] = 0;
-        stage_slice(sv_raw, Vx, Vz, pitch, 0, len);
+        stage_slice(sv_raw, Vx, Vz, pitch, vstride, 0, len);
         for (uint32_t sl = 0; sl < nslices; ++sl) {
             cp_async_wait_all();
             __syncthreads(); // slice sl staged; everyone is done with the other buffer
             if (sl + 1 < nslices)
-                stage_slice(sv_raw + ((sl + 1) & 1) * kSliceWords, Vx, Vz, pitch,
+                stage_slice(sv_raw + ((sl + 1) & 1) * kSliceWords, Vx, Vz, pitch, vstride,
                             uint64_t(sl + 1) * kSlice, len);
             if (U == 0) continue;
             const u64 *buf = sv_raw + (sl & 1) * kSliceWords;
@@ -373,18 +385,29 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
 
 } // namespace
 
-void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                   uint64_t seed, uint32_t &done, bool &det) {
+void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
     MeasureScratch &ms = t.ms;
-    const uint64_t nrows = 2 * t.n_pad;
+    const uint64_t nrows = 2 * t.ng;
     QSR_CUDA(cudaMemsetAsync(ms.bctl, 0, 16, t.stream));
-    k_colbits<<<unsigned((nrows + 255) / 256), 256, 0, t.stream>>>(t.x, t.rm_pitch, nrows, d_fq, b,
-                                                                    ms.colbits);
+    k_colbits<<<unsigned((nrows + 255) / 256), 256, 0, t.stream>>>(t.x, t.rm_pitch, nrows, t.ng, d_fq,
+                                                                    b, ms.colbits, ms.bctl + BL_STAB_OR);
     QSR_CUDA(cudaGetLastError());
-    k_batch_pivots<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n, t.n_pad, t.s, ms.colbits,
-                                             d_fq, d_fidx, b, ms.Vx, ms.Vz, ms.vinfo, ms.bctl, seed,
-                                             ms.coin_index, ms.out, ms.err, ms.coin_table);
+    count_launch();
+}
+
+void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
+                  uint64_t seed) {
+    MeasureScratch &ms = t.ms;
+    k_batch_pivots<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_gen, t.ng, t.g0, t.s,
+                                             ms.colbits, d_fq, d_fidx, b, ms.Vx, ms.Vz,
+                                             ms.vstride, ms.vinfo, ms.bctl, seed, ms.coin_index,
+                                             ms.out, ms.err, ms.coin_table);
     QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void batch_apply(DeviceTableau &t) {
+    MeasureScratch &ms = t.ms;
     static bool configured = false;
     if (!configured) {
         QSR_CUDA(cudaFuncSetAttribute(k_batch_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -392,12 +415,19 @@ void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fid
         configured = true;
     }
     k_batch_apply<<<unsigned(t.num_sms * 2), kCThreads, kApplySmem, t.stream>>>(
-        t.x, t.z, t.rm_pitch, t.k, nrows, t.n_pad, t.s, ms.colbits, ms.Vx, ms.Vz, ms.vinfo, ms.bctl,
-        ms.err);
+        t.x, t.z, t.rm_pitch, t.k, 2 * t.ng, t.ng, t.g0, t.s, ms.colbits, ms.Vx, ms.Vz, ms.vstride,
+        ms.vinfo, ms.bctl, ms.err);
     QSR_CUDA(cudaGetLastError());
-    count_launch(3);
+    count_launch();
+}
+
+void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
+                   uint64_t seed, uint32_t &done, bool &det) {
+    batch_colbits(t, d_fq, b);
+    batch_pivots(t, d_fq, d_fidx, b, seed);
+    batch_apply(t);
     uint32_t h[2];
-    QSR_CUDA(cudaMemcpyAsync(h, ms.bctl, 8, cudaMemcpyDeviceToHost, t.stream));
+    QSR_CUDA(cudaMemcpyAsync(h, t.ms.bctl, 8, cudaMemcpyDeviceToHost, t.stream));
     QSR_CUDA(cudaStreamSynchronize(t.stream));
     done = h[BL_LEN];
     det = h[BL_DET] != 0;

@@ -12,66 +12,72 @@ namespace qsr {
 
 namespace {
 
-__global__ void k_frames_init(uint64_t *__restrict__ zf, uint64_t n, uint64_t kf, uint64_t pitch,
-                              uint64_t last_mask, uint64_t seed, uint32_t epoch) {
+// kf = shot-words held here, j0 = their global offset, jl = global index of the last word
+// (the one the last-word mask applies to). Unsharded: j0 = 0, jl = kf - 1.
+__global__ void k_frames_init(uint64_t *__restrict__ zf, uint64_t n, uint64_t kf, uint64_t j0,
+                              uint64_t jl, uint64_t pitch, uint64_t last_mask, uint64_t seed,
+                              uint32_t epoch) {
     const uint64_t total = n * kf;
     for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t q = idx / kf, j = idx % kf;
-        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | j);
-        if (j == kf - 1) w &= last_mask;
+        uint64_t q = idx / kf, j = idx % kf, jg = j0 + j;
+        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | jg);
+        if (jg == jl) w &= last_mask;
         zf[q * pitch + j] = w;
     }
 }
 
 __global__ void k_measure_sample(const uint64_t *__restrict__ xf, uint64_t *__restrict__ zf,
-                                 uint64_t pitch, uint64_t kf, uint64_t last_mask,
+                                 uint64_t pitch, uint64_t kf, uint64_t j0, uint64_t jl,
+                                 uint64_t last_mask,
                                  uint64_t *__restrict__ rec, const uint32_t *__restrict__ qubits,
                                  const uint32_t *__restrict__ rows, uint64_t m, uint64_t seed,
                                  uint32_t epoch) {
     const uint64_t total = m * kf;
     for (uint64_t item = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
          item += uint64_t(gridDim.x) * blockDim.x) {
-        uint64_t i = item / kf, j = item % kf;
+        uint64_t i = item / kf, j = item % kf, jg = j0 + j;
         uint64_t q = qubits[i];
         rec[uint64_t(rows[i]) * pitch + j] = xf[q * pitch + j];
-        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | j);
-        if (j == kf - 1) w &= last_mask;
+        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | jg);
+        if (jg == jl) w &= last_mask;
         zf[q * pitch + j] = w;
     }
 }
 
 __global__ void k_record_fold(uint64_t *__restrict__ rec, uint64_t pitch, uint64_t kf,
-                              uint64_t last_mask, const uint32_t *__restrict__ flip_rows,
-                              uint64_t nflip) {
+                              uint64_t j0, uint64_t jl, uint64_t last_mask,
+                              const uint32_t *__restrict__ flip_rows, uint64_t nflip) {
     const uint64_t total = nflip * kf;
     for (uint64_t item = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
          item += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t i = item / kf, j = item % kf;
         uint64_t *p = rec + uint64_t(flip_rows[i]) * pitch + j;
-        uint64_t mask = j == kf - 1 ? last_mask : ~0ull;
+        uint64_t mask = j0 + j == jl ? last_mask : ~0ull;
         *p = (*p ^ ~0ull) & mask;
     }
 }
 
 __global__ void k_basis_state(uint64_t *__restrict__ x, uint64_t *__restrict__ z,
-                              uint64_t *__restrict__ s, uint64_t n, uint64_t k, uint64_t pitch,
-                              const uint8_t *__restrict__ init) {
-    // Destabilizer q = (-1)^b X_q, stabilizer q = (-1)^b Z_q (tableau.hpp:120-129).
-    for (uint64_t q = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
-         q += uint64_t(gridDim.x) * blockDim.x) {
-        x[q * pitch + q / 64] = 1ull << (q % 64);
-        z[q * pitch + k + q / 64] = 1ull << (q % 64);
+                              uint64_t *__restrict__ s, uint64_t g0, uint64_t n_gen, uint64_t kg,
+                              uint64_t pitch, const uint8_t *__restrict__ init) {
+    // Destabilizer g = (-1)^b X_g, stabilizer g = (-1)^b Z_g (tableau.hpp:120-129), for the
+    // generators g0 .. g0+n_gen-1 this tableau (shard) holds; local generator l = g - g0.
+    for (uint64_t l = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; l < n_gen;
+         l += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = g0 + l;
+        x[q * pitch + l / 64] = 1ull << (l % 64);
+        z[q * pitch + kg + l / 64] = 1ull << (l % 64);
     }
     if (init) {
         // Sign words: one thread per word (no write conflicts).
-        for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < k;
+        for (uint64_t w = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; w < kg;
              w += uint64_t(gridDim.x) * blockDim.x) {
             uint64_t v = 0;
-            for (uint64_t b = 0; b < 64 && w * 64 + b < n; ++b)
-                v |= uint64_t(init[w * 64 + b] & 1) << b;
+            for (uint64_t b = 0; b < 64 && w * 64 + b < n_gen; ++b)
+                v |= uint64_t(init[g0 + w * 64 + b] & 1) << b;
             s[w] = v;
-            s[k + w] = v;
+            s[kg + w] = v;
         }
     }
 }
@@ -90,30 +96,31 @@ inline unsigned grid_for(uint64_t total, unsigned threads) {
 
 } // namespace
 
-void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t pitch, uint64_t shots,
-                        uint64_t seed, uint32_t epoch, const uint32_t *, cudaStream_t st) {
-    k_frames_init<<<grid_for(n * kf, 256), 256, 0, st>>>(zf, n, kf, pitch, last_mask_for(shots),
-                                                         seed, epoch);
+void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t j0, uint64_t pitch,
+                        uint64_t shots, uint64_t seed, uint32_t epoch, cudaStream_t st) {
+    k_frames_init<<<grid_for(n * kf, 256), 256, 0, st>>>(zf, n, kf, j0, (shots + 63) / 64 - 1, pitch,
+                                                         last_mask_for(shots), seed, epoch);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
 
-void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf,
+void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf, uint64_t j0,
                            uint64_t shots, uint64_t *rec, const uint32_t *qubits,
                            const uint32_t *rows, uint64_t m, uint64_t seed, uint32_t epoch,
                            cudaStream_t st) {
     if (m == 0) return;
-    k_measure_sample<<<grid_for(m * kf, 256), 256, 0, st>>>(xf, zf, pitch, kf, last_mask_for(shots),
-                                                            rec, qubits, rows, m, seed, epoch);
+    k_measure_sample<<<grid_for(m * kf, 256), 256, 0, st>>>(xf, zf, pitch, kf, j0, (shots + 63) / 64 - 1,
+                                                            last_mask_for(shots), rec, qubits, rows,
+                                                            m, seed, epoch);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
 
-void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t shots,
+void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t j0, uint64_t shots,
                         const uint32_t *flip_rows, uint64_t nflip, cudaStream_t st) {
     if (nflip == 0) return;
-    k_record_fold<<<grid_for(nflip * kf, 256), 256, 0, st>>>(rec, pitch, kf, last_mask_for(shots),
-                                                             flip_rows, nflip);
+    k_record_fold<<<grid_for(nflip * kf, 256), 256, 0, st>>>(rec, pitch, kf, j0, (shots + 63) / 64 - 1,
+                                                             last_mask_for(shots), flip_rows, nflip);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -122,8 +129,8 @@ void launch_zero_state(DeviceTableau &t, const uint8_t *d_init) {
     QSR_CUDA(cudaMemsetAsync(t.x, 0, t.plane_words * 8, t.stream));
     QSR_CUDA(cudaMemsetAsync(t.z, 0, t.plane_words * 8, t.stream));
     QSR_CUDA(cudaMemsetAsync(t.s, 0, t.cm_pitch * 8, t.stream));
-    k_basis_state<<<grid_for(t.n, 256), 256, 0, t.stream>>>(t.x, t.z, t.s, t.n, t.k, t.cm_pitch,
-                                                            d_init);
+    k_basis_state<<<grid_for(std::max<uint64_t>(t.n_gen, t.kg), 256), 256, 0, t.stream>>>(
+        t.x, t.z, t.s, t.g0, t.n_gen, t.kg, t.cm_pitch, d_init);
     QSR_CUDA(cudaGetLastError());
     count_launch();
     t.layout = QSR_COLUMN_MAJOR;

@@ -24,7 +24,6 @@ namespace {
 struct V2 {
     uint64_t a, b;
     __device__ __forceinline__ V2 operator&(V2 o) const { return {a & o.a, b & o.b}; }
-    __device__ __forceinline__ V2 operator|(V2 o) const { return {a | o.a, b | o.b}; }
     __device__ __forceinline__ V2 operator^(V2 o) const { return {a ^ o.a, b ^ o.b}; }
     __device__ __forceinline__ V2 operator~() const { return {~a, ~b}; }
     __device__ __forceinline__ V2 &operator^=(V2 o) { a ^= o.a; b ^= o.b; return *this; }

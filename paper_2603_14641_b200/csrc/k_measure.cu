@@ -28,7 +28,7 @@ enum : uint32_t { MODE_COLLAPSE = 0, MODE_DET = 1, MODE_SWAP = 2, MODE_NONE = 3 
 enum : uint32_t { CTL_COUNT = 0, CTL_C = 1, CTL_MODE = 2, CTL_Q = 3, CTL_OUT = 4, CTL_WORDS = 8 };
 constexpr int kDetChunks = 128;
 
-// ---- K4/K5: one qubit column of all 2*n_pad rows -> bit mask (2k words) -------------
+// ---- K4/K5: one qubit column of all 2*ng generator rows -> bit mask (2kg words) ----
 __global__ void k_column_mask(const uint64_t *__restrict__ x, uint64_t rm_pitch, uint64_t nrows,
                               uint32_t iq, uint32_t bq, uint32_t *__restrict__ mask32) {
     uint64_t r = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -45,7 +45,7 @@ __global__ void k_column_mask(const uint64_t *__restrict__ x, uint64_t rm_pitch,
 // MODE_DET: list = destabilizers with X at q (ascending).
 // MODE_SWAP: c = ctl[CTL_C] given; list = destabilizers != c with X at q.
 __global__ void __launch_bounds__(1024)
-k_compact(uint64_t *__restrict__ mask, uint64_t k, uint64_t n_pad, uint32_t *__restrict__ ctl,
+k_compact(uint64_t *__restrict__ mask, uint64_t k, uint64_t ng, uint32_t *__restrict__ ctl,
           uint32_t *__restrict__ rows, const uint8_t *__restrict__ active) {
     __shared__ uint32_t s_min;
     __shared__ uint32_t s_warp[32];
@@ -109,7 +109,7 @@ k_compact(uint64_t *__restrict__ mask, uint64_t k, uint64_t n_pad, uint32_t *__r
     for (uint64_t w = w0; w < w1; ++w) {
         uint64_t v = mask[w];
         // Row id: word w < k -> destabilizer rows w*64+b; w >= k -> stabilizer rows
-        // n_pad + (w-k)*64 + b, which equals w*64 + b because n_pad = 64k.
+        // ng + (w-k)*64 + b, which equals w*64 + b because ng = 64k (k = generator-words here).
         while (v) {
             uint32_t b = __ffsll(v) - 1;
             v &= v - 1;
@@ -127,7 +127,7 @@ k_compact(uint64_t *__restrict__ mask, uint64_t k, uint64_t n_pad, uint32_t *__r
 // memory once per CTA. Only runs when ctl[CTL_MODE] == want_mode (or want_mode == any).
 __global__ void __launch_bounds__(512)
 k_rowmul(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, uint64_t k,
-         uint64_t n_pad, uint64_t *__restrict__ s, const uint32_t *__restrict__ ctl,
+         uint64_t ng, uint64_t *__restrict__ s, const uint32_t *__restrict__ ctl,
          const uint32_t *__restrict__ rows, uint32_t want_mask, int ctl_is_stab,
          int *__restrict__ err) {
     extern __shared__ uint64_t sc[]; // [2][rm_pitch]
@@ -135,7 +135,7 @@ k_rowmul(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
     if (!((want_mask >> mode) & 1)) return;
     const uint32_t count = ctl[CTL_COUNT];
     if (count == 0) return;
-    const uint64_t crow = (ctl_is_stab ? n_pad : 0) + ctl[CTL_C];
+    const uint64_t crow = (ctl_is_stab ? ng : 0) + ctl[CTL_C];
     // Whole pitch (padding words are zero) so the last word pair of an odd k is defined.
     for (uint64_t i = threadIdx.x; i < rm_pitch; i += blockDim.x) {
         sc[i] = x[crow * rm_pitch + i];
@@ -175,7 +175,7 @@ k_rowmul(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
 // row list in order for its 64 words and leaves the partial product + phase.
 __global__ void __launch_bounds__(32)
 k_det_partial(const uint64_t *__restrict__ x, const uint64_t *__restrict__ z, uint64_t rm_pitch,
-              uint64_t k, uint64_t n_pad, const uint64_t *__restrict__ s,
+              uint64_t k, uint64_t ng, const uint64_t *__restrict__ s,
               const uint32_t *__restrict__ ctl, const uint32_t *__restrict__ rows,
               uint64_t *__restrict__ px, uint64_t *__restrict__ pz, int64_t *__restrict__ pe) {
     if (ctl[CTL_MODE] != MODE_DET) return;
@@ -189,7 +189,7 @@ k_det_partial(const uint64_t *__restrict__ x, const uint64_t *__restrict__ z, ui
     int ph = 0, sg = 0;
     for (uint64_t e = e0; e < e1; ++e) {
         const uint64_t g = rows[e];          // destabilizer index -> stabilizer row
-        const uint64_t r = n_pad + g;
+        const uint64_t r = ng + g;
         if (blockIdx.x == 0 && lane == 0) sg += (s[r >> 6] >> (r & 63)) & 1;
         if (act) {
             ulonglong2 xv = __ldcg(reinterpret_cast<const ulonglong2 *>(x + r * rm_pitch + i));
@@ -211,7 +211,7 @@ k_det_partial(const uint64_t *__restrict__ x, const uint64_t *__restrict__ z, ui
 // ---- finish: deterministic combine, or pivot replacement + coin --------------------
 __global__ void __launch_bounds__(1024)
 k_finish(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, uint64_t k,
-         uint64_t n_pad, uint64_t *__restrict__ s, uint32_t *__restrict__ ctl,
+         uint64_t ng, uint64_t *__restrict__ s, uint32_t *__restrict__ ctl,
          const uint64_t *__restrict__ px, const uint64_t *__restrict__ pz,
          int64_t *__restrict__ pe, uint64_t seed, uint64_t *__restrict__ coin_index,
          qsr_record_entry *__restrict__ out, int *__restrict__ err,
@@ -252,7 +252,7 @@ k_finish(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
     }
     // MODE_COLLAPSE / MODE_SWAP: D_c <- S_c (bits + sign), S_c <- +Z_q.
     const uint64_t c = ctl[CTL_C];
-    const uint64_t rs = n_pad + c, rd = c;
+    const uint64_t rs = ng + c, rd = c;
     const uint64_t iq = q >> 6, bq = q & 63;
     for (uint64_t i = tid; i < k; i += blockDim.x) {
         uint64_t xs = x[rs * rm_pitch + i], zs = z[rs * rm_pitch + i];
@@ -273,6 +273,53 @@ k_finish(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t rm_pitch, 
         s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (coin << (rs & 63));
         ctl[CTL_OUT] = uint32_t(coin);
         if (out && mode == MODE_COLLAPSE) *out = qsr_record_entry{q, uint8_t(coin), 0};
+    }
+}
+
+// ---- ordered fold of partial products (deterministic outcome, sharded form) ----------
+// Parts c = 0..nparts-1 each hold a product row (x at px + c*stride, z at pz + c*stride) and an
+// exponent pe[c*pe_stride] (mod-4 phase incl. 2*signs). Folding them in order keeps the
+// product rows and the exponent mod 4 (measure.hpp:343-376 is associative).
+// final == 0: write the folded row + exponent to (ox, oz, oe). final == 1: the outcome.
+__global__ void __launch_bounds__(1024)
+k_det_reduce(const uint64_t *__restrict__ px, const uint64_t *__restrict__ pz,
+             int64_t *__restrict__ pe, uint64_t stride, uint64_t pe_stride, uint32_t nparts,
+             uint64_t k, int reset_pe, int final, uint64_t *__restrict__ ox,
+             uint64_t *__restrict__ oz, int64_t *__restrict__ oe, uint32_t *__restrict__ ctl,
+             uint32_t q, qsr_record_entry *__restrict__ out, int *__restrict__ err) {
+    __shared__ int s_ph;
+    const uint32_t tid = threadIdx.x;
+    if (ctl[CTL_MODE] != MODE_DET) return;
+    if (tid == 0) s_ph = 0;
+    __syncthreads();
+    int ph = 0;
+    for (uint64_t i = tid; i < k; i += blockDim.x) {
+        uint64_t ax = 0, az = 0;
+        for (uint32_t c = 0; c < nparts; ++c) {
+            const uint64_t bx = px[uint64_t(c) * stride + i], bz = pz[uint64_t(c) * stride + i];
+            ph += phase_delta(ax, az, bx, bz);
+            ax ^= bx;
+            az ^= bz;
+        }
+        if (!final) { ox[i] = ax; oz[i] = az; }
+    }
+    ph = warp_sum(ph);
+    if ((tid & 31) == 0) atomicAdd(&s_ph, ph);
+    __syncthreads();
+    if (tid == 0) {
+        int64_t e = s_ph;
+        for (uint32_t c = 0; c < nparts; ++c) {
+            e += pe[uint64_t(c) * pe_stride];
+            if (reset_pe) pe[uint64_t(c) * pe_stride] = 0;
+        }
+        if (!final) {
+            *oe = e;
+            return;
+        }
+        if (e & 1) atomicExch(err, 1);
+        const uint32_t outcome = uint32_t((e >> 1) & 1);
+        ctl[CTL_OUT] = outcome;
+        if (out) *out = qsr_record_entry{q, uint8_t(outcome), 1};
     }
 }
 
@@ -312,7 +359,7 @@ void set_ctl(DeviceTableau &t, uint32_t mode, uint32_t c, uint32_t q) {
 }
 
 void column_mask(DeviceTableau &t, uint64_t q) {
-    const uint64_t nrows = 2 * t.n_pad;
+    const uint64_t nrows = 2 * t.ng;
     const unsigned threads = 256;
     k_column_mask<<<unsigned((nrows + threads - 1) / threads), threads, 0, t.stream>>>(
         t.x, t.rm_pitch, nrows, uint32_t(q >> 6), uint32_t(q & 63),
@@ -322,14 +369,14 @@ void column_mask(DeviceTableau &t, uint64_t q) {
 }
 
 void compact(DeviceTableau &t, const uint8_t *active) {
-    k_compact<<<1, 1024, 0, t.stream>>>(t.ms.mask, t.k, t.n_pad, t.ms.ctl, t.ms.rows, active);
+    k_compact<<<1, 1024, 0, t.stream>>>(t.ms.mask, t.kg, t.ng, t.ms.ctl, t.ms.rows, active);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
 
 void rowmul(DeviceTableau &t, uint32_t want_mask, int ctl_is_stab) {
     size_t smem = rowmul_smem(t);
-    k_rowmul<<<rowmul_blocks(t), 512, smem, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_pad, t.s,
+    k_rowmul<<<rowmul_blocks(t), 512, smem, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.ng, t.s,
                                                         t.ms.ctl, t.ms.rows, want_mask,
                                                         ctl_is_stab, t.ms.err);
     QSR_CUDA(cudaGetLastError());
@@ -338,7 +385,7 @@ void rowmul(DeviceTableau &t, uint32_t want_mask, int ctl_is_stab) {
 
 void det_partial(DeviceTableau &t) {
     dim3 grid{unsigned((t.k + 63) / 64), unsigned(kDetChunks)};
-    k_det_partial<<<grid, 32, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_pad, t.s, t.ms.ctl,
+    k_det_partial<<<grid, 32, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.ng, t.s, t.ms.ctl,
                                               t.ms.rows, t.ms.partial_x, t.ms.partial_z,
                                               t.ms.partial_e);
     QSR_CUDA(cudaGetLastError());
@@ -346,7 +393,7 @@ void det_partial(DeviceTableau &t) {
 }
 
 void finish(DeviceTableau &t, uint64_t seed, qsr_record_entry *out) {
-    k_finish<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_pad, t.s, t.ms.ctl,
+    k_finish<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.ng, t.s, t.ms.ctl,
                                        t.ms.partial_x, t.ms.partial_z, t.ms.partial_e, seed,
                                        t.ms.coin_index, out, t.ms.err, t.ms.coin_table);
     QSR_CUDA(cudaGetLastError());
@@ -380,12 +427,7 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
         for (auto &e : ev) QSR_CUDA(cudaEventCreate(&e));
     // Flags on the CM tableau (find_probabilistic, measure.hpp:405).
     {
-        unsigned threads = 256;
-        unsigned blocks = unsigned((m * 32 + threads - 1) / threads);
-        k_flags_cm<<<blocks, threads, 0, t.stream>>>(t.x, t.cm_pitch, t.k, t.ms.mqubits, m,
-                                                     t.ms.flags);
-        QSR_CUDA(cudaGetLastError());
-        count_launch();
+        flags_cm(t, m);
         flags_host.resize(m);
         QSR_CUDA(cudaMemcpyAsync(flags_host.data(), t.ms.flags, m, cudaMemcpyDeviceToHost,
                                  t.stream));
@@ -456,13 +498,50 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
     }
 }
 
+uint64_t det_slot_words(const DeviceTableau &t) { return 2 * t.rm_pitch + 16; }
+
+void det_local_partial(DeviceTableau &t, uint64_t q, uint64_t *slot) {
+    set_ctl(t, MODE_DET, 0, uint32_t(q));
+    column_mask(t, q);
+    compact(t, nullptr);
+    det_partial(t);
+    k_det_reduce<<<1, 1024, 0, t.stream>>>(t.ms.partial_x, t.ms.partial_z, t.ms.partial_e,
+                                           t.rm_pitch, 1, kDetChunks, t.k, 1, 0, slot,
+                                           slot + t.rm_pitch,
+                                           reinterpret_cast<int64_t *>(slot + 2 * t.rm_pitch),
+                                           t.ms.ctl, uint32_t(q), nullptr, t.ms.err);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void det_combine(DeviceTableau &t, uint64_t q, const uint64_t *slots, uint32_t nslots,
+                 qsr_record_entry *out) {
+    const uint64_t sw = det_slot_words(t);
+    k_det_reduce<<<1, 1024, 0, t.stream>>>(
+        slots, slots + t.rm_pitch,
+        reinterpret_cast<int64_t *>(const_cast<uint64_t *>(slots) + 2 * t.rm_pitch), sw, sw,
+        nslots, t.k, 0, 1, nullptr, nullptr, nullptr, t.ms.ctl, uint32_t(q), out, t.ms.err);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void flags_cm(DeviceTableau &t, uint64_t m) {
+    if (m == 0) return;
+    const unsigned threads = 256;
+    const unsigned blocks = unsigned((m * 32 + threads - 1) / threads);
+    k_flags_cm<<<blocks, threads, 0, t.stream>>>(t.x, t.cm_pitch, t.kg, t.ms.mqubits, m,
+                                                 t.ms.flags);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 // ---- API-parity operations on a (transposed) RM tableau ------------------------------
 void rm_column_mask(DeviceTableau &t, uint64_t q) { column_mask(t, q); }
 
 void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries, uint64_t &count) {
     column_mask(t, q);
-    std::vector<uint64_t> mask(t.k);
-    QSR_CUDA(cudaMemcpyAsync(mask.data(), t.ms.mask + t.k, t.k * 8, cudaMemcpyDeviceToHost,
+    std::vector<uint64_t> mask(t.kg);
+    QSR_CUDA(cudaMemcpyAsync(mask.data(), t.ms.mask + t.kg, t.kg * 8, cudaMemcpyDeviceToHost,
                              t.stream));
     QSR_CUDA(cudaStreamSynchronize(t.stream));
     entries.assign(t.n, -1);
@@ -474,13 +553,13 @@ void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries,
 void rm_find_probabilistic(DeviceTableau &t, const std::vector<uint32_t> &qubits,
                            std::vector<int64_t> &out) {
     out.assign(qubits.size(), -1);
-    std::vector<uint64_t> mask(t.k);
+    std::vector<uint64_t> mask(t.kg);
     for (size_t i = 0; i < qubits.size(); ++i) {
         column_mask(t, qubits[i]);
-        QSR_CUDA(cudaMemcpyAsync(mask.data(), t.ms.mask + t.k, t.k * 8, cudaMemcpyDeviceToHost,
+        QSR_CUDA(cudaMemcpyAsync(mask.data(), t.ms.mask + t.kg, t.kg * 8, cudaMemcpyDeviceToHost,
                                  t.stream));
         QSR_CUDA(cudaStreamSynchronize(t.stream));
-        for (uint64_t w = 0; w < t.k; ++w)
+        for (uint64_t w = 0; w < t.kg; ++w)
             if (mask[w]) { out[i] = qubits[i]; break; }
     }
 }
@@ -525,7 +604,7 @@ void rm_parallel_ge(DeviceTableau &t, const std::vector<int64_t> &pivots) {
     if (T == 0) return;
     std::vector<uint32_t> stab_rows(T), dest_rows(T);
     for (uint64_t e = 0; e < T; ++e) {
-        stab_rows[e] = uint32_t(t.n_pad + uint64_t(pivots[e + 1]));
+        stab_rows[e] = uint32_t(t.ng + uint64_t(pivots[e + 1]));
         dest_rows[e] = uint32_t(pivots[e + 1]);
     }
     // Destabilizer half first (reads target destabilizers, which the stabilizer half never
@@ -548,8 +627,8 @@ void rm_parallel_ge(DeviceTableau &t, const std::vector<int64_t> &pivots) {
     uint32_t cnt = uint32_t(T);
     QSR_CUDA(cudaMemcpyAsync(t.ms.ctl + CTL_COUNT, &cnt, 4, cudaMemcpyHostToDevice, t.stream));
     rowmul(t, 1u << MODE_COLLAPSE, 1);
-    std::vector<uint64_t> s(2 * t.k);
-    QSR_CUDA(cudaMemcpyAsync(s.data(), t.s, 2 * t.k * 8, cudaMemcpyDeviceToHost, t.stream));
+    std::vector<uint64_t> s(2 * t.kg);
+    QSR_CUDA(cudaMemcpyAsync(s.data(), t.s, 2 * t.kg * 8, cudaMemcpyDeviceToHost, t.stream));
     QSR_CUDA(cudaStreamSynchronize(t.stream));
     QSR_CUDA(cudaFreeAsync(d_targets, t.stream));
     QSR_CUDA(cudaFreeAsync(d_phase, t.stream));

@@ -109,18 +109,18 @@ void run(const uint64_t *src, uint64_t *dst, uint64_t src_pitch, uint64_t dst_pi
 } // namespace
 
 void transpose_to_rm(DeviceTableau &t) {
-    // CM: row-tiles I in [0,k), words J in [0,2k).
-    run(t.x, t.x2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.k, true, t.stream);
-    run(t.z, t.z2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.k, true, t.stream);
+    // CM: row-tiles I in [0,k), words J in [0,2kg).
+    run(t.x, t.x2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.kg, true, t.stream);
+    run(t.z, t.z2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.kg, true, t.stream);
     std::swap(t.x, t.x2);
     std::swap(t.z, t.z2);
     t.layout = QSR_ROW_MAJOR;
 }
 
 void transpose_to_cm(DeviceTableau &t) {
-    // RM: row-tiles J in [0,2k), words I in [0,k).
-    run(t.x, t.x2, t.rm_pitch, t.cm_pitch, 2 * t.k, t.k, false, t.stream);
-    run(t.z, t.z2, t.rm_pitch, t.cm_pitch, 2 * t.k, t.k, false, t.stream);
+    // RM: row-tiles J in [0,2kg), words I in [0,k).
+    run(t.x, t.x2, t.rm_pitch, t.cm_pitch, 2 * t.kg, t.k, false, t.stream);
+    run(t.z, t.z2, t.rm_pitch, t.cm_pitch, 2 * t.kg, t.k, false, t.stream);
     std::swap(t.x, t.x2);
     std::swap(t.z, t.z2);
     t.layout = QSR_COLUMN_MAJOR;

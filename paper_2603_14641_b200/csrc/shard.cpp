@@ -1,0 +1,393 @@
+// Generator-row-sharded single-shot engine: run_single_shot<uint64_t>
+// (reference simulator.hpp:46-76) over `world` shards of the tableau, bit-identical to the
+// unsharded engine for every world size.
+//
+// Sharding. Shard r holds generator-words [j0, j0+kg) of both halves (k*r/world ..
+// k*(r+1)/world), i.e. destabilizers AND stabilizers g = 64*j0 .. 64*(j0+kg)-1, for all n
+// qubits; contiguous blocks, so shard order = generator order. Gate rules act per
+// generator-word (gates.hpp:173-194) and S[j] only receives j's contributions, so gate windows
+// and both transposes are shard-local: zero communication for ~all of the bytes.
+//
+// Measurement window (measure.hpp:381-442), per process:
+//   flags      local find_probabilistic (CM) -> max-all-reduce (u8 per measurement)
+//   collapses  batches of <= 32 flagged measurements (k_batch.cu). The reference's pivot is
+//              the smallest stabilizer with X at q. Each shard ORs its stabilizers' batch-start
+//              bits into a 32-bit mask (all-gather, 4 B per shard). The leader L = the first
+//              shard with bit 0 set holds the global pivot of collapse 0. A shard d < L has no
+//              stabilizer with X at q_m for m < ctz(mask_d): its rows can neither be pivots nor
+//              change before that. So L alone computes pivots, pivot rows and coins for
+//              m < lim = min(b, min_{d<L} ctz(mask_d)); it stops earlier if it has no candidate.
+//              The pivot block (V rows + vinfo) is broadcast from L. Every shard then absorbs it
+//              into its own rows in one pass, including the leader.
+//              No shard with bit 0 => the measurement is deterministic now (measure.hpp:417-421).
+//   deterministic  each shard folds its ordered partial product (k_det_partial), the partials
+//              are all-gathered, and every shard folds them in shard order (associativity of
+//              the ordered product), so every shard knows the outcome.
+//   record     the leader writes collapse entries; a max-all-reduce of the window's record
+//              (zero-initialised everywhere) gives every shard the whole record.
+// Coins: the coin index advances only on collapses, in window order, so the host tracks it
+// and hands it to each batch's leader.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "abi.hpp"
+#include "engine.hpp"
+#include "exchange.hpp"
+
+using namespace qsr;
+
+namespace {
+
+void shard_range(uint64_t n, int world, int rank, uint64_t &j0, uint64_t &kg) {
+    if (n == 0) fail(QSR_INVALID_ARGUMENT, "shard_range: n must be >= 1");
+    const uint64_t k = (n + 63) / 64;
+    if (world < 1 || uint64_t(world) > k)
+        fail(QSR_INVALID_ARGUMENT, "shard_range: world must be in [1, ceil(n/64)]");
+    if (rank < 0 || rank >= world) fail(QSR_INVALID_ARGUMENT, "shard_range: rank out of range");
+    j0 = k * uint64_t(rank) / uint64_t(world);
+    kg = k * uint64_t(rank + 1) / uint64_t(world) - j0;
+}
+
+struct Shard {
+    std::unique_ptr<DeviceTableau> t;
+    uint64_t j0 = 0;
+    qsr_record_entry *d_rec = nullptr;   // whole record (every shard)
+    uint32_t *d_masks = nullptr;         // [world] gathered stabilizer OR-masks
+    uint64_t *det_send = nullptr;        // [det_slot_words]
+    uint64_t *det_recv = nullptr;        // [world][det_slot_words]
+};
+
+} // namespace
+
+struct qsr_sharded {
+    uint64_t n = 0, k = 0;
+    int world = 1;
+    int device = 0;
+    std::vector<Shard> sh;                 // local shards, ascending global rank
+    std::unique_ptr<Exchange> ex;
+    std::unique_ptr<DeviceSchedule> ds;    // one copy per process (all local shards share a device)
+    RunTimes last;
+    uint64_t launches = 0;
+    ~qsr_sharded() {
+        cudaSetDevice(device);
+        for (auto &s : sh) {
+            if (s.t) s.t->sync();
+            for (void *p : {(void *)s.d_rec, (void *)s.d_masks, (void *)s.det_send, (void *)s.det_recv})
+                if (p) cudaFree(p);
+        }
+    }
+
+    int leader_local(int rank) const {
+        for (size_t i = 0; i < sh.size(); ++i)
+            if (ex->ranks[i] == rank) return int(i);
+        return -1;
+    }
+
+    // Deterministic outcome of q into entry `idx` of every shard's window record.
+    void deterministic(uint32_t q, uint64_t idx) {
+        std::vector<const void *> send;
+        std::vector<void *> recv;
+        for (auto &s : sh) {
+            det_local_partial(*s.t, q, s.det_send);
+            send.push_back(s.det_send);
+            recv.push_back(s.det_recv);
+        }
+        const uint64_t sw = det_slot_words(*sh[0].t);
+        ex->allgather(send, recv, sw * 8);
+        for (auto &s : sh) det_combine(*s.t, q, s.det_recv, uint32_t(world), s.t->ms.out + idx);
+    }
+
+    void measure_window(const std::vector<uint32_t> &mq, uint64_t seed, uint64_t &coin,
+                        RunTimes &rt) {
+        const uint64_t m = mq.size();
+        DeviceTableau &t0 = *sh[0].t;
+        cudaEvent_t ev[4];
+        for (auto &e : ev) QSR_CUDA(cudaEventCreate(&e));
+        std::vector<void *> flag_bufs, out_bufs, blocks;
+        for (auto &s : sh) {
+            DeviceTableau &t = *s.t;
+            t.ensure_window_cap(m);
+            QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
+            QSR_CUDA(cudaMemsetAsync(t.ms.out, 0, m * sizeof(qsr_record_entry), t.stream));
+            flags_cm(t, m);
+            flag_bufs.push_back(t.ms.flags);
+            out_bufs.push_back(t.ms.out);
+            blocks.push_back(t.ms.batch_block);
+        }
+        ex->allreduce_max_u8(flag_bufs, m);
+        std::vector<uint8_t> flags(m);
+        QSR_CUDA(cudaMemcpyAsync(flags.data(), t0.ms.flags, m, cudaMemcpyDeviceToHost, t0.stream));
+        QSR_CUDA(cudaEventRecord(ev[0], t0.stream));
+        for (auto &s : sh) transpose_to_rm(*s.t);
+        QSR_CUDA(cudaEventRecord(ev[1], t0.stream));
+        QSR_CUDA(cudaStreamSynchronize(t0.stream));
+
+        std::vector<uint32_t> fq, fidx;
+        for (uint64_t i = 0; i < m; ++i)
+            if (flags[i]) { fq.push_back(mq[i]); fidx.push_back(uint32_t(i)); }
+        if (!fq.empty())
+            for (auto &s : sh) {
+                DeviceTableau &t = *s.t;
+                QSR_CUDA(cudaMemcpyAsync(t.ms.fq, fq.data(), fq.size() * 4, cudaMemcpyHostToDevice, t.stream));
+                QSR_CUDA(cudaMemcpyAsync(t.ms.fidx, fidx.data(), fidx.size() * 4, cudaMemcpyHostToDevice,
+                                         t.stream));
+            }
+        std::vector<uint32_t> masks(world);
+        size_t pos = 0;
+        while (pos < fq.size()) {
+            const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - pos));
+            std::vector<const void *> msend;
+            std::vector<void *> mrecv;
+            for (auto &s : sh) {
+                batch_colbits(*s.t, s.t->ms.fq + pos, b);
+                msend.push_back(s.t->ms.bctl + 2);
+                mrecv.push_back(s.d_masks);
+            }
+            ex->allgather(msend, mrecv, 4);
+            QSR_CUDA(cudaMemcpyAsync(masks.data(), sh[0].d_masks, 4 * world, cudaMemcpyDeviceToHost,
+                                     t0.stream));
+            QSR_CUDA(cudaStreamSynchronize(t0.stream));
+            int L = -1;
+            for (int r = 0; r < world && L < 0; ++r)
+                if (masks[r] & 1u) L = r;
+            if (L < 0) { // no stabilizer anywhere anticommutes with Z_q now: deterministic
+                deterministic(fq[pos], fidx[pos]);
+                ++pos;
+                continue;
+            }
+            uint32_t lim = b;
+            for (int r = 0; r < L; ++r) lim = std::min<uint32_t>(lim, uint32_t(__builtin_ctz(masks[r])));
+            const int li = leader_local(L);
+            if (li >= 0) {
+                DeviceTableau &t = *sh[li].t;
+                QSR_CUDA(cudaMemcpyAsync(t.ms.coin_index, &coin, 8, cudaMemcpyHostToDevice, t.stream));
+                batch_pivots(t, t.ms.fq + pos, t.ms.fidx + pos, lim, seed);
+            }
+            ex->broadcast(blocks, t0.ms.batch_block_bytes, L);
+            for (auto &s : sh) batch_apply(*s.t);
+            uint32_t len = 0;
+            QSR_CUDA(cudaMemcpyAsync(&len, t0.ms.bctl, 4, cudaMemcpyDeviceToHost, t0.stream));
+            QSR_CUDA(cudaStreamSynchronize(t0.stream));
+            if (len == 0) fail(QSR_INTERNAL, "sharded measure: leader found no pivot");
+            coin += len;
+            pos += len;
+        }
+        for (uint64_t i = 0; i < m; ++i)
+            if (!flags[i]) deterministic(mq[i], i);
+        ex->allreduce_max_u8(out_bufs, m * sizeof(qsr_record_entry));
+        QSR_CUDA(cudaEventRecord(ev[2], t0.stream));
+        for (auto &s : sh) transpose_to_cm(*s.t);
+        QSR_CUDA(cudaEventRecord(ev[3], t0.stream));
+        QSR_CUDA(cudaEventSynchronize(ev[3]));
+        float a = 0, b2 = 0, c = 0;
+        QSR_CUDA(cudaEventElapsedTime(&a, ev[0], ev[1]));
+        QSR_CUDA(cudaEventElapsedTime(&b2, ev[1], ev[2]));
+        QSR_CUDA(cudaEventElapsedTime(&c, ev[2], ev[3]));
+        rt.t_ms += a + c;
+        rt.ge_ms += b2;
+        for (auto &e : ev) cudaEventDestroy(e);
+    }
+
+    void run(uint64_t seed) {
+        QSR_CUDA(cudaSetDevice(device));
+        RunTimes rt;
+        DeviceTableau &t0 = *sh[0].t;
+        cudaEvent_t e_start, e_end, a, b;
+        for (auto *e : {&e_start, &e_end, &a, &b}) QSR_CUDA(cudaEventCreate(e));
+        for (auto &s : sh) {
+            s.t->sync();
+            launch_zero_state(*s.t, nullptr);
+        }
+        QSR_CUDA(cudaEventRecord(e_start, t0.stream));
+        uint64_t coin = 0, rec_off = 0;
+        const uint64_t W = ds->is_meas.size();
+        uint64_t w = 0;
+        while (w < W) {
+            if (!ds->is_meas[w]) {
+                QSR_CUDA(cudaEventRecord(a, t0.stream));
+                const uint64_t w0 = w;
+                for (auto &s : sh)
+                    for (w = w0; w < W && !ds->is_meas[w]; ++w)
+                        launch_gate_window(*s.t, ds->d_gates + ds->offsets[w],
+                                           ds->offsets[w + 1] - ds->offsets[w]);
+                rt.gate_windows += w - w0;
+                // Shard 0's stream waits for the others so the event pair brackets all shards.
+                for (size_t i = 1; i < sh.size(); ++i) {
+                    QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
+                    QSR_CUDA(cudaStreamWaitEvent(t0.stream, b, 0));
+                }
+                QSR_CUDA(cudaEventRecord(b, t0.stream));
+                QSR_CUDA(cudaEventSynchronize(b));
+                float ms = 0;
+                QSR_CUDA(cudaEventElapsedTime(&ms, a, b));
+                rt.to_ms += ms;
+                continue;
+            }
+            const auto &mq = ds->mqubits[w];
+            measure_window(mq, seed, coin, rt);
+            for (auto &s : sh)
+                QSR_CUDA(cudaMemcpyAsync(s.d_rec + rec_off, s.t->ms.out, mq.size() * sizeof(qsr_record_entry),
+                                         cudaMemcpyDeviceToDevice, s.t->stream));
+            rec_off += mq.size();
+            ++w;
+        }
+        for (size_t i = 1; i < sh.size(); ++i) {
+            QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
+            QSR_CUDA(cudaStreamWaitEvent(t0.stream, b, 0));
+        }
+        QSR_CUDA(cudaEventRecord(e_end, t0.stream));
+        QSR_CUDA(cudaEventSynchronize(e_end));
+        float total = 0;
+        QSR_CUDA(cudaEventElapsedTime(&total, e_start, e_end));
+        rt.total_ms = total;
+        for (auto e : {e_start, e_end, a, b}) cudaEventDestroy(e);
+        for (auto &s : sh)
+            if (read_error_flag(*s.t))
+                fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+        last = rt;
+    }
+};
+
+extern "C" {
+
+qsr_status qsr_shard_range(uint64_t n, int world, int rank, uint64_t *j0, uint64_t *kg) {
+    return guard([&] {
+        REQUIRE_PTR(j0);
+        REQUIRE_PTR(kg);
+        shard_range(n, world, rank, *j0, *kg);
+    });
+}
+
+qsr_status qsr_nccl_unique_id(uint8_t out[128]) {
+    return guard([&] {
+        REQUIRE_PTR(out);
+        nccl_unique_id(out);
+    });
+}
+
+qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
+                              const qsr_shard_config *cfg, qsr_sharded **out) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        REQUIRE_PTR(cfg);
+        REQUIRE_PTR(out);
+        const Circuit &circ = *c;
+        auto e = std::make_unique<qsr_sharded>();
+        e->n = circ.num_qubits;
+        e->world = cfg->world;
+        e->device = cfg->device;
+        if (e->n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
+        e->k = (e->n + 63) / 64;
+        if (cfg->world < 1 || uint64_t(cfg->world) > e->k)
+            fail(QSR_INVALID_ARGUMENT, "sharded: world must be in [1, ceil(n/64)]");
+        std::vector<int> my_ranks;
+        if (cfg->exchange == QSR_EXCHANGE_LOCAL) {
+            for (int r = 0; r < cfg->world; ++r) my_ranks.push_back(r);
+        } else if (cfg->exchange == QSR_EXCHANGE_NCCL) {
+            REQUIRE_PTR(cfg->nccl_id);
+            my_ranks.push_back(cfg->rank);
+        } else {
+            fail(QSR_INVALID_ARGUMENT, "sharded: unknown exchange");
+        }
+        QSR_CUDA(cudaSetDevice(cfg->device));
+        std::vector<cudaStream_t> streams;
+        for (int r : my_ranks) {
+            uint64_t j0 = 0, kg = 0;
+            shard_range(e->n, cfg->world, r, j0, kg);
+            Shard sd;
+            sd.j0 = j0;
+            sd.t = std::make_unique<DeviceTableau>(e->n, cfg->device, j0, kg);
+            streams.push_back(sd.t->stream);
+            e->sh.push_back(std::move(sd));
+        }
+        e->ds = s ? upload_schedule(e->n, *s, cfg->device,
+                                    e->sh[0].t->stream)
+                  : upload_circuit(circ, cfg->device, e->sh[0].t->stream);
+        if (e->ds->measure_count != circ.measure_count())
+            fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
+        const uint64_t nm = std::max<uint64_t>(e->ds->measure_count, 1);
+        for (auto &sd : e->sh) {
+            const uint64_t sw = det_slot_words(*sd.t);
+            QSR_CUDA(cudaMalloc(&sd.d_rec, nm * sizeof(qsr_record_entry)));
+            QSR_CUDA(cudaMalloc(&sd.d_masks, 4 * size_t(cfg->world)));
+            QSR_CUDA(cudaMalloc(&sd.det_send, sw * 8));
+            QSR_CUDA(cudaMemset(sd.det_send, 0, sw * 8));
+            QSR_CUDA(cudaMalloc(&sd.det_recv, sw * 8 * size_t(cfg->world)));
+        }
+        if (cfg->exchange == QSR_EXCHANGE_LOCAL)
+            e->ex = make_local_exchange(cfg->world, streams);
+        else
+            e->ex = make_nccl_exchange(cfg->world, cfg->rank, streams[0], cfg->nccl_id);
+        QSR_CUDA(cudaDeviceSynchronize());
+        *out = e.release();
+    });
+}
+
+qsr_status qsr_sharded_run(qsr_sharded *e, uint64_t seed, double *device_ms) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        const uint64_t l0 = g_launches;
+        e->run(seed);
+        e->launches = g_launches - l0;
+        if (device_ms) *device_ms = e->last.total_ms;
+    });
+}
+
+qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *gate_launches,
+                             double *transpose_ms, double *measure_ms, uint64_t *launches) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        if (gate_ms) *gate_ms = e->last.to_ms;
+        if (gate_launches) *gate_launches = e->last.gate_windows * e->sh.size();
+        if (transpose_ms) *transpose_ms = e->last.t_ms;
+        if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
+        if (launches) *launches = e->launches;
+    });
+}
+
+qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        const uint64_t nm = e->ds->measure_count;
+        if (!nm) return;
+        REQUIRE_PTR(record);
+        QSR_CUDA(cudaSetDevice(e->device));
+        const Shard &s = e->sh[0];
+        QSR_CUDA(cudaMemcpyAsync(record, s.d_rec, nm * sizeof(qsr_record_entry), cudaMemcpyDeviceToHost,
+                                 s.t->stream));
+        s.t->sync();
+    });
+}
+
+qsr_status qsr_sharded_tableau(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        QSR_CUDA(cudaSetDevice(e->device));
+        const uint64_t k = e->k, n_pad = 64 * k;
+        for (const Shard &sd : e->sh) {
+            DeviceTableau &t = *sd.t;
+            if (t.layout != QSR_COLUMN_MAJOR) fail(QSR_INTERNAL, "sharded tableau not ColumnMajor");
+            // Destabilizer words j0.. and stabilizer words k+j0.. of every qubit row.
+            for (int plane = 0; plane < 2; ++plane) {
+                uint64_t *dst = plane ? z : x;
+                const uint64_t *src = plane ? t.z : t.x;
+                if (!dst) continue;
+                QSR_CUDA(cudaMemcpy2DAsync(dst + sd.j0, 2 * k * 8, src, t.cm_pitch * 8, t.kg * 8, n_pad,
+                                           cudaMemcpyDeviceToHost, t.stream));
+                QSR_CUDA(cudaMemcpy2DAsync(dst + k + sd.j0, 2 * k * 8, src + t.kg, t.cm_pitch * 8,
+                                           t.kg * 8, n_pad, cudaMemcpyDeviceToHost, t.stream));
+            }
+            if (s) {
+                QSR_CUDA(cudaMemcpyAsync(s + sd.j0, t.s, t.kg * 8, cudaMemcpyDeviceToHost, t.stream));
+                QSR_CUDA(cudaMemcpyAsync(s + k + sd.j0, t.s + t.kg, t.kg * 8, cudaMemcpyDeviceToHost,
+                                         t.stream));
+            }
+            t.sync();
+        }
+    });
+}
+
+void qsr_sharded_destroy(qsr_sharded *e) { delete e; }
+
+} // extern "C"

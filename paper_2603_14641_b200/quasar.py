@@ -23,7 +23,8 @@ __all__ = [
     "PivotList", "PhaseTimers", "RunReport", "SingleShotResult", "apply_window", "measure_window",
     "find_probabilistic", "find_and_compact_pivots", "parallel_ge", "swap_anti_commuting",
     "inject_x", "deterministic_outcome", "run_single_shot", "FrameTableau", "init_frames",
-    "apply_window_frames", "ShotRecord", "measure_sample", "sample", "Engine",
+    "apply_window_frames", "ShotRecord", "measure_sample", "sample", "Engine", "ShardedEngine",
+    "shard_range", "nccl_unique_id", "sample_shard",
     "kStreamMeasure", "kStreamFrames", "kStreamGenerator", "kGeBlockTargets",
     "InvalidArgument", "OutOfRange", "LogicError", "CudaError", "QuasarError",
 ]
@@ -659,6 +660,91 @@ class Engine:
         return x, z, s
 
 
+# ---- generator-row-sharded engine ------------------------------------
+def shard_range(n: int, world: int, rank: int) -> Tuple[int, int]:
+    """Generator-word range (j0, kg) of shard `rank` of `world` for n qubits (host only)."""
+    j0, kg = C.c_uint64(), C.c_uint64()
+    check(lib.qsr_shard_range(n, world, rank, C.byref(j0), C.byref(kg)))
+    return j0.value, kg.value
+
+
+def _pin_nccl() -> None:
+    """libqsr binds the NCCL already mapped into the process. Importing torch first maps
+    torch's bundled NCCL, so libqsr and torch.distributed share one NCCL (loading the older
+    system libnccl.so.2 first would break torch's own import later in the process)."""
+    try:
+        import torch  # noqa: F401
+    except ImportError:
+        pass
+
+
+def nccl_unique_id() -> bytes:
+    """ncclUniqueId (128 bytes) for the sharded engine's NCCL exchange; rank 0 creates it."""
+    _pin_nccl()
+    buf = (C.c_uint8 * 128)()
+    check(lib.qsr_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class ShardedEngine:
+    """run_single_shot on a tableau split by generator-words over `world` shards.
+
+    exchange="local": all shards in this process on `device` (the multi-GPU protocol on one
+    GPU). exchange="nccl": this process drives shard `rank` (one process per GPU); every rank
+    passes the same 128-byte `nccl_id` and the constructor is collective."""
+
+    def __init__(self, circuit: Circuit, world: int, device: int = 0, exchange: str = "local",
+                 rank: int = 0, nccl_id: Optional[bytes] = None, schedule: Optional[Schedule] = None):
+        cfg = _lib.ShardConfig_t()
+        cfg.world, cfg.rank, cfg.device = world, rank, device
+        cfg.exchange = {"local": _lib.EXCHANGE_LOCAL, "nccl": _lib.EXCHANGE_NCCL}[exchange]
+        self._id = None
+        if exchange == "nccl":
+            _pin_nccl()
+        if nccl_id is not None:
+            self._id = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            cfg.nccl_id = C.cast(self._id, C.POINTER(C.c_uint8))
+        h = C.c_void_p()
+        check(lib.qsr_sharded_create(circuit._h, schedule._h if schedule is not None else None,
+                                     C.byref(cfg), C.byref(h)))
+        self._h = h
+        self._nm = circuit.measure_count()
+        self.n = circuit.num_qubits
+        self.world, self.rank, self.exchange = world, rank, exchange
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.qsr_sharded_destroy(self._h)
+            self._h = None
+
+    def run(self, seed: int) -> float:
+        ms = C.c_double()
+        check(lib.qsr_sharded_run(self._h, seed, C.byref(ms)))
+        return ms.value
+
+    def stats(self) -> dict:
+        g, gl, t, m, l = C.c_double(), C.c_uint64(), C.c_double(), C.c_double(), C.c_uint64()
+        check(lib.qsr_sharded_stats(self._h, C.byref(g), C.byref(gl), C.byref(t), C.byref(m), C.byref(l)))
+        return {"gate_ms": g.value, "gate_launches": gl.value, "transpose_ms": t.value,
+                "measure_ms": m.value, "launches": l.value}
+
+    def record(self) -> np.ndarray:
+        rec = np.zeros(max(self._nm, 1), dtype=ENTRY_DTYPE)
+        check(lib.qsr_sharded_record(self._h, ptr(rec)))
+        return rec[:self._nm]
+
+    def tableau_planes(self, x=None, z=None, s=None):
+        """Reference-layout CM planes; only this process's shard columns are written (all of
+        them with exchange="local"). Pass zero-filled buffers to combine ranks by XOR/OR."""
+        k = (self.n + 63) // 64
+        if x is None:
+            x = np.zeros(64 * k * 2 * k, dtype=np.uint64)
+            z = np.zeros_like(x)
+            s = np.zeros(2 * k, dtype=np.uint64)
+        check(lib.qsr_sharded_tableau(self._h, ptr(x, C.c_uint64), ptr(z, C.c_uint64), ptr(s, C.c_uint64)))
+        return x, z, s
+
+
 # ---- Pauli frames (frames.hpp:32-204) -------------------------------------------------
 class FrameTableau:
     w = 64
@@ -763,6 +849,22 @@ def sample(circuit: Circuit, shots: int, seed: int, report: Optional[RunReport] 
         r = RunReport.from_c(rep)
         report.__dict__.update(r.__dict__)
     return f.record()
+
+
+def sample_shard(circuit: Circuit, shots: int, seed: int, world: int, rank: int,
+                 report: Optional[RunReport] = None, device: int = 0) -> Tuple[int, ShotRecord]:
+    """sample() sharded by shot: this rank's shot-word slice. Returns (w0, record) where the
+    record's rows hold the slice's kf = nw words (global words w0 .. w0+nw-1)."""
+    h = C.c_void_p()
+    rep = _lib.Report_t()
+    check(lib.qsr_sample_shard(circuit._h, shots, seed, world, rank, device, C.byref(h), C.byref(rep)))
+    f = FrameTableau(h)
+    if report is not None:
+        r = RunReport.from_c(rep)
+        report.__dict__.update(r.__dict__)
+    j0, nw = C.c_uint64(), C.c_uint64()
+    check(lib.qsr_frames_shot_words(h, C.byref(j0), C.byref(nw)))
+    return j0.value, f.record()
 
 
 def device_count() -> int:
