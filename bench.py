@@ -33,11 +33,14 @@ sys.path.insert(0, str(ROOT))
 CONFIGS = {
     "c1": dict(n=1000, depth=100, seed=42, p=1.0, run_seed=7),
     "c2": dict(n=20000, depth=1000, seed=42, p=0.0, run_seed=7),
+    "c3": dict(n=50000, depth=100, seed=1000, p=1.0, run_seed=7, segments=10),
     "c5": dict(n=180000, depth=1000, seed=42, p=0.01, run_seed=7),
 }
 DESCR = {
     "c1": "random Clifford, 1,000 qubits, depth 100, measure all (generate_random seed 42, run seed 7)",
     "c2": "random Clifford, 20,000 qubits, depth 1,000 (generate_random seed 42, run seed 7)",
+    "c3": "mid-circuit-measurement-heavy: 50,000 qubits, 10 segments generate_random(50000,100,1000+r,1.0) "
+          "(100 layers then measure every qubit), run seed 7",
     "c5": "paper headline: random Clifford+measure, 180,000 qubits, depth 1,000, "
           "Bernoulli(0.01) final measurements (generate_random(180000,1000,42,0.01), run seed 7)",
 }
@@ -178,7 +181,12 @@ def main():
     from paper_2603_14641_b200 import quasar as q
     device = local
     t0 = time.time()
-    circ = q.generate_random(cfg["n"], cfg["depth"], cfg["seed"], cfg["p"])
+    if cfg.get("segments"):  # concatenated measure-all segments
+        circ = q.Circuit(cfg["n"], np.concatenate(
+            [q.generate_random(cfg["n"], cfg["depth"], cfg["seed"] + r, cfg["p"]).gate_array
+             for r in range(cfg["segments"])]))
+    else:
+        circ = q.generate_random(cfg["n"], cfg["depth"], cfg["seed"], cfg["p"])
     G = len(circ)
     nm = circ.measure_count()
     log(f"[rank {rank}] generated {G} gates ({nm} measurements) in {time.time() - t0:.1f}s")

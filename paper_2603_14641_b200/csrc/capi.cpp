@@ -71,15 +71,18 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
     QSR_CUDA(cudaMalloc(&ms.colbits, 2 * ng * 4));
     {
         const uint64_t vwords = uint64_t(kMaxBatch) * 2 * rm_pitch;
-        const uint64_t info_words = (4 * kMaxBatch + 4) / 2;
+        const uint64_t info_words = (kVinfoWords + 4 + 1) / 2;
         ms.batch_block_bytes = (vwords + info_words) * 8;
         alloc(&ms.batch_block, vwords + info_words);
         ms.Vx = ms.batch_block;
         ms.Vz = ms.batch_block + rm_pitch;
         ms.vstride = 2 * rm_pitch;
         ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
-        ms.bctl = ms.vinfo + 4 * kMaxBatch;
+        ms.bctl = ms.vinfo + kVinfoWords;
     }
+    QSR_CUDA(cudaMalloc(&ms.gconst, kMaxBatch / 4 * 4));
+    QSR_CUDA(cudaMalloc(&ms.nz, (ng / 32 + 1) * 4));
+    QSR_CUDA(cudaMalloc(&ms.pcount, 2 * kMaxBatch * sizeof(int)));
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
 }
@@ -92,7 +95,7 @@ DeviceTableau::~DeviceTableau() {
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
                     (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits,
-                    (void *)ms.batch_block, (void *)ms.fq,
+                    (void *)ms.batch_block, (void *)ms.partial, (void *)ms.gconst, (void *)ms.nz, (void *)ms.pcount, (void *)ms.fq,
                     (void *)ms.fidx, (void *)ms.coin_buf})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);

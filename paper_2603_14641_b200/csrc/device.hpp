@@ -30,6 +30,7 @@ inline void count_launch(uint64_t n = 1) { g_launches += n; }
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
+constexpr int kVinfoWords = 5 * kMaxBatch; // per-batch pivot info (k_batch.cu)
 
 // Scratch used by the measurement pipeline; sized for one tableau.
 struct MeasureScratch {
@@ -49,13 +50,18 @@ struct MeasureScratch {
     uint32_t *colbits = nullptr;    // [2*ng] column bits at the batch's qubits
     // One contiguous batch block (broadcast as a unit by the sharded engine):
     //   V rows  [kMaxBatch][2][rm_pitch] (x words then z words of pivot row m)
-    //   vinfo   [4*kMaxBatch] u32, bctl [4] u32 (len, stopped, stabilizer OR-mask, -)
+    //   vinfo   [kVinfoWords] u32, bctl [4] u32 (len, stopped, stabilizer OR-mask, -)
     uint64_t *batch_block = nullptr;
     uint64_t batch_block_bytes = 0;
     uint64_t *Vx = nullptr, *Vz = nullptr; // views into batch_block, row stride vstride
     uint64_t vstride = 0;
     uint32_t *vinfo = nullptr;
     uint32_t *bctl = nullptr;
+    uint8_t *partial = nullptr;     // [slices][2ng] per-(row, slice) phase bytes (k_batch.cu)
+    uint64_t partial_bytes = 0;
+    uint32_t *gconst = nullptr;     // [kMaxBatch/4] per-group pair-parity constants
+    uint32_t *nz = nullptr;         // [ng/32] active-stabilizer ballot of the batch
+    int *pcount = nullptr;          // [2*kMaxBatch] per-pivot phase / beta counters
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
     // Caller-drawn coins for the current measurement window (nullptr = device Philox).
     uint8_t *coin_table = nullptr;

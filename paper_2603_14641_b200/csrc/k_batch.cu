@@ -28,6 +28,8 @@
 // Traffic: one read + write of the touched rows per batch instead of per collapse; the pivot
 // rows are staged through shared memory (cp.async, double-buffered 64-word slices) and each
 // staged word is reused by the 4 rows a warp carries.
+#include <string>
+
 #include "common.cuh"
 #include "device.hpp"
 
@@ -38,8 +40,9 @@ namespace {
 using u64 = unsigned long long;
 constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
 enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2 };
-// vinfo layout (u32 [4*kB]): vb | sign of V_m | c_m | beta(V_m) mod 4
-enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB };
+// vinfo layout (u32 [5*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m
+enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_MC = 4 * kB };
+static_assert(5 * kB == kVinfoWords, "vinfo layout");
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
 
@@ -74,7 +77,8 @@ __device__ __forceinline__ int block_sum(int v, int *red /* >= 32 ints */) {
 // X at q_m at batch start (the sharded leader protocol, shard.cpp).
 __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64_t nrows,
                           uint64_t ng, const uint32_t *__restrict__ fq, uint32_t b,
-                          uint32_t *__restrict__ colbits, uint32_t *__restrict__ stab_or) {
+                          uint32_t *__restrict__ colbits, uint32_t *__restrict__ stab_or,
+                          uint32_t *__restrict__ nz) {
     __shared__ uint32_t sq[kB];
     if (threadIdx.x < b) sq[threadIdx.x] = fq[threadIdx.x];
     __syncthreads();
@@ -90,6 +94,240 @@ __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64
     }
     const uint32_t any = __reduce_or_sync(0xffffffffu, r >= ng && r < nrows ? bits : 0u);
     if ((threadIdx.x & 31) == 0 && any) atomicOr(stab_or, any);
+    // Active-stabilizer ballot (bits != 0): rows with no X at any batch qubit can never be a
+    // pivot or absorb anything in this batch.
+    const uint32_t act = __ballot_sync(0xffffffffu, r >= ng && r < nrows && bits != 0);
+    if ((threadIdx.x & 31) == 0 && r >= ng && r < nrows) nz[(r - ng) >> 5] = act;
+}
+
+// ---- phase B, split: B1 select (32-bit column logic only), B2 pivot rows (word-parallel),
+// B3 signs / coins / record (one warp) ---------------------------------------------------
+// B1. The pivot of collapse m, its memberships Mc_m and the X bits of V_m at the batch's
+// qubits (vb_m) need only column bits: vb_m = cb(c_m) ^ XOR_{j in Mc_m} vb_j, because V_m is
+// S_{c_m}(batch start) times the V_j it absorbed. The candidates are the first kWin active
+// stabilizers (ascending, compacted from the nz ballot); each thread keeps their memberships
+// incrementally, so a step is O(1) per candidate. If none of them qualifies, the stabilizers
+// after the window are scanned with memberships recomputed from the column bits.
+constexpr int kSelThreads = 256;
+constexpr int kSelRows = 4;
+constexpr int kWin = kSelThreads * kSelRows;
+
+__global__ void __launch_bounds__(kSelThreads)
+k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
+               uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
+               uint32_t *__restrict__ bctl) {
+    __shared__ uint32_t s_rows[kWin];
+    __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
+    __shared__ uint32_t s_scan[kSelThreads / 32];
+    __shared__ uint32_t s_nwin, s_next, s_min, s_len, s_stop;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t nzw = (n_gen + 31) / 32;
+    if (tid < kB) s_vbcol[tid] = 0;
+    if (tid == 0) { s_nwin = 0; s_next = uint32_t(n_gen); s_len = b; s_stop = 0; }
+    __syncthreads();
+    // Window: the first kWin active stabilizers in ascending order.
+    for (uint64_t base = 0; base < nzw; base += kSelThreads) {
+        const uint64_t w = base + tid;
+        const uint32_t word = w < nzw ? nz[w] : 0u;
+        const uint32_t cnt = __popc(word);
+        uint32_t incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += v;
+        }
+        if (lane == 31) s_scan[warp] = incl;
+        __syncthreads();
+        uint32_t off = s_nwin;
+        for (uint32_t i = 0; i < warp; ++i) off += s_scan[i];
+        uint32_t pos = off + incl - cnt;
+        for (uint32_t v = word; v && pos < uint32_t(kWin); v &= v - 1, ++pos) {
+            const uint32_t row = uint32_t(w * 32 + __ffs(v) - 1);
+            s_rows[pos] = row;
+            if (pos == uint32_t(kWin) - 1) s_next = row + 1;
+        }
+        __syncthreads();
+        if (tid == kSelThreads - 1) s_nwin = min(off + incl, uint32_t(kWin));
+        __syncthreads();
+        if (s_nwin >= uint32_t(kWin)) break;
+    }
+    const uint32_t nwin = s_nwin;
+    uint32_t row[kSelRows], cb[kSelRows], M[kSelRows];
+#pragma unroll
+    for (int u = 0; u < kSelRows; ++u) {
+        const uint32_t e = tid + u * kSelThreads;
+        row[u] = e < nwin ? s_rows[e] : 0xFFFFFFFFu;
+        cb[u] = e < nwin ? colbits[ng + row[u]] : 0u;
+        M[u] = 0;
+    }
+    for (uint32_t m = 0; m < b; ++m) {
+        if (tid == 0) s_min = 0xFFFFFFFFu;
+        __syncthreads();
+        const uint32_t vc = s_vbcol[m];
+        uint32_t best = 0xFFFFFFFFu, bits = 0;
+#pragma unroll
+        for (int u = 0; u < kSelRows; ++u) {
+            const uint32_t bit = ((cb[u] >> m) ^ parity32(M[u] & vc)) & 1u;
+            bits |= bit << u;
+            if (bit) best = min(best, row[u]); // used pivots hold no X bit any more (cb masked)
+        }
+        best = __reduce_min_sync(0xffffffffu, best);
+        if (lane == 0 && best != 0xFFFFFFFFu) atomicMin(&s_min, best);
+        __syncthreads();
+        if (s_min == 0xFFFFFFFFu) {
+            // Fallback: stabilizers after the window, memberships from the column bits.
+            for (uint64_t g0r = s_next; g0r < n_gen; g0r += kSelThreads) {
+                const uint64_t g = g0r + tid;
+                uint32_t cand = 0xFFFFFFFFu;
+                if (g < n_gen) {
+                    bool used = false;
+                    for (uint32_t j = 0; j < m; ++j) used |= s_c[j] == uint32_t(g);
+                    const uint32_t cbg = colbits[ng + g];
+                    if (!used && cbg) {
+                        const uint32_t Mg = membership(cbg, s_vbcol, 0, m);
+                        if (((cbg >> m) ^ parity32(Mg & vc)) & 1u) cand = uint32_t(g);
+                    }
+                }
+                cand = __reduce_min_sync(0xffffffffu, cand);
+                if (lane == 0 && cand != 0xFFFFFFFFu) atomicMin(&s_min, cand);
+                __syncthreads();
+                if (s_min != 0xFFFFFFFFu) break;
+                __syncthreads();
+            }
+        }
+        if (s_min == 0xFFFFFFFFu) { // no stabilizer anticommutes with Z_{q_m}: batch ends here
+            if (tid == 0) { s_len = m; s_stop = 1; }
+            break;
+        }
+        const uint32_t c = s_min;
+        if (tid == 0) {
+            const uint32_t cbc = colbits[ng + c];
+            const uint32_t Mc = membership(cbc, s_vbcol, 0, m);
+            uint32_t vb = cbc;
+            for (uint32_t U = Mc; U; U &= U - 1) vb ^= s_vb[__ffs(U) - 1];
+            s_vb[m] = vb;
+            s_c[m] = c;
+            s_mc[m] = Mc;
+        }
+        __syncthreads();
+        if (tid < kB) s_vbcol[tid] |= ((s_vb[m] >> tid) & 1u) << m;
+#pragma unroll
+        for (int u = 0; u < kSelRows; ++u) {
+            if (row[u] == c) { cb[u] = 0; M[u] = 0; row[u] = 0xFFFFFFFFu; } // now +/-Z_q: inert
+            else if ((bits >> u) & 1u) M[u] |= 1u << m;
+        }
+        __syncthreads();
+    }
+    __syncthreads();
+    const uint32_t len = s_len;
+    if (tid < kB) {
+        const bool v = tid < len;
+        vinfo[VI_VB + tid] = v ? s_vb[tid] : 0u;
+        vinfo[VI_C + tid] = v ? uint32_t(g0 + s_c[tid]) : 0xFFFFFFFFu; // global generator
+        vinfo[VI_MC + tid] = v ? s_mc[tid] : 0u;
+    }
+    if (tid == 0) {
+        bctl[BL_LEN] = len;
+        bctl[BL_DET] = s_stop;
+    }
+}
+
+// B2. Pivot rows, word-parallel: thread = word i of every V_m (m in order, V_j of the same
+// word kept in shared memory), with the telescoped phase pieces of each V_m reduced into
+// pcount[m] (E part) and pcount[kB + m] (beta(V_m)). Then the pivot pairs are replaced
+// (D_c <- V_m, S_c <- Z_{q_m}); each word is read and rewritten by one thread only.
+constexpr int kRowThreads = 64;
+
+__global__ void __launch_bounds__(kRowThreads)
+k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t ng,
+             uint64_t g0, const uint32_t *__restrict__ fq, uint64_t *__restrict__ Vx,
+             uint64_t *__restrict__ Vz, uint64_t vstride, const uint32_t *__restrict__ vinfo,
+             const uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
+    __shared__ u64 sv[kB][2][kRowThreads];
+    __shared__ uint32_t s_c[kB], s_mc[kB], s_q[kB];
+    const uint32_t len = bctl[BL_LEN];
+    if (len == 0) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    if (tid < kB) {
+        s_c[tid] = tid < len ? uint32_t(vinfo[VI_C + tid] - g0) : 0u;
+        s_mc[tid] = tid < len ? vinfo[VI_MC + tid] : 0u;
+        s_q[tid] = tid < len ? fq[tid] : 0u;
+    }
+    __syncthreads();
+    const uint64_t i = uint64_t(blockIdx.x) * kRowThreads + tid;
+    const bool act = i < pitch;
+    for (uint32_t m = 0; m < len; ++m) {
+        const uint64_t rs = ng + s_c[m];
+        u64 cx = act ? x[rs * pitch + i] : 0ull, cz = act ? z[rs * pitch + i] : 0ull;
+        int e = __popcll(cx & cz);
+        u64 acc = 0;
+        for (uint32_t U = s_mc[m]; U; U &= U - 1) {
+            const uint32_t j = __ffs(U) - 1;
+            const u64 vx = sv[j][0][tid], vz = sv[j][1][tid];
+            acc ^= vz & cx;
+            cx ^= vx;
+            cz ^= vz;
+        }
+        const int bend = __popcll(cx & cz);
+        e += 2 * (__popcll(acc) & 1) - bend;
+        sv[m][0][tid] = cx;
+        sv[m][1][tid] = cz;
+        if (act) {
+            Vx[uint64_t(m) * vstride + i] = cx;
+            Vz[uint64_t(m) * vstride + i] = cz;
+        }
+        const int es = warp_sum(e), bs = warp_sum(bend);
+        if (lane == 0) {
+            if (es) atomicAdd(pcount + m, es);
+            if (bs) atomicAdd(pcount + kB + m, bs);
+        }
+    }
+    if (!act) return;
+    // Replace the pivot pairs: D_c <- V_m (bits), S_c <- Z_{q_m}.
+    for (uint32_t m = 0; m < len; ++m) {
+        const uint64_t c = s_c[m], q = s_q[m];
+        x[c * pitch + i] = sv[m][0][tid];
+        z[c * pitch + i] = sv[m][1][tid];
+        x[(ng + c) * pitch + i] = 0ull;
+        z[(ng + c) * pitch + i] = i == (q >> 6) ? (1ull << (q & 63)) : 0ull;
+    }
+}
+
+// B3. Signs of the V_m (telescoped phase, file header), coins, record entries and the signs of
+// the replaced pairs, in collapse order (one thread; len <= 32 steps).
+__global__ void k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
+                               const uint32_t *__restrict__ fq, const uint32_t *__restrict__ fidx,
+                               uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
+                               const int *__restrict__ pcount, uint64_t seed,
+                               uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
+                               int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
+    if (threadIdx.x != 0) return;
+    const uint32_t len = bctl[BL_LEN];
+    uint32_t vsign[kB], beta[kB];
+    uint64_t idx = *coin_index;
+    for (uint32_t m = 0; m < len; ++m) {
+        const uint64_t c = vinfo[VI_C + m] - g0, rs = ng + c, rd = c;
+        const uint32_t Mc = vinfo[VI_MC + m];
+        int E = pcount[m];
+        uint32_t sign = uint32_t((s[rs >> 6] >> (rs & 63)) & 1u);
+        for (uint32_t U = Mc; U; U &= U - 1) {
+            const uint32_t j = __ffs(U) - 1;
+            E += int(beta[j]);
+            sign ^= vsign[j];
+        }
+        if (E & 1) atomicExch(err, 1);
+        sign ^= (uint32_t(E) >> 1) & 1u;
+        vsign[m] = sign;
+        beta[m] = uint32_t(pcount[kB + m]) & 3u;
+        const uint32_t coin = draw_coin(seed, idx, coin_table);
+        ++idx;
+        out[fidx[m]] = qsr_record_entry{fq[m], uint8_t(coin), 0};
+        s[rd >> 6] = (s[rd >> 6] & ~(1ull << (rd & 63))) | (uint64_t(sign) << (rd & 63));
+        s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (uint64_t(coin) << (rs & 63));
+        vinfo[VI_SIGN + m] = sign;
+        vinfo[VI_BETA + m] = beta[m];
+    }
+    for (uint32_t m = len; m < kB; ++m) vinfo[VI_SIGN + m] = 0, vinfo[VI_BETA + m] = 0;
+    *coin_index = idx;
 }
 
 // ---- phase B: pivots, pivot rows, coins (one CTA) --------------------------------------
@@ -383,6 +621,240 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
     }
 }
 
+
+// ---- phase C (table form): membership pass, slice-major absorb pass, sign pass --------
+// C1 k_batch_member: M[r] (bit m = row r absorbs V_m) for every row, written over colbits;
+//    blocks >= row_blocks compute the per-group pair constants (below).
+// C2 k_batch_absorb: persistent, one CTA per SM walks (slice, row) items slice-major; for its
+//    64-word slice it stages, per group of 4 consecutive V's, all 16 XOR combinations
+//    T[g][S] = XOR_{j in S} V_{4g+j} (x and z) in shared memory. A row absorbs the group's
+//    members S = (M >> 4g) & 15 in ONE step: cur ^= T[g][S], and the phase accumulator takes
+//    acc ^= T_z[g][S] & cur_x(before). Absorbing V's one by one would give
+//    acc ^= V_jz & (cur_x ^ XOR_{j'<j in S} V_j'x), so the difference is the row-independent
+//    parity c_S = parity(sum_{j'<j in S} |V_jz & V_j'x|), added in C3. Per (row, slice) it
+//    stores (sum beta(start) - beta(end) + 2 parity(acc)) mod 4 as one byte.
+// C3 k_batch_signs: per row, sums its slice bytes, adds sum beta(V_j), the c_S of its groups
+//    and the V signs (file header), and flips the sign bit; a warp ballot forms each 32-bit
+//    half-word of the sign vector (one writer per half-word, no atomics).
+constexpr int kAThreads = 512;
+constexpr int kAWarps = kAThreads / 32;
+constexpr int kARows = 4;                    // rows in flight per warp
+constexpr int kGroups = kB / 4;              // 8 groups of 4 V's
+constexpr size_t kTableWords = size_t(kGroups) * 16 * 2 * kSlice; // 128 KB
+constexpr size_t kAbsorbSmem = kTableWords * sizeof(u64);
+
+__global__ void __launch_bounds__(256)
+k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint64_t g0,
+               const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
+               uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
+               uint32_t *__restrict__ gconst, uint32_t row_blocks) {
+    __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
+    const uint32_t len = bctl[BL_LEN];
+    const uint32_t tid = threadIdx.x;
+    if (blockIdx.x >= row_blocks) {
+        // Pair parities P(j', j) = parity(sum_i |V_jz[i] & V_j'x[i]|), j' < j in group g, then
+        // c_S for all 16 subsets S of the group -> gconst[g] (bit S).
+        const uint32_t g = blockIdx.x - row_blocks;
+        __shared__ uint32_t s_par[6];
+        if (tid < 6) s_par[tid] = 0;
+        __syncthreads();
+        const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {1, 2, 3, 2, 3, 3}; // (j', j)
+        uint32_t loc[6] = {0, 0, 0, 0, 0, 0};
+        for (uint64_t i = tid; i < k; i += blockDim.x) {
+            u64 vx[4], vz[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t j = 4 * g + b;
+                vx[b] = j < len ? Vx[uint64_t(j) * vstride + i] : 0ull;
+                vz[b] = j < len ? Vz[uint64_t(j) * vstride + i] : 0ull;
+            }
+#pragma unroll
+            for (int p = 0; p < 6; ++p) loc[p] ^= __popcll(vz[pb[p]] & vx[pa[p]]) & 1u;
+        }
+#pragma unroll
+        for (int p = 0; p < 6; ++p) {
+            const uint32_t v = __reduce_xor_sync(0xffffffffu, loc[p]);
+            if ((tid & 31) == 0 && v) atomicXor(&s_par[p], 1u);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t mask = 0;
+            for (uint32_t S = 0; S < 16; ++S) {
+                uint32_t c = 0;
+                for (int p = 0; p < 6; ++p)
+                    if (((S >> pa[p]) & 1u) && ((S >> pb[p]) & 1u)) c ^= s_par[p];
+                mask |= c << S;
+            }
+            gconst[g] = mask;
+        }
+        return;
+    }
+    if (tid < kB) {
+        s_vb[tid] = vinfo[VI_VB + tid];
+        const uint32_t cg = vinfo[VI_C + tid];
+        s_c[tid] = (cg != 0xFFFFFFFFu && cg >= g0 && cg < g0 + ng) ? uint32_t(cg - g0) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    if (tid < kB) {
+        uint32_t col = 0;
+        for (uint32_t mp = 0; mp < len && mp < tid; ++mp) col |= ((s_vb[mp] >> tid) & 1u) << mp;
+        s_vbcol[tid] = col;
+    }
+    __syncthreads();
+    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
+    if (r >= nrows || len == 0) return;
+    // Pivot stabilizers are final already; replaced destabilizers restart from V_m after
+    // collapse m; every other row starts from its batch-start column bits.
+    uint32_t cb = colbits[r], start = 0;
+    bool skip = false;
+    for (uint32_t j = 0; j < len; ++j) {
+        if (s_c[j] == 0xFFFFFFFFu) continue;
+        if (r == ng + s_c[j]) skip = true;
+        if (r == s_c[j]) { cb = s_vb[j]; start = j + 1; }
+    }
+    colbits[r] = skip ? 0u : membership(cb, s_vbcol, start, len);
+}
+
+__global__ void __launch_bounds__(kAThreads, 1)
+k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
+               uint64_t nrows, const uint32_t *__restrict__ member,
+               const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
+               const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial) {
+    extern __shared__ __align__(16) u64 tab[]; // [g][S][plane][kSlice]
+    const uint32_t len = bctl[BL_LEN];
+    if (len == 0) return;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t ngroups = (len + 3) / 4;
+    const uint64_t nslices = (pitch + kSlice - 1) / kSlice;
+    const uint64_t total = nslices * nrows;
+    const uint64_t item0 = total * blockIdx.x / gridDim.x, item1 = total * (blockIdx.x + 1) / gridDim.x;
+    uint64_t it = item0;
+    while (it < item1) {
+        const uint64_t sl = it / nrows;
+        const uint64_t r_begin = it - sl * nrows;
+        const uint64_t r_end = min(nrows, r_begin + (item1 - it));
+        const uint64_t w0 = sl * kSlice;
+        // Build the combination table of this slice.
+        __syncthreads(); // previous slice's readers are done
+        for (uint32_t e = tid; e < ngroups * 2 * (kSlice / 2); e += kAThreads) {
+            const uint32_t wp = e % (kSlice / 2), plane = (e / (kSlice / 2)) & 1, g = e / kSlice;
+            const uint64_t gw = w0 + 2 * wp;
+            ulonglong2 v[4];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const uint32_t j = 4 * g + b;
+                v[b] = make_ulonglong2(0ull, 0ull);
+                if (j < len && gw < pitch)
+                    v[b] = __ldcg(reinterpret_cast<const ulonglong2 *>((plane ? Vz : Vx) + uint64_t(j) * vstride + gw));
+            }
+            u64 *dst = tab + (size_t(g) * 16 * 2 + plane) * kSlice + 2 * wp;
+#pragma unroll
+            for (uint32_t S = 0; S < 16; ++S) {
+                u64 a = 0, b2 = 0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b)
+                    if ((S >> b) & 1u) { a ^= v[b].x; b2 ^= v[b].y; }
+                *reinterpret_cast<ulonglong2 *>(dst + size_t(S) * 2 * kSlice) = make_ulonglong2(a, b2);
+            }
+        }
+        __syncthreads();
+        const uint64_t i = w0 + 2 * lane;
+        const bool act = i < pitch;
+        for (uint64_t base = r_begin + uint64_t(warp) * kARows; base < r_end;
+             base += uint64_t(kAWarps) * kARows) {
+            uint32_t M[kARows];
+            uint32_t U = 0;
+#pragma unroll
+            for (int q = 0; q < kARows; ++q) {
+                M[q] = base + q < r_end ? member[base + q] : 0u;
+                U |= M[q];
+            }
+            if (U == 0) continue;
+            ulonglong2 cx[kARows], cz[kARows];
+            u64 acc[kARows];
+            int bd[kARows];
+#pragma unroll
+            for (int q = 0; q < kARows; ++q) {
+                cx[q] = make_ulonglong2(0ull, 0ull);
+                cz[q] = cx[q];
+                acc[q] = 0;
+                if (M[q] && act) {
+                    cx[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(x + (base + q) * pitch + i));
+                    cz[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(z + (base + q) * pitch + i));
+                }
+                bd[q] = __popcll(cx[q].x & cz[q].x) + __popcll(cx[q].y & cz[q].y);
+            }
+            for (uint32_t g = 0; g < ngroups; ++g) {
+                const u64 *tg = tab + size_t(g) * 16 * 2 * kSlice + 2 * lane;
+#pragma unroll
+                for (int q = 0; q < kARows; ++q) {
+                    const uint32_t S = (M[q] >> (4 * g)) & 15u;
+                    if (S) {
+                        const ulonglong2 tx = *reinterpret_cast<const ulonglong2 *>(tg + size_t(S) * 2 * kSlice);
+                        const ulonglong2 tz = *reinterpret_cast<const ulonglong2 *>(tg + (size_t(S) * 2 + 1) * kSlice);
+                        acc[q] ^= (tz.x & cx[q].x) ^ (tz.y & cx[q].y);
+                        cx[q].x ^= tx.x; cx[q].y ^= tx.y;
+                        cz[q].x ^= tz.x; cz[q].y ^= tz.y;
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kARows; ++q) {
+                if (!M[q]) continue;
+                if (act) {
+                    __stcs(reinterpret_cast<ulonglong2 *>(x + (base + q) * pitch + i), cx[q]);
+                    __stcs(reinterpret_cast<ulonglong2 *>(z + (base + q) * pitch + i), cz[q]);
+                }
+                const int v = warp_sum(bd[q] - __popcll(cx[q].x & cz[q].x) - __popcll(cx[q].y & cz[q].y) +
+                                       2 * (__popcll(acc[q]) & 1));
+                if (lane == 0) partial[sl * nrows + base + q] = uint8_t(v & 3);
+            }
+        }
+        it += r_end - r_begin;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
+              const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
+              const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
+              const uint32_t *__restrict__ gconst, int *__restrict__ err) {
+    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_const[kGroups];
+    const uint32_t len = bctl[BL_LEN];
+    if (len == 0) return;
+    const uint32_t tid = threadIdx.x;
+    if (tid == 0) {
+        uint32_t vs = 0, b0 = 0, b1 = 0;
+        for (uint32_t j = 0; j < len; ++j) {
+            vs |= (vinfo[VI_SIGN + j] & 1u) << j;
+            b0 |= (vinfo[VI_BETA + j] & 1u) << j;
+            b1 |= ((vinfo[VI_BETA + j] >> 1) & 1u) << j;
+        }
+        s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
+    }
+    if (tid < kGroups) s_const[tid] = gconst[tid];
+    __syncthreads();
+    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
+    uint32_t f = 0;
+    bool odd = false;
+    if (r < nrows) {
+        const uint32_t M = member[r];
+        if (M) {
+            int E = 0;
+            for (uint64_t sl = 0; sl < nslices; ++sl) E += partial[sl * nrows + r];
+            uint32_t c = 0;
+            for (uint32_t g = 0; g < (len + 3) / 4; ++g) c ^= (s_const[g] >> ((M >> (4 * g)) & 15u)) & 1u;
+            E += 2 * int(c) + __popc(M & s_b0_mask) + 2 * __popc(M & s_b1_mask);
+            odd = (E & 1) != 0;
+            f = parity32(M & s_vs_mask) ^ ((uint32_t(E) >> 1) & 1u);
+        }
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, f != 0);
+    if (__any_sync(0xffffffffu, odd) && (tid & 31) == 0) atomicExch(err, 1);
+    if ((tid & 31) == 0 && bits && r < nrows)
+        reinterpret_cast<uint32_t *>(s)[r >> 5] ^= bits; // rows r..r+31 own this half-word
+}
+
 } // namespace
 
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
@@ -390,14 +862,38 @@ void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
     const uint64_t nrows = 2 * t.ng;
     QSR_CUDA(cudaMemsetAsync(ms.bctl, 0, 16, t.stream));
     k_colbits<<<unsigned((nrows + 255) / 256), 256, 0, t.stream>>>(t.x, t.rm_pitch, nrows, t.ng, d_fq,
-                                                                    b, ms.colbits, ms.bctl + BL_STAB_OR);
+                                                                    b, ms.colbits, ms.bctl + BL_STAB_OR,
+                                                                    ms.nz);
     QSR_CUDA(cudaGetLastError());
     count_launch();
+}
+
+// QSR_PIVOTS=fused selects the single-CTA pivot kernel (A/B and differential tests).
+bool split_pivots() {
+    static bool on = [] {
+        const char *e = getenv("QSR_PIVOTS");
+        return !(e && std::string(e) == "fused");
+    }();
+    return on;
 }
 
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
                   uint64_t seed) {
     MeasureScratch &ms = t.ms;
+    if (split_pivots()) {
+        QSR_CUDA(cudaMemsetAsync(ms.pcount, 0, 2 * kB * sizeof(int), t.stream));
+        k_pivot_select<<<1, kSelThreads, 0, t.stream>>>(ms.colbits, ms.nz, t.n_gen, t.ng, t.g0, b,
+                                                        ms.vinfo, ms.bctl);
+        QSR_CUDA(cudaGetLastError());
+        k_pivot_rows<<<unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads), kRowThreads, 0, t.stream>>>(
+            t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz, ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
+        QSR_CUDA(cudaGetLastError());
+        k_pivot_finish<<<1, 32, 0, t.stream>>>(t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo, ms.bctl, ms.pcount,
+                                               seed, ms.coin_index, ms.out, ms.err, ms.coin_table);
+        QSR_CUDA(cudaGetLastError());
+        count_launch(3);
+        return;
+    }
     k_batch_pivots<<<1, 1024, 0, t.stream>>>(t.x, t.z, t.rm_pitch, t.k, t.n_gen, t.ng, t.g0, t.s,
                                              ms.colbits, d_fq, d_fidx, b, ms.Vx, ms.Vz,
                                              ms.vstride, ms.vinfo, ms.bctl, seed, ms.coin_index,
@@ -406,19 +902,56 @@ void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx
     count_launch();
 }
 
+// QSR_APPLY=rows selects the row-major one-V-at-a-time absorb pass (A/B and differential tests).
+bool table_absorb() {
+    static bool on = [] {
+        const char *e = getenv("QSR_APPLY");
+        return !(e && std::string(e) == "rows");
+    }();
+    return on;
+}
+
 void batch_apply(DeviceTableau &t) {
     MeasureScratch &ms = t.ms;
+    const uint64_t nrows = 2 * t.ng;
+    if (!table_absorb()) {
+        static bool configured = false;
+        if (!configured) {
+            QSR_CUDA(cudaFuncSetAttribute(k_batch_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          int(kApplySmem)));
+            configured = true;
+        }
+        k_batch_apply<<<unsigned(t.num_sms * 2), kCThreads, kApplySmem, t.stream>>>(
+            t.x, t.z, t.rm_pitch, t.k, nrows, t.ng, t.g0, t.s, ms.colbits, ms.Vx, ms.Vz, ms.vstride,
+            ms.vinfo, ms.bctl, ms.err);
+        QSR_CUDA(cudaGetLastError());
+        count_launch();
+        return;
+    }
     static bool configured = false;
     if (!configured) {
-        QSR_CUDA(cudaFuncSetAttribute(k_batch_apply, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      int(kApplySmem)));
+        QSR_CUDA(cudaFuncSetAttribute(k_batch_absorb, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kAbsorbSmem)));
         configured = true;
     }
-    k_batch_apply<<<unsigned(t.num_sms * 2), kCThreads, kApplySmem, t.stream>>>(
-        t.x, t.z, t.rm_pitch, t.k, 2 * t.ng, t.ng, t.g0, t.s, ms.colbits, ms.Vx, ms.Vz, ms.vstride,
-        ms.vinfo, ms.bctl, ms.err);
+    const uint64_t nslices = (t.rm_pitch + kSlice - 1) / kSlice;
+    if (!ms.partial || ms.partial_bytes < nslices * nrows) {
+        if (ms.partial) QSR_CUDA(cudaFree(ms.partial));
+        ms.partial_bytes = nslices * nrows;
+        QSR_CUDA(cudaMalloc(&ms.partial, ms.partial_bytes));
+    }
+    const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
+    k_batch_member<<<row_blocks + kGroups, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
+                                                               ms.Vz, ms.vstride, t.k, ms.vinfo,
+                                                               ms.bctl, ms.gconst, row_blocks);
     QSR_CUDA(cudaGetLastError());
-    count_launch();
+    k_batch_absorb<<<unsigned(t.num_sms), kAThreads, kAbsorbSmem, t.stream>>>(
+        t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial);
+    QSR_CUDA(cudaGetLastError());
+    k_batch_signs<<<row_blocks, 256, 0, t.stream>>>(t.s, nrows, nslices, ms.colbits, ms.partial, ms.vinfo,
+                                                    ms.bctl, ms.gconst, ms.err);
+    QSR_CUDA(cudaGetLastError());
+    count_launch(3);
 }
 
 void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,

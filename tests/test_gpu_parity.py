@@ -273,8 +273,10 @@ def test_mixed_bell_and_random(q, oracle):
     np.testing.assert_array_equal(r.record_array, rec)
 
 
-def test_single_collapse_path_matches(q):
-    """QSR_MEASURE_BATCH=0 (one collapse per pass) must agree with the batched default."""
+@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_APPLY": "rows"}, {"QSR_PIVOTS": "fused"}])
+def test_alternate_collapse_paths_match(q, env):
+    """QSR_MEASURE_BATCH=0 (one collapse per pass) and QSR_APPLY=rows (row-major absorb, one V
+    at a time) must agree with the default (batched, table absorb) and the oracle."""
     import subprocess
     import sys
     code = (
@@ -293,7 +295,7 @@ def test_single_collapse_path_matches(q):
         "    assert np.array_equal(r.record_array, rec)\n"
         "print('ok')\n")
     import os
-    env = dict(os.environ, QSR_MEASURE_BATCH="0")
+    env = dict(os.environ, **env)
     root = __import__("pathlib").Path(__file__).resolve().parents[1]
     out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
