@@ -80,7 +80,7 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
         ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
         ms.bctl = ms.vinfo + kVinfoWords;
     }
-    QSR_CUDA(cudaMalloc(&ms.gconst, kMaxBatch / 4 * 4));
+    QSR_CUDA(cudaMalloc(&ms.gconst, kMaxBatch * 4));
     QSR_CUDA(cudaMalloc(&ms.nz, (ng / 32 + 1) * 4));
     QSR_CUDA(cudaMalloc(&ms.pcount, 2 * kMaxBatch * sizeof(int)));
     configure_measure_kernels(*this);

@@ -59,7 +59,7 @@ struct MeasureScratch {
     uint32_t *bctl = nullptr;
     uint8_t *partial = nullptr;     // [slices][2ng] per-(row, slice) phase bytes (k_batch.cu)
     uint64_t partial_bytes = 0;
-    uint32_t *gconst = nullptr;     // [kMaxBatch/4] per-group pair-parity constants
+    uint32_t *gconst = nullptr;     // [kMaxBatch] pair-parity matrix rows of the batch's V's
     uint32_t *nz = nullptr;         // [ng/32] active-stabilizer ballot of the batch
     int *pcount = nullptr;          // [2*kMaxBatch] per-pivot phase / beta counters
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]

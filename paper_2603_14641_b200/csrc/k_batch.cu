@@ -623,19 +623,21 @@ k_batch_apply(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
 
 
 // ---- phase C (table form): membership pass, slice-major absorb pass, sign pass --------
+// Absorbing V_j1, V_j2, ... (ascending j, the row's membership set M) in order, the telescoped
+// phase (file header) needs parity(sum_j |V_jz & cur_x before V_j|). With cur_x = x0 ^
+// XOR_{j'<j in M} V_j'x this is  parity(|dz & x0|) ^ Q(M),  dz = XOR_{j in M} V_jz and
+// Q(M) = XOR_{j'<j, both in M} P(j', j),  P(j', j) = parity(sum_i |V_jz[i] & V_j'x[i]|).
+// So the absorb pass only XORs row deltas; the quadratic form is a per-row 32-bit fold.
 // C1 k_batch_member: M[r] (bit m = row r absorbs V_m) for every row, written over colbits;
-//    blocks >= row_blocks compute the per-group pair constants (below).
+//    blocks >= row_blocks compute row j of the pair-parity matrix: pmat[j] bit j' = P(j', j).
 // C2 k_batch_absorb: persistent, one CTA per SM walks (slice, row) items slice-major; for its
 //    64-word slice it stages, per group of 4 consecutive V's, all 16 XOR combinations
-//    T[g][S] = XOR_{j in S} V_{4g+j} (x and z) in shared memory. A row absorbs the group's
-//    members S = (M >> 4g) & 15 in ONE step: cur ^= T[g][S], and the phase accumulator takes
-//    acc ^= T_z[g][S] & cur_x(before). Absorbing V's one by one would give
-//    acc ^= V_jz & (cur_x ^ XOR_{j'<j in S} V_j'x), so the difference is the row-independent
-//    parity c_S = parity(sum_{j'<j in S} |V_jz & V_j'x|), added in C3. Per (row, slice) it
-//    stores (sum beta(start) - beta(end) + 2 parity(acc)) mod 4 as one byte.
-// C3 k_batch_signs: per row, sums its slice bytes, adds sum beta(V_j), the c_S of its groups
-//    and the V signs (file header), and flips the sign bit; a warp ballot forms each 32-bit
-//    half-word of the sign vector (one writer per half-word, no atomics).
+//    T[g][S] = XOR_{j in S} V_{4g+j} (x and z; T[g][0] = 0) in shared memory, so a row
+//    absorbs its members S = (M >> 4g) & 15 of a group with one branch-free lookup. Per
+//    (row, slice) it stores (beta(start) - beta(end) + 2 parity(|dz & x0|)) mod 4 as a byte.
+// C3 k_batch_signs: per row, sums its slice bytes, adds sum beta(V_j), 2 Q(M) and the V signs
+//    (file header), and flips the sign bit; a warp ballot forms each 32-bit half-word of the
+//    sign vector (one writer per half-word, no atomics).
 constexpr int kAThreads = 512;
 constexpr int kAWarps = kAThreads / 32;
 constexpr int kARows = 4;                    // rows in flight per warp
@@ -647,46 +649,27 @@ __global__ void __launch_bounds__(256)
 k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint64_t g0,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-               uint32_t *__restrict__ gconst, uint32_t row_blocks) {
+               uint32_t *__restrict__ pmat, uint32_t row_blocks) {
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
+    __shared__ uint32_t s_p;
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
     if (blockIdx.x >= row_blocks) {
-        // Pair parities P(j', j) = parity(sum_i |V_jz[i] & V_j'x[i]|), j' < j in group g, then
-        // c_S for all 16 subsets S of the group -> gconst[g] (bit S).
-        const uint32_t g = blockIdx.x - row_blocks;
-        __shared__ uint32_t s_par[6];
-        if (tid < 6) s_par[tid] = 0;
+        const uint32_t j = blockIdx.x - row_blocks;
+        if (tid == 0) s_p = 0;
         __syncthreads();
-        const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {1, 2, 3, 2, 3, 3}; // (j', j)
-        uint32_t loc[6] = {0, 0, 0, 0, 0, 0};
-        for (uint64_t i = tid; i < k; i += blockDim.x) {
-            u64 vx[4], vz[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const uint32_t j = 4 * g + b;
-                vx[b] = j < len ? Vx[uint64_t(j) * vstride + i] : 0ull;
-                vz[b] = j < len ? Vz[uint64_t(j) * vstride + i] : 0ull;
+        uint32_t mask = 0;
+        if (j < len) {
+            for (uint64_t i = tid; i < k; i += blockDim.x) {
+                const u64 vz = Vz[uint64_t(j) * vstride + i];
+                for (uint32_t jp = 0; jp < j; ++jp)
+                    mask ^= (uint32_t(__popcll(vz & Vx[uint64_t(jp) * vstride + i])) & 1u) << jp;
             }
-#pragma unroll
-            for (int p = 0; p < 6; ++p) loc[p] ^= __popcll(vz[pb[p]] & vx[pa[p]]) & 1u;
         }
-#pragma unroll
-        for (int p = 0; p < 6; ++p) {
-            const uint32_t v = __reduce_xor_sync(0xffffffffu, loc[p]);
-            if ((tid & 31) == 0 && v) atomicXor(&s_par[p], 1u);
-        }
+        mask = __reduce_xor_sync(0xffffffffu, mask);
+        if ((tid & 31) == 0 && mask) atomicXor(&s_p, mask);
         __syncthreads();
-        if (tid == 0) {
-            uint32_t mask = 0;
-            for (uint32_t S = 0; S < 16; ++S) {
-                uint32_t c = 0;
-                for (int p = 0; p < 6; ++p)
-                    if (((S >> pa[p]) & 1u) && ((S >> pb[p]) & 1u)) c ^= s_par[p];
-                mask |= c << S;
-            }
-            gconst[g] = mask;
-        }
+        if (tid == 0) pmat[j] = s_p;
         return;
     }
     if (tid < kB) {
@@ -770,45 +753,49 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                 U |= M[q];
             }
             if (U == 0) continue;
-            ulonglong2 cx[kARows], cz[kARows];
-            u64 acc[kARows];
-            int bd[kARows];
+            ulonglong2 x0[kARows], z0[kARows], dx[kARows], dz[kARows];
 #pragma unroll
             for (int q = 0; q < kARows; ++q) {
-                cx[q] = make_ulonglong2(0ull, 0ull);
-                cz[q] = cx[q];
-                acc[q] = 0;
+                x0[q] = make_ulonglong2(0ull, 0ull);
+                z0[q] = x0[q];
+                dx[q] = x0[q];
+                dz[q] = x0[q];
                 if (M[q] && act) {
-                    cx[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(x + (base + q) * pitch + i));
-                    cz[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(z + (base + q) * pitch + i));
+                    x0[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(x + (base + q) * pitch + i));
+                    z0[q] = __ldcs(reinterpret_cast<const ulonglong2 *>(z + (base + q) * pitch + i));
                 }
-                bd[q] = __popcll(cx[q].x & cz[q].x) + __popcll(cx[q].y & cz[q].y);
             }
+            const u64 *tl = tab + 2 * lane;
             for (uint32_t g = 0; g < ngroups; ++g) {
-                const u64 *tg = tab + size_t(g) * 16 * 2 * kSlice + 2 * lane;
 #pragma unroll
                 for (int q = 0; q < kARows; ++q) {
-                    const uint32_t S = (M[q] >> (4 * g)) & 15u;
-                    if (S) {
-                        const ulonglong2 tx = *reinterpret_cast<const ulonglong2 *>(tg + size_t(S) * 2 * kSlice);
-                        const ulonglong2 tz = *reinterpret_cast<const ulonglong2 *>(tg + (size_t(S) * 2 + 1) * kSlice);
-                        acc[q] ^= (tz.x & cx[q].x) ^ (tz.y & cx[q].y);
-                        cx[q].x ^= tx.x; cx[q].y ^= tx.y;
-                        cz[q].x ^= tz.x; cz[q].y ^= tz.y;
-                    }
+                    const uint32_t S = (M[q] >> (4 * g)) & 15u; // S = 0 reads the zero entry
+                    const u64 *te = tl + (size_t(g) * 16 + S) * 2 * kSlice;
+                    const ulonglong2 tx = *reinterpret_cast<const ulonglong2 *>(te);
+                    const ulonglong2 tz = *reinterpret_cast<const ulonglong2 *>(te + kSlice);
+                    dx[q].x ^= tx.x; dx[q].y ^= tx.y;
+                    dz[q].x ^= tz.x; dz[q].y ^= tz.y;
                 }
             }
+            // Per row: (beta(x0,z0) - beta(end) + 2 parity(|dz & x0|)) mod 4 per lane, packed one
+            // byte per row (each lane's value < 4, a warp's sum < 256) into a single warp sum.
+            uint32_t packed = 0;
 #pragma unroll
             for (int q = 0; q < kARows; ++q) {
-                if (!M[q]) continue;
-                if (act) {
-                    __stcs(reinterpret_cast<ulonglong2 *>(x + (base + q) * pitch + i), cx[q]);
-                    __stcs(reinterpret_cast<ulonglong2 *>(z + (base + q) * pitch + i), cz[q]);
+                const u64 ex = x0[q].x ^ dx[q].x, ey = x0[q].y ^ dx[q].y;
+                const u64 fx = z0[q].x ^ dz[q].x, fy = z0[q].y ^ dz[q].y;
+                const int v = __popcll(x0[q].x & z0[q].x) + __popcll(x0[q].y & z0[q].y) -
+                              __popcll(ex & fx) - __popcll(ey & fy) +
+                              2 * (__popcll((dz[q].x & x0[q].x) ^ (dz[q].y & x0[q].y)) & 1);
+                packed |= uint32_t(v & 3) << (8 * q);
+                if (M[q] && act) {
+                    __stcs(reinterpret_cast<ulonglong2 *>(x + (base + q) * pitch + i), make_ulonglong2(ex, ey));
+                    __stcs(reinterpret_cast<ulonglong2 *>(z + (base + q) * pitch + i), make_ulonglong2(fx, fy));
                 }
-                const int v = warp_sum(bd[q] - __popcll(cx[q].x & cz[q].x) - __popcll(cx[q].y & cz[q].y) +
-                                       2 * (__popcll(acc[q]) & 1));
-                if (lane == 0) partial[sl * nrows + base + q] = uint8_t(v & 3);
             }
+            packed = __reduce_add_sync(0xffffffffu, packed);
+            if (lane < kARows && M[lane] != 0u) // M[] is warp-uniform; lane q writes row q
+                partial[sl * nrows + base + lane] = uint8_t((packed >> (8 * lane)) & 3u);
         }
         it += r_end - r_begin;
     }
@@ -818,8 +805,8 @@ __global__ void __launch_bounds__(256)
 k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
               const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-              const uint32_t *__restrict__ gconst, int *__restrict__ err) {
-    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_const[kGroups];
+              const uint32_t *__restrict__ pmat, int *__restrict__ err) {
+    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB];
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x;
@@ -832,7 +819,7 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
         }
         s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
     }
-    if (tid < kGroups) s_const[tid] = gconst[tid];
+    if (tid < kB) s_p[tid] = tid < len ? pmat[tid] : 0u;
     __syncthreads();
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
     uint32_t f = 0;
@@ -842,9 +829,9 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
         if (M) {
             int E = 0;
             for (uint64_t sl = 0; sl < nslices; ++sl) E += partial[sl * nrows + r];
-            uint32_t c = 0;
-            for (uint32_t g = 0; g < (len + 3) / 4; ++g) c ^= (s_const[g] >> ((M >> (4 * g)) & 15u)) & 1u;
-            E += 2 * int(c) + __popc(M & s_b0_mask) + 2 * __popc(M & s_b1_mask);
+            uint32_t qf = 0; // Q(M): pairs j' < j of M with P(j', j) = 1
+            for (uint32_t U = M; U; U &= U - 1) qf ^= parity32(M & s_p[__ffs(U) - 1]);
+            E += 2 * int(qf) + __popc(M & s_b0_mask) + 2 * __popc(M & s_b1_mask);
             odd = (E & 1) != 0;
             f = parity32(M & s_vs_mask) ^ ((uint32_t(E) >> 1) & 1u);
         }
@@ -941,9 +928,9 @@ void batch_apply(DeviceTableau &t) {
         QSR_CUDA(cudaMalloc(&ms.partial, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
-    k_batch_member<<<row_blocks + kGroups, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
-                                                               ms.Vz, ms.vstride, t.k, ms.vinfo,
-                                                               ms.bctl, ms.gconst, row_blocks);
+    k_batch_member<<<row_blocks + kB, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
+                                                          ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl,
+                                                          ms.gconst, row_blocks);
     QSR_CUDA(cudaGetLastError());
     k_batch_absorb<<<unsigned(t.num_sms), kAThreads, kAbsorbSmem, t.stream>>>(
         t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial);
