@@ -235,23 +235,25 @@ def main():
     ms_per_step = total_ms / args.steps
     value = G * args.steps / (total_ms * 1e-3)
 
-    # Roofline of the dominant kernel (gate window): algorithmic bytes per launch over the
-    # average launch duration measured above with CUDA events on the engine's stream.
-    # Per launch: one window on this process's shard (2*kg_local generator-words per qubit).
-    gb = gate_bytes(circ, kg_local, gate_windows)
-    if world == 1 and shards > 1:
-        gb = gate_bytes(circ, k, gate_windows) / shards  # mean shard (launches count all shards)
-    per_launch_bytes = gb / gate_windows
+    # Roofline of the dominant kernel (gate windows): algorithmic bytes per launch over the
+    # average launch duration measured above with CUDA events on the engine's stream: one
+    # k_gate_window launch per window (QSR_GATE_ENGINE=segment: one temporally blocked
+    # k_gate_segment launch per unitary segment, an opt-in experiment).
+    # Bytes: every window on this process's shard(s) (2*kg generator-words per qubit).
+    launches_per_step = gate_launch / args.steps
+    gb_step = gate_bytes(circ, k if (world == 1 and shards > 1) else kg_local, gate_windows)
+    per_launch_bytes = gb_step / launches_per_step
     per_launch_s = (gate_ms / gate_launch) * 1e-3
     achieved = per_launch_bytes / per_launch_s / 1e9
     peak, peak_src = peaks()
+    kernel = "k_gate_segment" if os.environ.get("QSR_GATE_ENGINE") == "segment" else "k_gate_window"
     traffic = None
     tp = ROOT / "profiles" / "gate_window_traffic.json"
     if tp.exists():
         try:
-            d = json.loads(tp.read_text())
-            if d.get("config") == args.config:
-                traffic = d.get("dram_bytes_per_launch")
+            for d in json.loads(tp.read_text()).get("entries", []):
+                if d.get("config") == args.config and d.get("kernel", "").startswith(kernel) and shards == 1:
+                    traffic = d.get("dram_bytes_per_launch")
         except Exception:
             pass
     st = eng.stats()
@@ -324,7 +326,7 @@ def main():
         "wall_s_per_step": ms_per_step / 1e3,
         "phase_ms_per_step": {"gate_windows": gate_ms / args.steps, "transpose": st["transpose_ms"],
                               "measure": st["measure_ms"]},
-        "roofline": {"bound": "hbm", "kernel": "k_gate_window", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_s * 1e3,
                      "peak_source": peak_src},

@@ -90,7 +90,7 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
 DeviceTableau::~DeviceTableau() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void *p : {(void *)x, (void *)z, (void *)x2, (void *)z2, (void *)s, (void *)sign_partials,
+    for (void *p : {(void *)x, (void *)z, (void *)x2, (void *)z2, (void *)s, (void *)sign_partials, (void *)seg_bar,
                     (void *)tile_counters, (void *)gate_buf, (void *)ms.mask, (void *)ms.rows,
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
@@ -643,7 +643,7 @@ qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate
     return guard([&] {
         REQUIRE_PTR(e);
         if (gate_ms) *gate_ms = e->last.to_ms;
-        if (gate_launches) *gate_launches = e->last.gate_windows;
+        if (gate_launches) *gate_launches = e->last.gate_launches;
         if (transpose_ms) *transpose_ms = e->last.t_ms;
         if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
         if (launches) *launches = e->launches;
@@ -691,12 +691,15 @@ struct qsr_frames {
     std::vector<int64_t> row_of; // qubit -> record row
     uint64_t *gate_buf = nullptr;
     uint64_t gate_cap = 0;
+    unsigned int *seg_bar = nullptr; // segment-kernel grid barrier
+    uint64_t *xs = nullptr, *zs = nullptr; // slab-major scratch planes of the segment kernel
     uint32_t *d_idx = nullptr;   // qubits + rows staging
     uint64_t idx_cap = 0;
     ~qsr_frames() {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        for (void *p : {(void *)xf, (void *)zf, (void *)rec, (void *)gate_buf, (void *)d_idx})
+        for (void *p : {(void *)xf, (void *)zf, (void *)rec, (void *)gate_buf, (void *)d_idx, (void *)seg_bar,
+                        (void *)xs, (void *)zs})
             if (p) cudaFree(p);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -932,10 +935,29 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         auto f = make_frames(c->num_qubits, shots, seed, device, w0, nw);
         QSR_CUDA(cudaStreamSynchronize(t.stream));
         uint32_t epoch = 1;
-        for (uint64_t w = 0; w < ds->is_meas.size(); ++w) {
+        const uint64_t W = ds->is_meas.size();
+        for (uint64_t w = 0; w < W;) {
             const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
-            if (ds->is_meas[w]) frames_measure(*f, sched.gates.data() + b, e - b, seed, epoch++);
-            else frames_window(*f, ds->d_gates + b, e - b);
+            if (ds->is_meas[w]) {
+                frames_measure(*f, sched.gates.data() + b, e - b, seed, epoch++);
+                ++w;
+                continue;
+            }
+            uint64_t w1 = w;
+            while (w1 < W && !ds->is_meas[w1]) ++w1;
+            if (gate_segment_enabled() && w1 - w >= 2 && f->n) {
+                if (!f->seg_bar) QSR_CUDA(cudaMalloc(&f->seg_bar, 256));
+                if (!f->xs) {
+                    QSR_CUDA(cudaMalloc(&f->xs, f->n * f->pitch * 8));
+                    QSR_CUDA(cudaMalloc(&f->zs, f->n * f->pitch * 8));
+                }
+                launch_frame_segment(f->xf, f->zf, f->pitch, f->n, ds->d_gates, ds->d_offsets + w,
+                                     uint32_t(w1 - w), f->num_sms, f->stream, f->seg_bar, f->xs, f->zs);
+            } else {
+                for (uint64_t v = w; v < w1; ++v)
+                    frames_window(*f, ds->d_gates + ds->offsets[v], ds->offsets[v + 1] - ds->offsets[v]);
+            }
+            w = w1;
         }
         // Fold in the reference outcomes: per_qubit() = last outcome per qubit
         // (measure.hpp:50-64, frames.hpp:183-202).

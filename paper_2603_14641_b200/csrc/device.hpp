@@ -95,6 +95,7 @@ struct DeviceTableau {
     uint64_t *sign_partials = nullptr;
     uint64_t sign_partial_chunks = 0;
     uint32_t *tile_counters = nullptr;
+    unsigned int *seg_bar = nullptr;       // grid barrier of the segment kernel
     uint64_t *gate_buf = nullptr;          // staging for single-window API calls
     uint64_t gate_buf_cap = 0;
     MeasureScratch ms;
@@ -110,6 +111,15 @@ struct DeviceTableau {
 // ---- launchers --------------------------------------------------------------------
 // Gate window on a CM tableau: `gates` is a device array of packed gate words.
 void launch_gate_window(DeviceTableau &t, const uint64_t *gates, uint64_t ngates);
+// All windows of a unitary segment in one persistent launch (temporally blocked, L2-resident
+// slabs; k_gates.cu). d_woff = device window offsets into `gates` (nwin + 1 entries).
+bool gate_segment_enabled();
+void launch_gate_segment(DeviceTableau &t, const uint64_t *gates, const uint64_t *d_woff,
+                         uint32_t nwin);
+void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t rows,
+                          const uint64_t *gates, const uint64_t *d_woff, uint32_t nwin,
+                          int num_sms, cudaStream_t st, unsigned int *bar, uint64_t *xs,
+                          uint64_t *zs); // xs, zs: scratch planes of the same size (slab-major)
 // Frames: same rules, no signs.
 void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *gates,
                          uint64_t ngates, int num_sms, cudaStream_t st);

@@ -2,6 +2,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <thread>
 
 namespace qsr {
 
@@ -32,22 +33,15 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
     QSR_CUDA(cudaSetDevice(device));
     QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
     if (G) {
-        // Pack + upload in 32 Mi-gate slabs through pinned staging.
-        const uint64_t slab = uint64_t(1) << 25;
-        uint64_t *pinned = nullptr;
-        QSR_CUDA(cudaMallocHost(&pinned, std::min(G, slab) * 8 * 2));
-        uint64_t *buf[2] = {pinned, pinned + std::min(G, slab)};
-        int cur = 0;
-        for (uint64_t b = 0; b < G; b += slab, cur ^= 1) {
-            uint64_t e = std::min(G, b + slab);
-            QSR_CUDA(cudaStreamSynchronize(st)); // previous use of buf[cur] finished
-            for (uint64_t i = b; i < e; ++i) buf[cur][i - b] = pack_gate(s.gates[i]);
-            QSR_CUDA(cudaMemcpyAsync(ds->d_gates + b, buf[cur], (e - b) * 8,
-                                     cudaMemcpyHostToDevice, st));
-        }
+        std::unique_ptr<uint64_t[]> packed(new uint64_t[G]);
+        for (uint64_t i = 0; i < G; ++i) packed[i] = pack_gate(s.gates[i]);
+        if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
+            sort_unitary_windows(packed.get(), s.offsets, s.is_meas);
+
+        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
         QSR_CUDA(cudaStreamSynchronize(st));
-        QSR_CUDA(cudaFreeHost(pinned));
     }
+    upload_offsets(*ds, st);
     return ds;
 }
 
@@ -62,6 +56,9 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
     const uint64_t G = c.gates.size();
     std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
     scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
+    if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
+        sort_unitary_windows(packed.get(), p.offsets, p.is_meas);
+
     auto ds = std::make_unique<DeviceSchedule>();
     ds->device = device;
     ds->offsets = std::move(p.offsets);
@@ -83,7 +80,55 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
         QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
         QSR_CUDA(cudaStreamSynchronize(st));
     }
+    upload_offsets(*ds, st);
     return ds;
+}
+
+// Device gate order inside a unitary window is free (operands are disjoint and the sign fold
+// is an XOR), so each window's packed gates are grouped by kind. The gate kernels hand gates to
+// CTAs / chunks strided (b, b + NB, ...), so every CTA still gets a representative kind mix,
+// while consecutive gates of a CTA share a kind and the 8-lane groups of a warp stay
+// convergent in the per-kind rule switch.
+// Measurement windows keep their order (it is the record order).
+void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
+                          const std::vector<uint8_t> &is_meas) {
+    const uint64_t W = is_meas.size();
+    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < nt; ++t)
+        th.emplace_back([&, t] {
+            std::vector<uint64_t> tmp;
+            for (uint64_t w = t; w < W; w += nt) {
+                if (is_meas[w]) continue;
+                const uint64_t b = offsets[w], e = offsets[w + 1];
+                uint64_t cnt[16] = {0};
+                for (uint64_t i = b; i < e; ++i) ++cnt[(packed[i] >> 28) & 0xF];
+                uint64_t pos[16], acc = 0;
+                for (int k = 0; k < 16; ++k) { pos[k] = acc; acc += cnt[k]; }
+                tmp.resize(e - b);
+                for (uint64_t i = b; i < e; ++i) tmp[pos[(packed[i] >> 28) & 0xF]++] = packed[i];
+                std::copy(tmp.begin(), tmp.end(), packed + b);
+            }
+        });
+    for (auto &x : th) x.join();
+}
+
+void upload_offsets(DeviceSchedule &ds, cudaStream_t st) {
+    QSR_CUDA(cudaMalloc(&ds.d_offsets, ds.offsets.size() * 8));
+    QSR_CUDA(cudaMemcpyAsync(ds.d_offsets, ds.offsets.data(), ds.offsets.size() * 8,
+                             cudaMemcpyHostToDevice, st));
+    QSR_CUDA(cudaStreamSynchronize(st));
+}
+
+uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1) {
+    if (w1 <= w0) return 0;
+    if (gate_segment_enabled() && w1 - w0 >= 2) {
+        launch_gate_segment(t, ds.d_gates, ds.d_offsets + w0, uint32_t(w1 - w0));
+        return 1;
+    }
+    for (uint64_t w = w0; w < w1; ++w)
+        launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+    return w1 - w0;
 }
 
 // The single-shot driver on device-resident inputs (simulator.hpp:46-70). `record` is a
@@ -106,10 +151,10 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
         if (!ds.is_meas[w]) {
             // A maximal run of unitary windows, bracketed by one event pair (TO bucket).
             QSR_CUDA(cudaEventRecord(a, t.stream));
-            for (; w < W && !ds.is_meas[w]; ++w) {
-                launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
-                ++rt.gate_windows;
-            }
+            uint64_t w1 = w;
+            while (w1 < W && !ds.is_meas[w1]) ++w1;
+            rt.gate_launches += run_unitary_windows(t, ds, w, w1);
+            w = w1;
             QSR_CUDA(cudaEventRecord(b, t.stream));
             QSR_CUDA(cudaEventSynchronize(b));
             float ms = 0;

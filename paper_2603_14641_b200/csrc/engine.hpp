@@ -14,12 +14,15 @@ namespace qsr {
 struct DeviceSchedule {
     int device = 0;
     uint64_t *d_gates = nullptr;
+    uint64_t *d_offsets = nullptr; // device copy of offsets (segment kernel)
     std::vector<uint64_t> offsets;
     std::vector<uint8_t> is_meas;
     std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
     uint64_t measure_count = 0, unitary_count = 0;
     ~DeviceSchedule() {
-        if (d_gates) { cudaSetDevice(device); cudaFree(d_gates); }
+        cudaSetDevice(device);
+        if (d_gates) cudaFree(d_gates);
+        if (d_offsets) cudaFree(d_offsets);
     }
 };
 
@@ -31,8 +34,17 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
 
 struct RunTimes {
     double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
-    uint64_t gate_windows = 0;
+    uint64_t gate_launches = 0; // gate-window kernel launches (a segment launch covers many windows)
 };
+
+// Windows [w0, w1) (all unitary) on t: one temporally blocked segment launch when the segment
+// engine is on and there are >= 2 windows, else one launch per window. Returns launches.
+uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1);
+// Groups each unitary window's packed gates by kind (device order inside a window is free).
+void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
+                          const std::vector<uint8_t> &is_meas);
+// Uploads ds.offsets to ds.d_offsets.
+void upload_offsets(DeviceSchedule &ds, cudaStream_t st);
 
 // The single-shot driver on device-resident inputs; `d_record` has measure_count entries.
 void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,

@@ -12,6 +12,8 @@
 //   CM word (q, J)      at q*cm_pitch + J          bits = generators J*64 + b
 //   RM word (r = J*64+t, I) at r*rm_pitch + I      bits = qubits I*64 + c
 // Tile (I, J): CM rows I*64..I*64+63, word J  <->  RM rows J*64..J*64+63, word I.
+#include <algorithm>
+
 #include "common.cuh"
 #include "device.hpp"
 
@@ -92,6 +94,19 @@ k_transpose(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst, uint64
     }
 }
 
+// RM row padding (qubit-words k .. rm_pitch-1) must read as zero for the measurement kernels;
+// the RM buffer doubles as slab-major scratch of the gate-segment kernel, so it is re-zeroed.
+__global__ void k_zero_rm_padding(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
+                                  uint64_t k, uint64_t rows) {
+    const uint64_t pad = pitch - k;
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * pad;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t r = e / pad, w = k + e % pad;
+        x[r * pitch + w] = 0;
+        z[r * pitch + w] = 0;
+    }
+}
+
 void run(const uint64_t *src, uint64_t *dst, uint64_t src_pitch, uint64_t dst_pitch,
          uint64_t src_row_tiles, uint64_t src_words, bool to_rm, cudaStream_t st) {
     dim3 grid{unsigned((src_row_tiles + TB - 1) / TB), unsigned((src_words + TB - 1) / TB)};
@@ -112,6 +127,13 @@ void transpose_to_rm(DeviceTableau &t) {
     // CM: row-tiles I in [0,k), words J in [0,2kg).
     run(t.x, t.x2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.kg, true, t.stream);
     run(t.z, t.z2, t.cm_pitch, t.rm_pitch, t.k, 2 * t.kg, true, t.stream);
+    if (t.rm_pitch > t.k) {
+        const uint64_t rows = 2 * t.ng, work = rows * (t.rm_pitch - t.k);
+        const unsigned blocks = unsigned(std::min<uint64_t>((work + 255) / 256, uint64_t(t.num_sms) * 16));
+        k_zero_rm_padding<<<blocks, 256, 0, t.stream>>>(t.x2, t.z2, t.rm_pitch, t.k, rows);
+        QSR_CUDA(cudaGetLastError());
+        count_launch();
+    }
     std::swap(t.x, t.x2);
     std::swap(t.z, t.z2);
     t.layout = QSR_ROW_MAJOR;

@@ -207,11 +207,8 @@ struct qsr_sharded {
             if (!ds->is_meas[w]) {
                 QSR_CUDA(cudaEventRecord(a, t0.stream));
                 const uint64_t w0 = w;
-                for (auto &s : sh)
-                    for (w = w0; w < W && !ds->is_meas[w]; ++w)
-                        launch_gate_window(*s.t, ds->d_gates + ds->offsets[w],
-                                           ds->offsets[w + 1] - ds->offsets[w]);
-                rt.gate_windows += w - w0;
+                while (w < W && !ds->is_meas[w]) ++w;
+                for (auto &s : sh) rt.gate_launches += run_unitary_windows(*s.t, *ds, w0, w);
                 // Shard 0's stream waits for the others so the event pair brackets all shards.
                 for (size_t i = 1; i < sh.size(); ++i) {
                     QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
@@ -339,7 +336,7 @@ qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *ga
     return guard([&] {
         REQUIRE_PTR(e);
         if (gate_ms) *gate_ms = e->last.to_ms;
-        if (gate_launches) *gate_launches = e->last.gate_windows * e->sh.size();
+        if (gate_launches) *gate_launches = e->last.gate_launches;
         if (transpose_ms) *transpose_ms = e->last.t_ms;
         if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
         if (launches) *launches = e->launches;

@@ -273,7 +273,8 @@ def test_mixed_bell_and_random(q, oracle):
     np.testing.assert_array_equal(r.record_array, rec)
 
 
-@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_APPLY": "rows"}, {"QSR_PIVOTS": "fused"}])
+@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_APPLY": "rows"}, {"QSR_PIVOTS": "fused"},
+                                 {"QSR_GATE_ENGINE": "segment"}])
 def test_alternate_collapse_paths_match(q, env):
     """QSR_MEASURE_BATCH=0 (one collapse per pass) and QSR_APPLY=rows (row-major absorb, one V
     at a time) must agree with the default (batched, table absorb) and the oracle."""
