@@ -90,6 +90,9 @@ typedef struct qsr_run_report {
 const char *qsr_last_error(void);
 int qsr_abi_version(void);
 qsr_status qsr_device_count(int *count);
+/* Tableau planes of destroyed tableaux are cached for reuse by the next tableau of the same
+ * shape (QSR_PLANE_CACHE=0 disables); this frees them. */
+void qsr_release_cached_memory(void);
 /* Kernel launches issued by this library since load (bench `gpu_launches`). */
 uint64_t qsr_launch_count(void);
 /* Page-locked host buffers for fast tableau / record transfers (cudaHostAlloc). */

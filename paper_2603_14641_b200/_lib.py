@@ -88,6 +88,7 @@ SIGNATURES = {
     "qsr_abi_version": (i32, []),
     "qsr_device_count": (i32, [pi32]),
     "qsr_launch_count": (u64, []),
+    "qsr_release_cached_memory": (None, []),
     "qsr_host_alloc": (i32, [u64, C.POINTER(P)]),
     "qsr_host_free": (None, [P]),
     "qsr_philox_block": (None, [pu32, pu32, pu32]),

@@ -2,6 +2,7 @@
 // between the reference's host storage and the device layouts, and the single-shot /
 // sampling drivers (reference simulator.hpp:46-76, frames.hpp:163-204).
 #include <chrono>
+#include <mutex>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -27,6 +28,67 @@ void cuda_check(cudaError_t e, const char *what) {
     fail(QSR_CUDA_ERROR, m);
 }
 
+// Caching allocator for the four tableau planes (GBs each): released planes are kept per
+// (device, bytes) and handed to the next tableau of the same shape, so repeated calls do not pay
+// cudaMalloc / cudaFree of tens of GB. On an allocation failure the cache is flushed and the
+// allocation retried; QSR_PLANE_CACHE=0 disables it; qsr_release_cached_memory() empties it.
+namespace {
+struct PlaneCache {
+    std::mutex mu;
+    struct Entry { int device; uint64_t bytes; void *p; };
+    std::vector<Entry> free_list;
+    static bool enabled() {
+        static const bool on = [] {
+            const char *e = getenv("QSR_PLANE_CACHE");
+            return !(e && e[0] == '0');
+        }();
+        return on;
+    }
+    void *acquire(int device, uint64_t bytes) {
+        {
+            std::lock_guard<std::mutex> g(mu);
+            for (size_t i = 0; i < free_list.size(); ++i)
+                if (free_list[i].device == device && free_list[i].bytes == bytes) {
+                    void *p = free_list[i].p;
+                    free_list.erase(free_list.begin() + long(i));
+                    return p;
+                }
+        }
+        void *p = nullptr;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation) {
+            cudaGetLastError();
+            flush(device);
+            e = cudaMalloc(&p, bytes);
+        }
+        QSR_CUDA(e);
+        return p;
+    }
+    void release(int device, uint64_t bytes, void *p) {
+        if (!p) return;
+        if (!enabled()) { cudaFree(p); return; }
+        std::lock_guard<std::mutex> g(mu);
+        free_list.push_back({device, bytes, p});
+    }
+    void flush(int device) {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto it = free_list.begin(); it != free_list.end();) {
+            if (device < 0 || it->device == device) {
+                cudaSetDevice(it->device);
+                cudaFree(it->p);
+                it = free_list.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+};
+PlaneCache &plane_cache() {
+    static PlaneCache *c = new PlaneCache(); // leaked on purpose: outlives static destructors
+    return *c;
+}
+} // namespace
+
 DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : device(dev), n(n_) {
     if (n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "Tableau: n exceeds the supported maximum");
@@ -49,10 +111,10 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
         QSR_CUDA(cudaMalloc(p, words * 8));
         QSR_CUDA(cudaMemsetAsync(*p, 0, words * 8, stream));
     };
-    alloc(&x, plane_words);
-    alloc(&z, plane_words);
-    alloc(&x2, plane_words);
-    alloc(&z2, plane_words);
+    for (uint64_t **pp : {&x, &z, &x2, &z2}) {
+        *pp = static_cast<uint64_t *>(plane_cache().acquire(device, plane_words * 8));
+        QSR_CUDA(cudaMemsetAsync(*pp, 0, plane_words * 8, stream));
+    }
     alloc(&s, cm_pitch);
     QSR_CUDA(cudaMalloc(&tile_counters, (cm_pitch / 64 + 2) * 4));
     QSR_CUDA(cudaMemsetAsync(tile_counters, 0, (cm_pitch / 64 + 2) * 4, stream));
@@ -90,8 +152,11 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
 DeviceTableau::~DeviceTableau() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    for (void *p : {(void *)x, (void *)z, (void *)x2, (void *)z2, (void *)s, (void *)sign_partials, (void *)seg_bar,
-                    (void *)tile_counters, (void *)gate_buf, (void *)ms.mask, (void *)ms.rows,
+    for (uint64_t *p : {x, z, x2, z2}) plane_cache().release(device, plane_words * 8, p);
+    if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf);
+    gate_buf = nullptr;
+    for (void *p : {(void *)s, (void *)sign_partials, (void *)seg_bar,
+                    (void *)tile_counters, (void *)ms.mask, (void *)ms.rows,
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
                     (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits,
@@ -103,9 +168,9 @@ DeviceTableau::~DeviceTableau() {
 
 void DeviceTableau::ensure_gate_buf(uint64_t ng) {
     if (ng <= gate_buf_cap) return;
-    if (gate_buf) QSR_CUDA(cudaFree(gate_buf));
+    if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf);
     gate_buf_cap = std::max<uint64_t>(ng, 1024);
-    QSR_CUDA(cudaMalloc(&gate_buf, gate_buf_cap * 8));
+    gate_buf = static_cast<uint64_t *>(plane_cache().acquire(device, gate_buf_cap * 8));
 }
 
 void DeviceTableau::ensure_window_cap(uint64_t m) {
@@ -165,6 +230,7 @@ uint64_t rm_word_x(DeviceTableau &t, uint64_t r, uint64_t i) {
 extern "C" {
 
 const char *qsr_last_error(void) { return g_err.c_str(); }
+void qsr_release_cached_memory(void) { plane_cache().flush(-1); }
 int qsr_abi_version(void) { return QSR_ABI_VERSION; }
 uint64_t qsr_launch_count(void) { return g_launches; }
 
@@ -572,16 +638,37 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
         const uint64_t nm = c->measure_count();
         if (nm) REQUIRE_PTR(record);
         auto h = std::make_unique<qsr_tableau>();
-        h->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
+        {
+            TraceScope tr("tableau alloc");
+            h->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
+        }
         DeviceTableau &t = *h->t;
-        auto ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream);
-        if (ds->measure_count != nm)
-            fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
+        // Circuit only: the scheduler runs overlapped with the device (stream.cpp); a caller's
+        // Schedule is validated window by window and uploaded first (QSR_STREAM=0 forces that
+        // path for circuits too).
+        const bool streaming = !s && !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0');
+        std::unique_ptr<DeviceSchedule> ds;
+        if (!streaming) {
+            ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream);
+            if (ds->measure_count != nm)
+                fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
+        }
         qsr_record_entry *d_rec = nullptr;
         QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
         RunTimes rt;
         try {
-            run_device(t, *ds, seed, d_rec, rt);
+            TraceScope tr("run_device");
+            if (streaming) {
+                StreamCounts sc;
+                run_circuit_streaming(t, *c, seed, d_rec, rt, sc);
+                ds = std::make_unique<DeviceSchedule>();
+                ds->device = device;
+                ds->unitary_count = sc.unitary;
+                ds->measure_count = sc.measures;
+                ds->is_meas.resize(sc.windows);
+            } else {
+                run_device(t, *ds, seed, d_rec, rt);
+            }
         } catch (...) {
             cudaFree(d_rec);
             throw;

@@ -50,12 +50,19 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
 // by the plan are operand-disjoint by construction; the only error the reference would raise
 // later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
 std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st) {
-    WindowPlan p = plan_windows(c);
+    TraceScope tr_all("upload_circuit");
+    WindowPlan p = [&] {
+        TraceScope tr("  plan_windows");
+        return plan_windows(c);
+    }();
     if (p.duplicate_measure)
         fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
     const uint64_t G = c.gates.size();
     std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
-    scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
+    {
+        TraceScope tr("  scatter_windows");
+        scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
+    }
     if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
         sort_unitary_windows(packed.get(), p.offsets, p.is_meas);
 
@@ -77,6 +84,7 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
     QSR_CUDA(cudaSetDevice(device));
     QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
     if (G) {
+        TraceScope tr("  gates H2D");
         QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
         QSR_CUDA(cudaStreamSynchronize(st));
     }
@@ -224,6 +232,7 @@ void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int l
 }
 
 void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z) {
+    TraceScope tr("download_planes");
     if (t.layout == QSR_COLUMN_MAJOR) {
         if (x) QSR_CUDA(cudaMemcpy2DAsync(x, 2 * t.kg * 8, t.x, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad,
                                           cudaMemcpyDeviceToHost, t.stream));

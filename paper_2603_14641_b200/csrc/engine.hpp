@@ -51,6 +51,14 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
                 qsr_record_entry *d_record, RunTimes &rt);
 void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
                  const std::vector<qsr_record_entry> &record, double total_s);
+
+// run_single_shot straight from a Circuit with the scheduler overlapped with the device
+// (stream.cpp): windows are uploaded and launched as soon as they are final.
+struct StreamCounts {
+    uint64_t unitary = 0, measures = 0, windows = 0;
+};
+void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
+                           qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts);
 // Host reference-layout <-> device layout (CM: [n_pad][2kg] words; RM: reference i-major).
 void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout);
 void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z);

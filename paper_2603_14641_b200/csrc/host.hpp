@@ -2,6 +2,7 @@
 // the device object model. Kernel launchers are declared in device.hpp.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -11,6 +12,20 @@
 #include "../../include/qsr.h"
 
 namespace qsr {
+
+// Host-side phase trace: QSR_TRACE=1 prints "[qsr] phase ms" lines to stderr (wall clock of the
+// calling thread; device work inside a phase is synchronised by the phase itself).
+bool trace_on();
+void trace(const char *phase, double ms);
+struct TraceScope {
+    const char *phase;
+    std::chrono::steady_clock::time_point t0;
+    explicit TraceScope(const char *p) : phase(p), t0(std::chrono::steady_clock::now()) {}
+    ~TraceScope() {
+        if (trace_on())
+            trace(phase, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    }
+};
 
 // Error carrying a qsr_status; thrown inside the library, converted at the C boundary.
 struct Error : std::runtime_error {

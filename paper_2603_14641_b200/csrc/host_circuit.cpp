@@ -13,6 +13,7 @@
 // are flushed after the unitary scan of the round in which their wire's predecessor was
 // taken, chaining through consecutive measurements on one wire (the reference's quirk that
 // later makes measure_window reject the window is therefore preserved).
+#include <cstdio>
 #include <algorithm>
 #include <cstring>
 #include <thread>
@@ -20,6 +21,17 @@
 #include "host.hpp"
 
 namespace qsr {
+
+bool trace_on() {
+    static const bool on = [] {
+        const char *e = getenv("QSR_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+void trace(const char *phase, double ms) { fprintf(stderr, "[qsr] %-28s %10.2f ms\n", phase, ms); }
+
 
 void philox_block(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
     uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
@@ -203,7 +215,10 @@ WindowPlan plan_windows(const Circuit &c) {
 }
 
 Schedule schedule_windows(const Circuit &c, int mode) {
-    WindowPlan p = plan_windows(c);
+    WindowPlan p = [&] {
+        TraceScope tr("plan_windows");
+        return plan_windows(c);
+    }();
     Schedule s;
     s.mode = mode;
     s.gates.resize(c.gates.size());
