@@ -322,7 +322,8 @@ def main():
                    "parallelism": (f"generator-row shards x{world} (NCCL)" if world > 1 else
                                    f"generator-row shards x{shards} on one GPU (local exchange)"
                                    if shards > 1 else "single GPU"),
-                   "l2": "inputs larger than L2 (tableau 16.2 GB vs 126 MB L2); no flush needed"},
+                   "l2": f"inputs larger than L2 (tableau {2 * n_pad * 2 * k * 8 / 1e9:.2f} GB vs 126 MB L2); "
+                         "no flush needed"},
         "wall_s_per_step": ms_per_step / 1e3,
         "phase_ms_per_step": {"gate_windows": gate_ms / args.steps, "transpose": st["transpose_ms"],
                               "measure": st["measure_ms"]},
