@@ -220,7 +220,7 @@ def main():
 
     launches0 = q.launch_count()
     barrier(dist)
-    step_ms, gate_ms, gate_launch = [], 0.0, 0
+    step_ms, gate_ms, gate_launch, gate_dev_bytes = [], 0.0, 0, 0.0
     with Clocks(device) as clk:
         for i in range(args.steps):
             ms = eng.run(run_seed)
@@ -228,6 +228,7 @@ def main():
             step_ms.append(ms)
             gate_ms += st["gate_ms"]
             gate_launch += st["gate_launches"]
+            gate_dev_bytes += st.get("gate_bytes", 0.0)
             log(f"[rank {rank}] step {i}: {ms:.1f} ms  {st}")
     barrier(dist)
     launches = q.launch_count() - launches0
@@ -236,15 +237,18 @@ def main():
     value = G * args.steps / (total_ms * 1e-3)
 
     # Roofline of the dominant kernel (gate windows): algorithmic bytes per launch over the
-    # average launch duration measured above with CUDA events on the engine's stream: one
-    # k_gate_window launch per window (QSR_GATE_ENGINE=segment: one temporally blocked
-    # k_gate_segment launch per unitary segment, an opt-in experiment).
-    # Bytes: every window on this process's shard(s) (2*kg generator-words per qubit).
+    # average launch duration measured above with CUDA events on the engine's stream. The bytes
+    # are those of the device gates actually launched (kind-exact words), i.e. after
+    # the exact gate fusion (SWAP relabelling, single-qubit runs folded into the next two-qubit
+    # gate); `unfused_*` restates the reference-semantics bytes of the same windows and the
+    # resulting effective bandwidth.
     launches_per_step = gate_launch / args.steps
-    gb_step = gate_bytes(circ, k if (world == 1 and shards > 1) else kg_local, gate_windows)
+    gb_ref_step = gate_bytes(circ, k if (world == 1 and shards > 1) else kg_local, gate_windows)
+    gb_step = gate_dev_bytes / args.steps if gate_dev_bytes > 0 else gb_ref_step
     per_launch_bytes = gb_step / launches_per_step
     per_launch_s = (gate_ms / gate_launch) * 1e-3
     achieved = per_launch_bytes / per_launch_s / 1e9
+    effective = gb_ref_step / (gate_ms / args.steps * 1e-3) / 1e9
     peak, peak_src = peaks()
     kernel = "k_gate_segment" if os.environ.get("QSR_GATE_ENGINE") == "segment" else "k_gate_window"
     traffic = None
@@ -330,6 +334,7 @@ def main():
         "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_s * 1e3,
+                     "unfused_bytes_per_step": gb_ref_step, "effective_unfused_gbs": effective,
                      "peak_source": peak_src},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "s_per_step": e2e_total / max(e2e_steps, 1)},

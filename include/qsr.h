@@ -193,6 +193,9 @@ qsr_status qsr_engine_run(qsr_engine *e, uint64_t seed, double *device_ms);
 /* Per-kernel-class device time of the last run (ms) and launch counts. */
 qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate_launches,
                             double *transpose_ms, double *measure_ms, uint64_t *launches);
+/* Algorithmic bytes of the last run's gate-window launches (kind-exact words of the device
+ * gates actually launched — after gate fusion, DESIGN.md §5 — times 8 B x 2kg, + sign words). */
+qsr_status qsr_engine_gate_bytes(const qsr_engine *e, double *bytes);
 qsr_status qsr_engine_record(const qsr_engine *e, qsr_record_entry *record);
 qsr_status qsr_engine_tableau(const qsr_engine *e, uint64_t *x, uint64_t *z, uint64_t *s);
 void qsr_engine_destroy(qsr_engine *e);
@@ -261,6 +264,7 @@ qsr_status qsr_sharded_run(qsr_sharded *e, uint64_t seed, double *device_ms);
 qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *gate_launches,
                              double *transpose_ms, double *measure_ms, uint64_t *launches);
 /* The full measurement record (identical on every rank). */
+qsr_status qsr_sharded_gate_bytes(const qsr_sharded *e, double *bytes); /* this process's shards */
 qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record);
 /* Writes the generator-word columns of this process's shards into full-size reference-layout
  * CM buffers (x, z: n_pad*2k words; s: 2k words); other columns are left untouched. */

@@ -127,6 +127,8 @@ SIGNATURES = {
     "qsr_engine_run": (i32, [P, u64, pd]),
     "qsr_engine_stats": (i32, [P, pd, pu64, pd, pd, pu64]),
     "qsr_engine_record": (i32, [P, P]),
+    "qsr_engine_gate_bytes": (i32, [P, pd]),
+    "qsr_sharded_gate_bytes": (i32, [P, pd]),
     "qsr_engine_tableau": (i32, [P, pu64, pu64, pu64]),
     "qsr_engine_destroy": (None, [P]),
     "qsr_init_frames": (i32, [u64, u64, u64, i32, C.POINTER(P)]),

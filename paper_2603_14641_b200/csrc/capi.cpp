@@ -649,7 +649,7 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
         const bool streaming = !s && !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0');
         std::unique_ptr<DeviceSchedule> ds;
         if (!streaming) {
-            ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream);
+            ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream, true);
             if (ds->measure_count != nm)
                 fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
         }
@@ -706,7 +706,7 @@ qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int de
         auto e = std::make_unique<qsr_engine>();
         e->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
         e->ds = s ? upload_schedule(e->t->n, *s, device, e->t->stream)
-                  : upload_circuit(*c, device, e->t->stream);
+                  : upload_circuit(*c, device, e->t->stream, true);
         QSR_CUDA(cudaMalloc(&e->d_rec,
                             std::max<uint64_t>(e->ds->measure_count, 1) * sizeof(qsr_record_entry)));
         *out = e.release();
@@ -734,6 +734,14 @@ qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate
         if (transpose_ms) *transpose_ms = e->last.t_ms;
         if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
         if (launches) *launches = e->launches;
+    });
+}
+
+qsr_status qsr_engine_gate_bytes(const qsr_engine *e, double *bytes) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        REQUIRE_PTR(bytes);
+        *bytes = e->last.gate_bytes;
     });
 }
 

@@ -35,10 +35,26 @@ __device__ __forceinline__ uint32_t draw_coin(uint64_t seed, uint64_t idx, const
 
 enum : uint32_t { K_X = 0, K_Y, K_Z, K_H, K_S, K_SDG, K_CX, K_CY, K_CZ, K_SWAP, K_ISWAP };
 
-__device__ __forceinline__ uint32_t gate_q0(uint64_t g) { return uint32_t(g) & 0x0FFFFFFFu; }
-__device__ __forceinline__ uint32_t gate_kind(uint64_t g) { return (uint32_t(g) >> 28) & 0xF; }
-__device__ __forceinline__ uint32_t gate_q1(uint64_t g) { return uint32_t(g >> 32); }
+enum : uint32_t { K_C1 = 11, K_ISWAP_R = 12 }; // device-only kinds (host.hpp, fuse.cpp)
 
+// Packed gate word (host.hpp): q0 [0,24) kind [24,28) pre0 [28,33) pre1 [33,38) q1 [38,62).
+__device__ __forceinline__ uint32_t gate_q0(uint64_t g) { return uint32_t(g) & 0xFFFFFFu; }
+__device__ __forceinline__ uint32_t gate_kind(uint64_t g) { return (uint32_t(g) >> 24) & 0xF; }
+__device__ __forceinline__ uint32_t gate_pre0(uint64_t g) { return uint32_t(g >> 28) & 31u; }
+__device__ __forceinline__ uint32_t gate_pre1(uint64_t g) { return uint32_t(g >> 33) & 31u; }
+__device__ __forceinline__ uint32_t gate_q1(uint64_t g) { return uint32_t(g >> 38) & 0xFFFFFFu; }
+
+// The 24 single-qubit Cliffords (fuse.hpp): bits 0-3 = GF(2) matrix m00 m01 m10 m11 acting on
+// (x, z) (x' = m00 x ^ m01 z, z' = m10 x ^ m11 z), bits 4-6 = sign flip of the images of X, Z, Y.
+// Element 0 is the identity; 0-3 are the Paulis (matrix = identity, code 9).
+__device__ __constant__ const uint8_t kCliff1[24] = {9,   105, 57,  89, 70, 77, 29, 38,
+                                                     45,  125, 118, 22, 14, 110, 87, 7,
+                                                     55,  103, 62,  94, 43, 75, 123, 27};
+// Words an element rewrites (x and z) unless its matrix is the identity.
+__device__ __forceinline__ bool cliff1_moves(uint32_t e) { return (kCliff1[e] & 0xFu) != 9u; }
+
+// Operand words a packed gate reads / writes, pre-operations included: bit0 x0, bit1 z0,
+// bit2 x1, bit3 z1.
 // Operand words each kind reads / writes: bit0 x0, bit1 z0, bit2 x1, bit3 z1
 // (reference gates.hpp:35-115; X/Y/Z only contribute signs).
 __device__ __forceinline__ uint32_t kind_reads(uint32_t kind, bool signs) {
@@ -50,7 +66,8 @@ __device__ __forceinline__ uint32_t kind_reads(uint32_t kind, bool signs) {
     case K_S:
     case K_SDG: return 0x3u;
     case K_SWAP: return 0xFu;
-    default: return 0xFu; // CX CY CZ ISWAP
+    case K_C1: return 0x3u;
+    default: return 0xFu; // CX CY CZ ISWAP ISWAP_R
     }
 }
 __device__ __forceinline__ uint32_t kind_writes(uint32_t kind) {
@@ -63,70 +80,23 @@ __device__ __forceinline__ uint32_t kind_writes(uint32_t kind) {
     case K_CY: return 0xEu;  // z0, x1, z1
     case K_SWAP:
     case K_ISWAP: return 0xFu;
-    default: return 0u;
+    case K_ISWAP_R: return 0xAu; // z0, z1
+    default: return 0u;          // X Y Z; K_C1 decided by its element (gate_writes)
     }
 }
 
-// One word of the column update rules; returns the sign-flip word. Operand 0 = control.
-// Restates the frozen conjugation table of gates.hpp:35-115.
-__device__ __forceinline__ uint64_t apply_rule(uint32_t kind, uint64_t &x0, uint64_t &z0,
-                                               uint64_t &x1, uint64_t &z1) {
-    uint64_t sign = 0;
-    switch (kind) {
-    case K_H: {
-        sign = x0 & z0;
-        uint64_t t = x0; x0 = z0; z0 = t;
-        break;
-    }
-    case K_S: sign = x0 & z0; z0 ^= x0; break;
-    case K_SDG: sign = x0 & ~z0; z0 ^= x0; break;
-    case K_X: sign = z0; break;
-    case K_Y: sign = x0 ^ z0; break;
-    case K_Z: sign = x0; break;
-    case K_CX:
-        sign = x0 & z1 & ~(x1 ^ z0);
-        x1 ^= x0;
-        z0 ^= z1;
-        break;
-    case K_CZ:
-        sign = x0 & x1 & (z0 ^ z1);
-        z1 ^= x0;
-        z0 ^= x1;
-        break;
-    case K_CY: {
-        uint64_t s1 = x1 & ~z1;
-        uint64_t zt = z1 ^ x1;
-        uint64_t s2 = x0 & zt & ~(x1 ^ z0);
-        uint64_t xt = x1 ^ x0;
-        uint64_t zc = z0 ^ zt;
-        uint64_t s3 = xt & zt;
-        sign = s1 ^ s2 ^ s3;
-        x1 = xt;
-        z0 = zc;
-        z1 = zt ^ xt;
-        break;
-    }
-    case K_SWAP: {
-        uint64_t t = x0; x0 = x1; x1 = t;
-        t = z0; z0 = z1; z1 = t;
-        break;
-    }
-    case K_ISWAP: {
-        uint64_t t = x0; x0 = x1; x1 = t;
-        t = z0; z0 = z1; z1 = t;
-        uint64_t s2 = x0 & x1 & (z0 ^ z1);
-        uint64_t zt = z1 ^ x0;
-        uint64_t zc = z0 ^ x1;
-        uint64_t s3 = x1 & zt;
-        uint64_t s4 = x0 & zc;
-        sign = s2 ^ s3 ^ s4;
-        z1 = zt ^ x1;
-        z0 = zc ^ x0;
-        break;
-    }
-    default: break;
-    }
-    return sign;
+__device__ __forceinline__ uint32_t gate_reads(uint64_t g, bool signs) {
+    const uint32_t k = gate_kind(g);
+    uint32_t r = kind_reads(k, signs);
+    if (gate_pre0(g)) r |= 0x3u;
+    if (gate_pre1(g)) r |= 0xCu;
+    return r;
+}
+__device__ __forceinline__ uint32_t gate_writes(uint64_t g) {
+    uint32_t w = kind_writes(gate_kind(g));
+    if (gate_pre0(g) && cliff1_moves(gate_pre0(g))) w |= 0x3u;
+    if (gate_pre1(g) && cliff1_moves(gate_pre1(g))) w |= 0xCu;
+    return w;
 }
 
 // (plus - minus) contribution of control*target for one word (tableau.hpp:336-342). Only

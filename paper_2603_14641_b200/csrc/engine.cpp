@@ -1,5 +1,6 @@
 // Device-resident schedules, the single-shot driver and layout conversion (engine.hpp).
 #include "engine.hpp"
+#include "fuse.hpp"
 
 #include <algorithm>
 #include <thread>
@@ -49,7 +50,58 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
 // parallel stable scatter straight into packed device words, then one upload. Windows built
 // by the plan are operand-disjoint by construction; the only error the reference would raise
 // later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
-std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st) {
+// Rewrites a planned schedule with the gate fusion of fuse.hpp: unitary windows go through the
+// Fuser, pending single-qubit operations are flushed in a window of their own before every
+// measurement window and at the end, measurement windows measure the physical rows of their
+// logical qubits. Windows that end up empty are dropped.
+void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vector<uint64_t> &out,
+               std::vector<uint32_t> &record_qubits, std::vector<uint32_t> &perm) {
+    Fuser f(n);
+    const std::vector<uint64_t> offsets = ds.offsets;
+    const std::vector<uint8_t> is_meas = ds.is_meas;
+    ds.offsets.assign(1, 0);
+    ds.is_meas.clear();
+    ds.mqubits.clear();
+    ds.wwords.clear();
+    auto close_unitary = [&](size_t s0) {
+        if (out.size() == s0) return;
+        uint32_t words = 0;
+        for (size_t i = s0; i < out.size(); ++i)
+            words += uint32_t(__builtin_popcount(packed_reads(out[i])) + __builtin_popcount(packed_writes(out[i])));
+        ds.offsets.push_back(out.size());
+        ds.is_meas.push_back(0);
+        ds.mqubits.emplace_back();
+        ds.wwords.push_back(words);
+    };
+    for (size_t w = 0; w + 1 < offsets.size(); ++w) {
+        const uint64_t b = offsets[w], e = offsets[w + 1];
+        size_t s0 = out.size();
+        if (!is_meas[w]) {
+            f.unitary(packed + b, e - b, out);
+            close_unitary(s0);
+            continue;
+        }
+        f.flush(out);
+        close_unitary(s0);
+        std::vector<uint32_t> phys;
+        for (uint64_t i = b; i < e; ++i) {
+            const uint32_t q = packed_q0(packed[i]);
+            record_qubits.push_back(q);
+            phys.push_back(f.phys(q));
+            out.push_back(pack_dev(QSR_MEASURE, f.phys(q), 0));
+        }
+        ds.offsets.push_back(out.size());
+        ds.is_meas.push_back(1);
+        ds.mqubits.push_back(std::move(phys));
+        ds.wwords.push_back(0);
+    }
+    const size_t s0 = out.size();
+    f.flush(out);
+    close_unitary(s0);
+    if (!f.identity_permutation()) perm = f.permutation();
+}
+
+std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st, bool fuse) {
     TraceScope tr_all("upload_circuit");
     WindowPlan p = [&] {
         TraceScope tr("  plan_windows");
@@ -78,16 +130,44 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
             ds->unitary_count += e - b;
             continue;
         }
-        for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(uint32_t(packed[i] & 0x0FFFFFFFu));
+        for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(packed_q0(packed[i]));
         ds->measure_count += e - b;
     }
     QSR_CUDA(cudaSetDevice(device));
-    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
-    if (G) {
-        TraceScope tr("  gates H2D");
-        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
-        QSR_CUDA(cudaStreamSynchronize(st));
+    const uint64_t *dev_gates = packed.get();
+    uint64_t DG = G;
+    std::vector<uint64_t> fused;
+    if (fuse && fusion_enabled()) {
+        TraceScope tr("  fuse");
+        std::vector<uint32_t> rq, perm;
+        fused.reserve(G);
+        fuse_into(*ds, c.num_qubits, packed.get(), fused, rq, perm);
+        dev_gates = fused.data();
+        DG = fused.size();
+        if (!rq.empty()) {
+            QSR_CUDA(cudaMalloc(&ds->d_record_qubits, rq.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(ds->d_record_qubits, rq.data(), rq.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+        if (!perm.empty()) {
+            QSR_CUDA(cudaMalloc(&ds->d_perm, perm.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(ds->d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+    } else {
+        for (size_t w = 0; w + 1 < ds->offsets.size(); ++w) {
+            uint32_t words = 0;
+            if (!ds->is_meas[w])
+                for (uint64_t i = ds->offsets[w]; i < ds->offsets[w + 1]; ++i)
+                    words += uint32_t(__builtin_popcount(packed_reads(packed[i])) +
+                                      __builtin_popcount(packed_writes(packed[i])));
+            ds->wwords.push_back(words);
+        }
     }
+    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(DG, 1) * 8));
+    if (DG) {
+        TraceScope tr("  gates H2D");
+        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, dev_gates, DG * 8, cudaMemcpyHostToDevice, st));
+    }
+    QSR_CUDA(cudaStreamSynchronize(st));
     upload_offsets(*ds, st);
     return ds;
 }
@@ -128,8 +208,11 @@ void upload_offsets(DeviceSchedule &ds, cudaStream_t st) {
     QSR_CUDA(cudaStreamSynchronize(st));
 }
 
-uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1) {
+uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1,
+                             double *bytes) {
     if (w1 <= w0) return 0;
+    if (bytes && ds.wwords.size() >= w1)
+        for (uint64_t w = w0; w < w1; ++w) *bytes += (8.0 * ds.wwords[w] + 16.0) * 2.0 * double(t.kg);
     if (gate_segment_enabled() && w1 - w0 >= 2) {
         launch_gate_segment(t, ds.d_gates, ds.d_offsets + w0, uint32_t(w1 - w0));
         return 1;
@@ -161,7 +244,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             QSR_CUDA(cudaEventRecord(a, t.stream));
             uint64_t w1 = w;
             while (w1 < W && !ds.is_meas[w1]) ++w1;
-            rt.gate_launches += run_unitary_windows(t, ds, w, w1);
+            rt.gate_launches += run_unitary_windows(t, ds, w, w1, &rt.gate_bytes);
             w = w1;
             QSR_CUDA(cudaEventRecord(b, t.stream));
             QSR_CUDA(cudaEventSynchronize(b));
@@ -180,6 +263,8 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
         rec_off += m;
         ++w;
     }
+    if (ds.d_record_qubits) launch_set_record_qubits(d_record, ds.d_record_qubits, ds.measure_count, t.stream);
+    if (ds.d_perm) launch_unpermute_rows(t, ds.d_perm);
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));
     float total = 0;

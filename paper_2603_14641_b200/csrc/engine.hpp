@@ -18,28 +18,38 @@ struct DeviceSchedule {
     std::vector<uint64_t> offsets;
     std::vector<uint8_t> is_meas;
     std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
-    uint64_t measure_count = 0, unitary_count = 0;
+    uint64_t measure_count = 0, unitary_count = 0; // of the circuit (before fusion)
+    // Gate fusion (fuse.hpp): per-window device words moved per generator-word (reads + writes,
+    // for the bytes accounting), the logical qubit of every record entry (the windows measure
+    // physical rows) and the final logical -> physical row map (nullptr: identity).
+    std::vector<uint32_t> wwords;
+    uint32_t *d_record_qubits = nullptr;
+    uint32_t *d_perm = nullptr;
     ~DeviceSchedule() {
         cudaSetDevice(device);
-        if (d_gates) cudaFree(d_gates);
-        if (d_offsets) cudaFree(d_offsets);
+        for (void *p : {(void *)d_gates, (void *)d_offsets, (void *)d_record_qubits, (void *)d_perm})
+            if (p) cudaFree(p);
     }
 };
 
 // Validates every window (apply_window / measure_window checks) and uploads the packed gates.
 std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
                                                 cudaStream_t st);
-// Circuit -> device schedule through the O(G) plan (no API Schedule materialised).
-std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st);
+// Circuit -> device schedule through the O(G) plan (no API Schedule materialised); with `fuse`
+// (and QSR_FUSE != 0) the windows are rewritten by the gate fusion of fuse.hpp.
+std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st,
+                                               bool fuse = false);
 
 struct RunTimes {
     double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
+    double gate_bytes = 0; // algorithmic bytes of the gate-window launches (device gates)
     uint64_t gate_launches = 0; // gate-window kernel launches (a segment launch covers many windows)
 };
 
 // Windows [w0, w1) (all unitary) on t: one temporally blocked segment launch when the segment
 // engine is on and there are >= 2 windows, else one launch per window. Returns launches.
-uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1);
+uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1,
+                             double *bytes = nullptr);
 // Groups each unitary window's packed gates by kind (device order inside a window is free).
 void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
                           const std::vector<uint8_t> &is_meas);

@@ -41,12 +41,22 @@ inline int gate_arity(uint8_t kind) {
                : 1;
 }
 
-// Packed device gate word: bits [0,28) q0, [28,32) kind, [32,64) q1. 8 bytes per gate so
-// a whole c5 schedule (124 M gates) is ~1 GB of HBM, read by every gate-window CTA.
-inline uint64_t pack_gate(const qsr_gate &g) {
-    return uint64_t(g.q0 & 0x0FFFFFFFu) | (uint64_t(g.kind & 0xF) << 28) | (uint64_t(g.q1) << 32);
+// Packed device gate word (8 bytes per gate, a whole c5 schedule is ~1 GB of HBM):
+//   bits [0,24) q0 | [24,28) kind | [28,33) pre0 | [33,38) pre1 | [38,62) q1
+// pre0 / pre1 = single-qubit Clifford (index into the 24-element group, fuse.hpp; 0 = identity)
+// applied to operand 0 / 1 before the gate's own rule (gate fusion, fuse.cpp). Device-only kinds
+// beyond the reference's: kDevC1 (pre0 alone on q0) and kDevIswapR (ISWAP after its SWAP part
+// has been absorbed into the qubit relabelling).
+constexpr uint32_t kDevC1 = 11, kDevIswapR = 12;
+inline uint64_t pack_dev(uint32_t kind, uint32_t q0, uint32_t q1, uint32_t pre0 = 0, uint32_t pre1 = 0) {
+    return uint64_t(q0 & 0xFFFFFFu) | (uint64_t(kind & 0xF) << 24) | (uint64_t(pre0 & 31) << 28) |
+           (uint64_t(pre1 & 31) << 33) | (uint64_t(q1 & 0xFFFFFFu) << 38);
 }
-constexpr uint64_t kMaxQubits = (uint64_t(1) << 28) - 1;
+inline uint64_t pack_gate(const qsr_gate &g) { return pack_dev(g.kind, g.q0, g.q1); }
+inline uint32_t packed_q0(uint64_t w) { return uint32_t(w & 0xFFFFFFu); }
+inline uint32_t packed_kind(uint64_t w) { return uint32_t(w >> 24) & 0xF; }
+inline uint32_t packed_q1(uint64_t w) { return uint32_t(w >> 38) & 0xFFFFFFu; }
+constexpr uint64_t kMaxQubits = (uint64_t(1) << 24) - 1; // 16.7 M qubits (a 2.2 PB tableau)
 
 // Philox-4x32-10 (reference rng.hpp:28-55), host side.
 void philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -64,8 +64,9 @@ __device__ __forceinline__ V2 rule2(uint32_t kind, V2 &x0, V2 &z0, V2 &x1, V2 &z
         break;
     }
     case K_SWAP: { V2 t = x0; x0 = x1; x1 = t; t = z0; z0 = z1; z1 = t; break; }
-    case K_ISWAP: {
-        V2 t = x0; x0 = x1; x1 = t; t = z0; z0 = z1; z1 = t;
+    case K_ISWAP:
+    case K_ISWAP_R: { // ISWAP = the swap, then this residual (symmetric in its operands)
+        if (kind == K_ISWAP) { V2 t = x0; x0 = x1; x1 = t; t = z0; z0 = z1; z1 = t; }
         V2 s2 = x0 & x1 & (z0 ^ z1);
         V2 zt = z1 ^ x0;
         V2 zc = z0 ^ x1;
@@ -75,8 +76,37 @@ __device__ __forceinline__ V2 rule2(uint32_t kind, V2 &x0, V2 &z0, V2 &x1, V2 &z
         z1 = zt ^ x1; z0 = zc ^ x0;
         break;
     }
-    default: break;
+    default: break; // K_C1: only its pre-operation
     }
+    return sign;
+}
+
+__device__ __forceinline__ uint64_t bitmask(uint32_t c, int b) { return 0ull - uint64_t((c >> b) & 1u); }
+
+// One of the 24 single-qubit Cliffords (kCliff1) on a word pair; returns the sign-flip words.
+__device__ __forceinline__ V2 cliff1_apply(uint32_t e, V2 &x, V2 &z) {
+    const uint32_t c = kCliff1[e];
+    const uint64_t m00 = bitmask(c, 0), m01 = bitmask(c, 1), m10 = bitmask(c, 2), m11 = bitmask(c, 3);
+    const uint64_t fx = bitmask(c, 4), fz = bitmask(c, 5), fy = bitmask(c, 6);
+    V2 f, nx, nz;
+    f.a = (fx & x.a & ~z.a) ^ (fz & z.a & ~x.a) ^ (fy & x.a & z.a);
+    f.b = (fx & x.b & ~z.b) ^ (fz & z.b & ~x.b) ^ (fy & x.b & z.b);
+    nx.a = (m00 & x.a) ^ (m01 & z.a);
+    nx.b = (m00 & x.b) ^ (m01 & z.b);
+    nz.a = (m10 & x.a) ^ (m11 & z.a);
+    nz.b = (m10 & x.b) ^ (m11 & z.b);
+    x = nx;
+    z = nz;
+    return f;
+}
+
+// A packed gate on its operand words: the fused single-qubit pre-operations, then the rule.
+__device__ __forceinline__ V2 gate2(uint64_t gw, V2 &x0, V2 &z0, V2 &x1, V2 &z1) {
+    V2 sign{0, 0};
+    const uint32_t p0 = gate_pre0(gw), p1 = gate_pre1(gw);
+    if (p0) sign ^= cliff1_apply(p0, x0, z0);
+    if (p1) sign ^= cliff1_apply(p1, x1, z1);
+    sign ^= rule2(gate_kind(gw), x0, z0, x1, z1);
     return sign;
 }
 
@@ -100,15 +130,15 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
     if (active) {
         uint32_t g = g_begin + warp;
         for (; g + kWarps * (U - 1) < g_end; g += kWarps * U) {
-            uint32_t kind[U], rd[U], wr[U];
+            uint64_t gws[U];
+            uint32_t rd[U], wr[U];
             uint64_t o0[U], o1[U];
             V2 X0[U], Z0[U], X1[U], Z1[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                uint64_t gw = __ldg(gates + g + kWarps * u);
-                kind[u] = gate_kind(gw);
-                rd[u] = kind_reads(kind[u], kSigns);
-                wr[u] = kind_writes(kind[u]);
+                const uint64_t gw = gws[u] = __ldg(gates + g + kWarps * u);
+                rd[u] = gate_reads(gw, kSigns);
+                wr[u] = gate_writes(gw);
                 o0[u] = uint64_t(gate_q0(gw)) * pitch + j;
                 o1[u] = uint64_t(gate_q1(gw)) * pitch + j;
                 X0[u] = Z0[u] = X1[u] = Z1[u] = V2{0, 0};
@@ -119,7 +149,7 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                V2 sg = rule2(kind[u], X0[u], Z0[u], X1[u], Z1[u]);
+                V2 sg = gate2(gws[u], X0[u], Z0[u], X1[u], Z1[u]);
                 if (kSigns) sacc ^= sg;
                 if (wr[u] & 1) st2(x + o0[u], X0[u]);
                 if (wr[u] & 2) st2(z + o0[u], Z0[u]);
@@ -129,14 +159,14 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
         }
         for (; g < g_end; g += kWarps) {
             uint64_t gw = __ldg(gates + g);
-            uint32_t kd = gate_kind(gw), rd = kind_reads(kd, kSigns), wr = kind_writes(kd);
+            uint32_t rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
             uint64_t a0 = uint64_t(gate_q0(gw)) * pitch + j, a1 = uint64_t(gate_q1(gw)) * pitch + j;
             V2 X0{0, 0}, Z0{0, 0}, X1{0, 0}, Z1{0, 0};
             if (rd & 1) X0 = ld2(x + a0);
             if (rd & 2) Z0 = ld2(z + a0);
             if (rd & 4) X1 = ld2(x + a1);
             if (rd & 8) Z1 = ld2(z + a1);
-            V2 sg = rule2(kd, X0, Z0, X1, Z1);
+            V2 sg = gate2(gw, X0, Z0, X1, Z1);
             if (kSigns) sacc ^= sg;
             if (wr & 1) st2(x + a0, X0);
             if (wr & 2) st2(z + a0, Z0);
@@ -354,14 +384,14 @@ __device__ __forceinline__ void seg_prefetch(uint64_t *buf, const uint64_t *gate
 
 template <bool kSigns>
 __device__ __forceinline__ void seg_gate(const SegArgs &a, uint64_t gw, uint64_t j, V2 &sacc) {
-    const uint32_t kd = gate_kind(gw), rd = kind_reads(kd, kSigns), wr = kind_writes(kd);
+    const uint32_t rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
     const uint64_t a0 = uint64_t(gate_q0(gw)) * a.pitch + j, a1 = uint64_t(gate_q1(gw)) * a.pitch + j;
     V2 X0{0, 0}, Z0{0, 0}, X1{0, 0}, Z1{0, 0};
     if (rd & 1) X0 = ld2(a.x + a0);
     if (rd & 2) Z0 = ld2(a.z + a0);
     if (rd & 4) X1 = ld2(a.x + a1);
     if (rd & 8) Z1 = ld2(a.z + a1);
-    const V2 sg2 = rule2(kd, X0, Z0, X1, Z1);
+    const V2 sg2 = gate2(gw, X0, Z0, X1, Z1);
     if (kSigns) sacc ^= sg2;
     if (wr & 1) st2(a.x + a0, X0);
     if (wr & 2) st2(a.z + a0, Z0);
@@ -403,15 +433,15 @@ __global__ void __launch_bounds__(kSegThreads, kMinB) k_gate_segment(SegArgs a) 
             if (act) {
                 uint64_t t = gi;
                 for (; t + uint64_t(gstride) * (kSegU - 1) < nb; t += uint64_t(gstride) * kSegU) {
-                    uint32_t kind[kSegU], wr[kSegU];
+                    uint64_t gws[kSegU];
+                    uint32_t wr[kSegU];
                     uint64_t o0[kSegU], o1[kSegU];
                     V2 X0[kSegU], Z0[kSegU], X1[kSegU], Z1[kSegU];
 #pragma unroll
                     for (int u = 0; u < kSegU; ++u) {
-                        const uint64_t gw = gb[t + uint64_t(gstride) * u];
-                        kind[u] = gate_kind(gw);
-                        const uint32_t rd = kind_reads(kind[u], kSigns);
-                        wr[u] = kind_writes(kind[u]);
+                        const uint64_t gw = gws[u] = gb[t + uint64_t(gstride) * u];
+                        const uint32_t rd = gate_reads(gw, kSigns);
+                        wr[u] = gate_writes(gw);
                         o0[u] = uint64_t(gate_q0(gw)) * pitch + j;
                         o1[u] = uint64_t(gate_q1(gw)) * pitch + j;
                         X0[u] = Z0[u] = X1[u] = Z1[u] = V2{0, 0};
@@ -422,7 +452,7 @@ __global__ void __launch_bounds__(kSegThreads, kMinB) k_gate_segment(SegArgs a) 
                     }
 #pragma unroll
                     for (int u = 0; u < kSegU; ++u) {
-                        const V2 sg2 = rule2(kind[u], X0[u], Z0[u], X1[u], Z1[u]);
+                        const V2 sg2 = gate2(gws[u], X0[u], Z0[u], X1[u], Z1[u]);
                         if (kSigns) sacc ^= sg2;
                         if (wr[u] & 1) st2(a.x + o0[u], X0[u]);
                         if (wr[u] & 2) st2(a.z + o0[u], Z0[u]);
@@ -572,6 +602,49 @@ void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t r
                           uint64_t *zs) {
     launch_segment<false>(xf, zf, pitch, rows, gates, d_woff, nwin, 0, num_sms, st, bar, nullptr,
                           xs, zs);
+}
+
+} // namespace qsr
+
+namespace qsr {
+
+namespace {
+__global__ void k_set_record_qubits(qsr_record_entry *__restrict__ rec, const uint32_t *__restrict__ logical,
+                                    uint64_t m) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += uint64_t(gridDim.x) * blockDim.x)
+        rec[i].qubit = logical[i];
+}
+
+// dst row q = src row perm[q] (q < n), rows n .. rows-1 copied as they are (zero padding).
+__global__ void k_unpermute_rows(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst, uint64_t pitch,
+                                 uint64_t n, uint64_t rows, const uint32_t *__restrict__ perm) {
+    const uint64_t chunks = pitch / 2; // 16-byte chunks per row
+    for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < rows * chunks;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t q = e / chunks, c = e - q * chunks;
+        const uint64_t from = q < n ? perm[q] : q;
+        __stcs(reinterpret_cast<ulonglong2 *>(dst + q * pitch) + c,
+               __ldcs(reinterpret_cast<const ulonglong2 *>(src + from * pitch) + c));
+    }
+}
+} // namespace
+
+void launch_set_record_qubits(qsr_record_entry *rec, const uint32_t *logical, uint64_t m, cudaStream_t st) {
+    if (m == 0) return;
+    k_set_record_qubits<<<unsigned(std::min<uint64_t>((m + 255) / 256, 4096)), 256, 0, st>>>(rec, logical, m);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm) {
+    for (int plane = 0; plane < 2; ++plane) {
+        k_unpermute_rows<<<unsigned(t.num_sms * 8), 512, 0, t.stream>>>(plane ? t.z : t.x, plane ? t.z2 : t.x2,
+                                                                       t.cm_pitch, t.n, t.n_pad, d_perm);
+        QSR_CUDA(cudaGetLastError());
+        count_launch();
+    }
+    std::swap(t.x, t.x2);
+    std::swap(t.z, t.z2);
 }
 
 } // namespace qsr

@@ -208,7 +208,7 @@ struct qsr_sharded {
                 QSR_CUDA(cudaEventRecord(a, t0.stream));
                 const uint64_t w0 = w;
                 while (w < W && !ds->is_meas[w]) ++w;
-                for (auto &s : sh) rt.gate_launches += run_unitary_windows(*s.t, *ds, w0, w);
+                for (auto &s : sh) rt.gate_launches += run_unitary_windows(*s.t, *ds, w0, w, &rt.gate_bytes);
                 // Shard 0's stream waits for the others so the event pair brackets all shards.
                 for (size_t i = 1; i < sh.size(); ++i) {
                     QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
@@ -340,6 +340,14 @@ qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *ga
         if (transpose_ms) *transpose_ms = e->last.t_ms;
         if (measure_ms) *measure_ms = e->last.ge_ms + e->last.cmp_ms;
         if (launches) *launches = e->launches;
+    });
+}
+
+qsr_status qsr_sharded_gate_bytes(const qsr_sharded *e, double *bytes) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        REQUIRE_PTR(bytes);
+        *bytes = e->last.gate_bytes;
     });
 }
 

@@ -19,6 +19,7 @@
 #include <cstring>
 
 #include "engine.hpp"
+#include "fuse.hpp"
 
 namespace qsr {
 
@@ -67,11 +68,41 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     launch_zero_state(t, nullptr);
     QSR_CUDA(cudaMemsetAsync(t.ms.coin_index, 0, 8, t.stream));
 
+    const bool fuse = fusion_enabled();
+    Fuser fuser(fuse ? n : 0);
+    std::vector<uint64_t> dev;            // device gates of the window being emitted
+    std::vector<uint32_t> record_qubits;  // logical qubit of every record entry (fusion)
     std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
     std::vector<std::vector<uint64_t>> buckets(2);
     uint64_t next_key = 2, dev_off = 0, rec_off = 0;
     std::vector<uint8_t> flags;
     std::vector<uint32_t> mq;
+
+    // Stage one device window through the pinned ring (async H2D) and launch it.
+    auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
+        uint32_t words = 0;
+        for (uint64_t i = 0; i < cnt; ++i)
+            words += uint32_t(__builtin_popcount(packed_reads(src[i])) + __builtin_popcount(packed_writes(src[i])));
+        for (uint64_t i = 0; i < cnt;) {
+            if (ring.fill == kRingGates) {
+                QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
+                ring.used[ring.cur] = true;
+                ring.cur ^= 1;
+                ring.fill = 0;
+                if (ring.used[ring.cur]) QSR_CUDA(cudaEventSynchronize(ring.done[ring.cur]));
+            }
+            const uint64_t take = std::min(cnt - i, kRingGates - ring.fill);
+            uint64_t *dst = ring.buf[ring.cur] + ring.fill;
+            std::memcpy(dst, src + i, take * 8);
+            QSR_CUDA(cudaMemcpyAsync(d_gates + dev_off + i, dst, take * 8, cudaMemcpyHostToDevice, t.stream));
+            ring.fill += take;
+            i += take;
+        }
+        launch_gate_window(t, d_gates + dev_off, cnt);
+        ++rt.gate_launches;
+        rt.gate_bytes += (8.0 * words + 16.0) * 2.0 * double(t.kg);
+        dev_off += cnt;
+    };
 
     // Upload + launch every window with key in [next_key, limit).
     auto emit = [&](uint64_t limit) {
@@ -97,32 +128,35 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             const uint64_t cnt = b.size();
             ++counts.windows;
             if ((next_key & 1) == 0) {
-                open_run();
-                // Stage through the pinned ring, then one async H2D per slot fill.
-                for (uint64_t i = 0; i < cnt;) {
-                    if (ring.fill == kRingGates) {
-                        QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
-                        ring.used[ring.cur] = true;
-                        ring.cur ^= 1;
-                        ring.fill = 0;
-                        if (ring.used[ring.cur]) QSR_CUDA(cudaEventSynchronize(ring.done[ring.cur]));
-                    }
-                    const uint64_t take = std::min(cnt - i, kRingGates - ring.fill);
-                    uint64_t *dst = ring.buf[ring.cur] + ring.fill;
-                    std::memcpy(dst, b.data() + i, take * 8);
-                    QSR_CUDA(cudaMemcpyAsync(d_gates + dev_off + i, dst, take * 8, cudaMemcpyHostToDevice,
-                                             t.stream));
-                    ring.fill += take;
-                    i += take;
-                }
-                launch_gate_window(t, d_gates + dev_off, cnt);
-                ++rt.gate_launches;
-                dev_off += cnt;
                 counts.unitary += cnt;
+                const uint64_t *src = b.data();
+                uint64_t ng = cnt;
+                if (fuse) {
+                    dev.clear();
+                    fuser.unitary(b.data(), cnt, dev);
+                    src = dev.data();
+                    ng = dev.size();
+                }
+                if (ng) {
+                    open_run();
+                    launch_staged(src, ng);
+                }
             } else {
+                if (fuse) {
+                    dev.clear();
+                    fuser.flush(dev);
+                    if (!dev.empty()) {
+                        open_run();
+                        launch_staged(dev.data(), dev.size());
+                    }
+                }
                 close_run();
                 mq.resize(cnt);
-                for (uint64_t i = 0; i < cnt; ++i) mq[i] = uint32_t(b[i] & 0x0FFFFFFFu);
+                for (uint64_t i = 0; i < cnt; ++i) {
+                    const uint32_t q = packed_q0(b[i]);
+                    mq[i] = fuse ? fuser.phys(q) : q;
+                    if (fuse) record_qubits.push_back(q);
+                }
                 t.ensure_window_cap(cnt);
                 QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
                 measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
@@ -164,6 +198,35 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
         emit(2 * uint64_t(rmin) + 1);
     }
     emit(~uint64_t(0));
+    if (fuse) {
+        dev.clear();
+        fuser.flush(dev);
+        if (!dev.empty()) {
+            cudaEvent_t ra, rb;
+            QSR_CUDA(cudaEventCreate(&ra));
+            QSR_CUDA(cudaEventCreate(&rb));
+            QSR_CUDA(cudaEventRecord(ra, t.stream));
+            launch_staged(dev.data(), dev.size());
+            QSR_CUDA(cudaEventRecord(rb, t.stream));
+            to_events.emplace_back(ra, rb);
+        }
+        uint32_t *d_rq = nullptr, *d_perm = nullptr;
+        if (!record_qubits.empty()) {
+            QSR_CUDA(cudaMalloc(&d_rq, record_qubits.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(d_rq, record_qubits.data(), record_qubits.size() * 4, cudaMemcpyHostToDevice,
+                                     t.stream));
+            launch_set_record_qubits(d_record, d_rq, record_qubits.size(), t.stream);
+        }
+        if (!fuser.identity_permutation()) {
+            const auto &perm = fuser.permutation();
+            QSR_CUDA(cudaMalloc(&d_perm, perm.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, t.stream));
+            launch_unpermute_rows(t, d_perm);
+        }
+        QSR_CUDA(cudaStreamSynchronize(t.stream));
+        if (d_rq) cudaFree(d_rq);
+        if (d_perm) cudaFree(d_perm);
+    }
 
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));

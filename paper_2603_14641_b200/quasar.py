@@ -643,8 +643,10 @@ class Engine:
     def stats(self) -> dict:
         g, gl, t, m, l = C.c_double(), C.c_uint64(), C.c_double(), C.c_double(), C.c_uint64()
         check(lib.qsr_engine_stats(self._h, C.byref(g), C.byref(gl), C.byref(t), C.byref(m), C.byref(l)))
+        b = C.c_double()
+        check(lib.qsr_engine_gate_bytes(self._h, C.byref(b)))
         return {"gate_ms": g.value, "gate_launches": gl.value, "transpose_ms": t.value,
-                "measure_ms": m.value, "launches": l.value}
+                "measure_ms": m.value, "launches": l.value, "gate_bytes": b.value}
 
     def record(self) -> np.ndarray:
         rec = np.zeros(max(self._nm, 1), dtype=ENTRY_DTYPE)
@@ -725,8 +727,10 @@ class ShardedEngine:
     def stats(self) -> dict:
         g, gl, t, m, l = C.c_double(), C.c_uint64(), C.c_double(), C.c_double(), C.c_uint64()
         check(lib.qsr_sharded_stats(self._h, C.byref(g), C.byref(gl), C.byref(t), C.byref(m), C.byref(l)))
+        b = C.c_double()
+        check(lib.qsr_sharded_gate_bytes(self._h, C.byref(b)))
         return {"gate_ms": g.value, "gate_launches": gl.value, "transpose_ms": t.value,
-                "measure_ms": m.value, "launches": l.value}
+                "measure_ms": m.value, "launches": l.value, "gate_bytes": b.value}
 
     def record(self) -> np.ndarray:
         rec = np.zeros(max(self._nm, 1), dtype=ENTRY_DTYPE)
