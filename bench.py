@@ -207,7 +207,7 @@ def main():
             return q.ShardedEngine(circ, world, device=device, exchange="nccl", rank=rank, nccl_id=nccl_id)
         if shards > 1:
             return q.ShardedEngine(circ, shards, device=device, exchange="local")
-        return q.Engine(circ, sched, device=device)
+        return q.Engine(circ, device=device)  # circuit upload: scheduled + gate-fused (fuse.hpp)
 
     t0 = time.time()
     eng = make_engine()

@@ -229,15 +229,19 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
     }
 }
 
-// Kernel variants (unroll U, min resident CTAs): 0 = <2,3>, 1 = <1,4>, 2 = <2,4>.
+// Kernel variants (unroll U, min resident CTAs): 0 = <2,3>, 1 = <1,4>, 2 = <2,4>, 3 = <2,2>,
+// 4 = <4,2>.
 // QSR_GATE_VARIANT selects one for tuning runs; the default is the measured best
 // (profiles/r01_gate_tune.log: <2,3> 6.37 TB/s at c5, <1,4> 6.31, <2,4> 6.07 with spills).
-int gate_variant() {
+// Default: <1,4> for big windows (fused c5: 216.7 vs 226.2 ms per 100 windows at 180k qubits,
+// no spills at 64 registers), <2,3> for small ones (20k qubits: 10.5 vs 11.1 ms per 300).
+int gate_variant(uint64_t ngates) {
     static int v = [] {
         const char *e = getenv("QSR_GATE_VARIANT");
-        return e ? atoi(e) : 0;
+        return e ? atoi(e) : -1;
     }();
-    return v;
+    if (v >= 0) return v;
+    return ngates >= (uint64_t(1) << 16) ? 1 : 0;
 }
 
 template <bool kSigns, int U, int B>
@@ -291,9 +295,17 @@ void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uin
             uint32_t *counters, uint64_t *s) {
     if (ngates == 0)
         return;
-    switch (gate_variant()) {
+    switch (gate_variant(ngates)) {
     case 0:
         launch_variant<kSigns, 2, 3>(x, z, pitch, gates, ngates, num_sms, st, partials,
+                                     partial_chunks, counters, s);
+        break;
+    case 3:
+        launch_variant<kSigns, 2, 2>(x, z, pitch, gates, ngates, num_sms, st, partials,
+                                     partial_chunks, counters, s);
+        break;
+    case 4:
+        launch_variant<kSigns, 4, 2>(x, z, pitch, gates, ngates, num_sms, st, partials,
                                      partial_chunks, counters, s);
         break;
     case 2:
