@@ -256,7 +256,9 @@ def main():
     if tp.exists():
         try:
             for d in json.loads(tp.read_text()).get("entries", []):
-                if d.get("config") == args.config and d.get("kernel", "").startswith(kernel) and shards == 1:
+                fused = os.environ.get("QSR_FUSE", "1") != "0" and world == 1 and shards == 1
+                if (d.get("config") == args.config and d.get("kernel", "").startswith(kernel) and shards == 1
+                        and bool(d.get("fused", False)) == fused):
                     traffic = d.get("dram_bytes_per_launch")
         except Exception:
             pass
