@@ -229,6 +229,12 @@ struct qsr_sharded {
             rec_off += mq.size();
             ++w;
         }
+        // Gate fusion (fuse.hpp): logical qubits into the record, rows back to logical order.
+        for (auto &s : sh) {
+            if (ds->d_record_qubits)
+                launch_set_record_qubits(s.d_rec, ds->d_record_qubits, ds->measure_count, s.t->stream);
+            if (ds->d_perm) launch_unpermute_rows(*s.t, ds->d_perm);
+        }
         for (size_t i = 1; i < sh.size(); ++i) {
             QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
             QSR_CUDA(cudaStreamWaitEvent(t0.stream, b, 0));
@@ -300,7 +306,7 @@ qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
         }
         e->ds = s ? upload_schedule(e->n, *s, cfg->device,
                                     e->sh[0].t->stream)
-                  : upload_circuit(circ, cfg->device, e->sh[0].t->stream);
+                  : upload_circuit(circ, cfg->device, e->sh[0].t->stream, true);
         if (e->ds->measure_count != circ.measure_count())
             fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
         const uint64_t nm = std::max<uint64_t>(e->ds->measure_count, 1);
