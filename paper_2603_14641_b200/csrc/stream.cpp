@@ -79,10 +79,9 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     std::vector<uint32_t> mq;
 
     // Stage one device window through the pinned ring (async H2D) and launch it.
+    // (No per-gate byte accounting here: the host is on the critical path of this pipeline; the
+    // resident engines report gate bytes.)
     auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
-        uint32_t words = 0;
-        for (uint64_t i = 0; i < cnt; ++i)
-            words += uint32_t(__builtin_popcount(packed_reads(src[i])) + __builtin_popcount(packed_writes(src[i])));
         for (uint64_t i = 0; i < cnt;) {
             if (ring.fill == kRingGates) {
                 QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
@@ -100,7 +99,6 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
         }
         launch_gate_window(t, d_gates + dev_off, cnt);
         ++rt.gate_launches;
-        rt.gate_bytes += (8.0 * words + 16.0) * 2.0 * double(t.kg);
         dev_off += cnt;
     };
 
