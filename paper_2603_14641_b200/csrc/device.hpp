@@ -120,11 +120,8 @@ void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t r
                           const uint64_t *gates, const uint64_t *d_woff, uint32_t nwin,
                           int num_sms, cudaStream_t st, unsigned int *bar, uint64_t *xs,
                           uint64_t *zs); // xs, zs: scratch planes of the same size (slab-major)
-// Gate fusion support (fuse.hpp): record entries rewritten with their logical qubits, and the
-// CM rows un-permuted (logical q <- physical perm[q]) into the spare planes, which then become
-// the current ones.
-void launch_set_record_qubits(qsr_record_entry *rec, const uint32_t *logical, uint64_t m,
-                              cudaStream_t st);
+// Gate fusion support (fuse.hpp): the CM rows un-permuted (logical q <- physical perm[q]) into
+// the spare planes, which then become the current ones.
 void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm);
 // Frames: same rules, no signs.
 void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *gates,

@@ -55,7 +55,7 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
 // measurement window and at the end, measurement windows measure the physical rows of their
 // logical qubits. Windows that end up empty are dropped.
 void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vector<uint64_t> &out,
-               std::vector<uint32_t> &record_qubits, std::vector<uint32_t> &perm) {
+               std::vector<uint32_t> &perms) {
     Fuser f(n);
     const std::vector<uint64_t> offsets = ds.offsets;
     const std::vector<uint8_t> is_meas = ds.is_meas;
@@ -83,22 +83,32 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         }
         f.flush(out);
         close_unitary(s0);
-        std::vector<uint32_t> phys;
+        auto unpermute_here = [&] {
+            ds.perm_at.resize(ds.is_meas.size() + 1, -1);
+            if (f.identity_permutation()) return;
+            ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
+            perms.insert(perms.end(), f.permutation().begin(), f.permutation().end());
+            f.reset_permutation();
+        };
+        unpermute_here();
+        std::vector<uint32_t> qs;
         for (uint64_t i = b; i < e; ++i) {
-            const uint32_t q = packed_q0(packed[i]);
-            record_qubits.push_back(q);
-            phys.push_back(f.phys(q));
-            out.push_back(pack_dev(QSR_MEASURE, f.phys(q), 0));
+            qs.push_back(packed_q0(packed[i]));
+            out.push_back(packed[i]);
         }
         ds.offsets.push_back(out.size());
         ds.is_meas.push_back(1);
-        ds.mqubits.push_back(std::move(phys));
+        ds.mqubits.push_back(std::move(qs));
         ds.wwords.push_back(0);
     }
     const size_t s0 = out.size();
     f.flush(out);
     close_unitary(s0);
-    if (!f.identity_permutation()) perm = f.permutation();
+    ds.perm_at.resize(ds.is_meas.size() + 1, -1);
+    if (!f.identity_permutation()) {
+        ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
+        perms.insert(perms.end(), f.permutation().begin(), f.permutation().end());
+    }
 }
 
 std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st, bool fuse) {
@@ -139,18 +149,14 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
     std::vector<uint64_t> fused;
     if (fuse && fusion_enabled()) {
         TraceScope tr("  fuse");
-        std::vector<uint32_t> rq, perm;
+        std::vector<uint32_t> perms;
         fused.reserve(G);
-        fuse_into(*ds, c.num_qubits, packed.get(), fused, rq, perm);
+        fuse_into(*ds, c.num_qubits, packed.get(), fused, perms);
         dev_gates = fused.data();
         DG = fused.size();
-        if (!rq.empty()) {
-            QSR_CUDA(cudaMalloc(&ds->d_record_qubits, rq.size() * 4));
-            QSR_CUDA(cudaMemcpyAsync(ds->d_record_qubits, rq.data(), rq.size() * 4, cudaMemcpyHostToDevice, st));
-        }
-        if (!perm.empty()) {
-            QSR_CUDA(cudaMalloc(&ds->d_perm, perm.size() * 4));
-            QSR_CUDA(cudaMemcpyAsync(ds->d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, st));
+        if (!perms.empty()) {
+            QSR_CUDA(cudaMalloc(&ds->d_perms, perms.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(ds->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, st));
         }
     } else {
         for (size_t w = 0; w + 1 < ds->offsets.size(); ++w) {
@@ -253,6 +259,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             rt.to_ms += ms;
             continue;
         }
+        if (const uint32_t *perm = ds.perm_before(w)) launch_unpermute_rows(t, perm);
         const auto &mq = ds.mqubits[w];
         const uint64_t m = mq.size();
         t.ensure_window_cap(m);
@@ -263,8 +270,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
         rec_off += m;
         ++w;
     }
-    if (ds.d_record_qubits) launch_set_record_qubits(d_record, ds.d_record_qubits, ds.measure_count, t.stream);
-    if (ds.d_perm) launch_unpermute_rows(t, ds.d_perm);
+    if (const uint32_t *perm = ds.perm_before(W)) launch_unpermute_rows(t, perm);
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));
     float total = 0;

@@ -20,15 +20,19 @@ struct DeviceSchedule {
     std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
     uint64_t measure_count = 0, unitary_count = 0; // of the circuit (before fusion)
     // Gate fusion (fuse.hpp): per-window device words moved per generator-word (reads + writes,
-    // for the bytes accounting), the logical qubit of every record entry (the windows measure
-    // physical rows) and the final logical -> physical row map (nullptr: identity).
+    // for the bytes accounting) and where the CM rows return to logical order.
     std::vector<uint32_t> wwords;
-    uint32_t *d_record_qubits = nullptr;
-    uint32_t *d_perm = nullptr;
+    // perm_at[w] >= 0: before window w (w == num_windows: after the last one) un-permute the CM
+    // rows with the logical -> physical map at d_perms + perm_at[w].
+    std::vector<int64_t> perm_at;
+    uint32_t *d_perms = nullptr;
     ~DeviceSchedule() {
         cudaSetDevice(device);
-        for (void *p : {(void *)d_gates, (void *)d_offsets, (void *)d_record_qubits, (void *)d_perm})
+        for (void *p : {(void *)d_gates, (void *)d_offsets, (void *)d_perms})
             if (p) cudaFree(p);
+    }
+    const uint32_t *perm_before(uint64_t w) const {
+        return (w < perm_at.size() && perm_at[w] >= 0) ? d_perms + perm_at[w] : nullptr;
     }
 };
 

@@ -13,8 +13,9 @@
 // Every rule acts on each generator bit independently, so composing the per-bit actions composes
 // the gates exactly (conjugation is a group homomorphism, signs included). Gates of one window act
 // on disjoint logical qubits, hence on disjoint physical rows; the emitted windows stay disjoint.
-// Measurement windows measure the physical rows of their logical qubits; the record is written
-// with the logical qubit, and the final tableau is un-permuted on the device.
+// Before every measurement window (and at the end) the device rows are un-permuted to logical
+// order and the map reset, so measurements see logical qubits (their batch qubits stay adjacent
+// in the tableau words, and the record needs no fix-up).
 #pragma once
 
 #include <cstdint>
@@ -43,6 +44,8 @@ class Fuser {
     uint32_t phys(uint32_t q) const { return pi_[q]; }
     const std::vector<uint32_t> &permutation() const { return pi_; } // logical -> physical
     bool identity_permutation() const;
+    // After the device rows were un-permuted to logical order.
+    void reset_permutation();
 
   private:
     std::vector<uint32_t> pi_;

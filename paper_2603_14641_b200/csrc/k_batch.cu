@@ -255,9 +255,14 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
     __syncthreads();
     const uint64_t i = uint64_t(blockIdx.x) * kRowThreads + tid;
     const bool act = i < pitch;
+    // All pivot rows' batch-start words first (independent loads, all in flight at once).
     for (uint32_t m = 0; m < len; ++m) {
         const uint64_t rs = ng + s_c[m];
-        u64 cx = act ? x[rs * pitch + i] : 0ull, cz = act ? z[rs * pitch + i] : 0ull;
+        sv[m][0][tid] = act ? __ldcg(x + rs * pitch + i) : 0ull;
+        sv[m][1][tid] = act ? __ldcg(z + rs * pitch + i) : 0ull;
+    }
+    for (uint32_t m = 0; m < len; ++m) {
+        u64 cx = sv[m][0][tid], cz = sv[m][1][tid];
         int e = __popcll(cx & cz);
         u64 acc = 0;
         for (uint32_t U = s_mc[m]; U; U &= U - 1) {
@@ -293,41 +298,59 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
 }
 
 // B3. Signs of the V_m (telescoped phase, file header), coins, record entries and the signs of
-// the replaced pairs, in collapse order (one thread; len <= 32 steps).
-__global__ void k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
-                               const uint32_t *__restrict__ fq, const uint32_t *__restrict__ fidx,
-                               uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-                               const int *__restrict__ pcount, uint64_t seed,
-                               uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
-                               int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
-    if (threadIdx.x != 0) return;
+// the replaced pairs. One warp: lane m stages collapse m's inputs and draws its coin (coins depend
+// only on their index), lane 0 runs the sign chain over shared memory, lanes write the results.
+__global__ void __launch_bounds__(32)
+k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
+               const uint32_t *__restrict__ fq, const uint32_t *__restrict__ fidx,
+               uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
+               const int *__restrict__ pcount, uint64_t seed,
+               uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
+               int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
+    __shared__ uint32_t s_c[kB], s_mc[kB], s_ss[kB], s_coin[kB], s_vsign[kB], s_beta[kB];
+    __shared__ int s_e[kB];
+    const uint32_t lane = threadIdx.x;
     const uint32_t len = bctl[BL_LEN];
-    uint32_t vsign[kB], beta[kB];
-    uint64_t idx = *coin_index;
-    for (uint32_t m = 0; m < len; ++m) {
-        const uint64_t c = vinfo[VI_C + m] - g0, rs = ng + c, rd = c;
-        const uint32_t Mc = vinfo[VI_MC + m];
-        int E = pcount[m];
-        uint32_t sign = uint32_t((s[rs >> 6] >> (rs & 63)) & 1u);
-        for (uint32_t U = Mc; U; U &= U - 1) {
-            const uint32_t j = __ffs(U) - 1;
-            E += int(beta[j]);
-            sign ^= vsign[j];
-        }
-        if (E & 1) atomicExch(err, 1);
-        sign ^= (uint32_t(E) >> 1) & 1u;
-        vsign[m] = sign;
-        beta[m] = uint32_t(pcount[kB + m]) & 3u;
-        const uint32_t coin = draw_coin(seed, idx, coin_table);
-        ++idx;
-        out[fidx[m]] = qsr_record_entry{fq[m], uint8_t(coin), 0};
-        s[rd >> 6] = (s[rd >> 6] & ~(1ull << (rd & 63))) | (uint64_t(sign) << (rd & 63));
-        s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (uint64_t(coin) << (rs & 63));
-        vinfo[VI_SIGN + m] = sign;
-        vinfo[VI_BETA + m] = beta[m];
+    const uint64_t idx0 = *coin_index;
+    if (lane < len) {
+        const uint64_t c = vinfo[VI_C + lane] - g0, rs = ng + c;
+        s_c[lane] = uint32_t(c);
+        s_mc[lane] = vinfo[VI_MC + lane];
+        s_e[lane] = pcount[lane];
+        s_beta[lane] = uint32_t(pcount[kB + lane]) & 3u;
+        s_ss[lane] = uint32_t((s[rs >> 6] >> (rs & 63)) & 1u); // S_c sign at batch start
+        s_coin[lane] = draw_coin(seed, idx0 + lane, coin_table);
     }
-    for (uint32_t m = len; m < kB; ++m) vinfo[VI_SIGN + m] = 0, vinfo[VI_BETA + m] = 0;
-    *coin_index = idx;
+    __syncwarp();
+    if (lane == 0) {
+        bool odd = false;
+        for (uint32_t m = 0; m < len; ++m) {
+            int E = s_e[m];
+            uint32_t sign = s_ss[m];
+            for (uint32_t U = s_mc[m]; U; U &= U - 1) {
+                const uint32_t j = __ffs(U) - 1;
+                E += int(s_beta[j]);
+                sign ^= s_vsign[j];
+            }
+            odd |= (E & 1) != 0;
+            s_vsign[m] = sign ^ ((uint32_t(E) >> 1) & 1u);
+            // Replaced pair: D_c <- sign of V_m, S_c <- coin (same 64-bit words possible: serial).
+            const uint64_t c = s_c[m], rs = ng + c;
+            s[c >> 6] = (s[c >> 6] & ~(1ull << (c & 63))) | (uint64_t(s_vsign[m]) << (c & 63));
+            s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (uint64_t(s_coin[m]) << (rs & 63));
+        }
+        if (odd) atomicExch(err, 1);
+        *coin_index = idx0 + len;
+    }
+    __syncwarp();
+    if (lane < len) {
+        out[fidx[lane]] = qsr_record_entry{fq[lane], uint8_t(s_coin[lane]), 0};
+        vinfo[VI_SIGN + lane] = s_vsign[lane];
+        vinfo[VI_BETA + lane] = s_beta[lane];
+    } else {
+        vinfo[VI_SIGN + lane] = 0;
+        vinfo[VI_BETA + lane] = 0;
+    }
 }
 
 // ---- phase B: pivots, pivot rows, coins (one CTA) --------------------------------------

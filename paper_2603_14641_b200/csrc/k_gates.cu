@@ -621,12 +621,6 @@ void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t r
 namespace qsr {
 
 namespace {
-__global__ void k_set_record_qubits(qsr_record_entry *__restrict__ rec, const uint32_t *__restrict__ logical,
-                                    uint64_t m) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += uint64_t(gridDim.x) * blockDim.x)
-        rec[i].qubit = logical[i];
-}
-
 // dst row q = src row perm[q] (q < n), rows n .. rows-1 copied as they are (zero padding).
 __global__ void k_unpermute_rows(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst, uint64_t pitch,
                                  uint64_t n, uint64_t rows, const uint32_t *__restrict__ perm) {
@@ -640,13 +634,6 @@ __global__ void k_unpermute_rows(const uint64_t *__restrict__ src, uint64_t *__r
     }
 }
 } // namespace
-
-void launch_set_record_qubits(qsr_record_entry *rec, const uint32_t *logical, uint64_t m, cudaStream_t st) {
-    if (m == 0) return;
-    k_set_record_qubits<<<unsigned(std::min<uint64_t>((m + 255) / 256, 4096)), 256, 0, st>>>(rec, logical, m);
-    QSR_CUDA(cudaGetLastError());
-    count_launch();
-}
 
 void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm) {
     for (int plane = 0; plane < 2; ++plane) {

@@ -221,6 +221,8 @@ struct qsr_sharded {
                 rt.to_ms += ms;
                 continue;
             }
+            if (const uint32_t *perm = ds->perm_before(w))
+                for (auto &s : sh) launch_unpermute_rows(*s.t, perm);
             const auto &mq = ds->mqubits[w];
             measure_window(mq, seed, coin, rt);
             for (auto &s : sh)
@@ -229,12 +231,9 @@ struct qsr_sharded {
             rec_off += mq.size();
             ++w;
         }
-        // Gate fusion (fuse.hpp): logical qubits into the record, rows back to logical order.
-        for (auto &s : sh) {
-            if (ds->d_record_qubits)
-                launch_set_record_qubits(s.d_rec, ds->d_record_qubits, ds->measure_count, s.t->stream);
-            if (ds->d_perm) launch_unpermute_rows(*s.t, ds->d_perm);
-        }
+        // Gate fusion (fuse.hpp): rows back to logical order.
+        if (const uint32_t *perm = ds->perm_before(W))
+            for (auto &s : sh) launch_unpermute_rows(*s.t, perm);
         for (size_t i = 1; i < sh.size(); ++i) {
             QSR_CUDA(cudaEventRecord(b, sh[i].t->stream));
             QSR_CUDA(cudaStreamWaitEvent(t0.stream, b, 0));

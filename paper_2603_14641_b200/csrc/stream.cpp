@@ -71,7 +71,6 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     const bool fuse = fusion_enabled();
     Fuser fuser(fuse ? n : 0);
     std::vector<uint64_t> dev;            // device gates of the window being emitted
-    std::vector<uint32_t> record_qubits;  // logical qubit of every record entry (fusion)
     std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
     std::vector<std::vector<uint64_t>> buckets(2);
     uint64_t next_key = 2, dev_off = 0, rec_off = 0;
@@ -100,6 +99,18 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
         launch_gate_window(t, d_gates + dev_off, cnt);
         ++rt.gate_launches;
         dev_off += cnt;
+    };
+
+    // CM rows back to logical order (before a measurement window and at the end).
+    uint32_t *d_perm = nullptr;
+    auto unpermute = [&] {
+        if (fuser.identity_permutation()) return;
+        if (!d_perm) QSR_CUDA(cudaMalloc(&d_perm, uint64_t(n) * 4));
+        QSR_CUDA(cudaMemcpyAsync(d_perm, fuser.permutation().data(), uint64_t(n) * 4, cudaMemcpyHostToDevice,
+                                 t.stream));
+        QSR_CUDA(cudaStreamSynchronize(t.stream)); // the host map is reset right after
+        launch_unpermute_rows(t, d_perm);
+        fuser.reset_permutation();
     };
 
     // Upload + launch every window with key in [next_key, limit).
@@ -147,14 +158,12 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                         open_run();
                         launch_staged(dev.data(), dev.size());
                     }
+                    close_run();
+                    unpermute();
                 }
                 close_run();
                 mq.resize(cnt);
-                for (uint64_t i = 0; i < cnt; ++i) {
-                    const uint32_t q = packed_q0(b[i]);
-                    mq[i] = fuse ? fuser.phys(q) : q;
-                    if (fuse) record_qubits.push_back(q);
-                }
+                for (uint64_t i = 0; i < cnt; ++i) mq[i] = packed_q0(b[i]);
                 t.ensure_window_cap(cnt);
                 QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
                 measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
@@ -208,23 +217,10 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             QSR_CUDA(cudaEventRecord(rb, t.stream));
             to_events.emplace_back(ra, rb);
         }
-        uint32_t *d_rq = nullptr, *d_perm = nullptr;
-        if (!record_qubits.empty()) {
-            QSR_CUDA(cudaMalloc(&d_rq, record_qubits.size() * 4));
-            QSR_CUDA(cudaMemcpyAsync(d_rq, record_qubits.data(), record_qubits.size() * 4, cudaMemcpyHostToDevice,
-                                     t.stream));
-            launch_set_record_qubits(d_record, d_rq, record_qubits.size(), t.stream);
-        }
-        if (!fuser.identity_permutation()) {
-            const auto &perm = fuser.permutation();
-            QSR_CUDA(cudaMalloc(&d_perm, perm.size() * 4));
-            QSR_CUDA(cudaMemcpyAsync(d_perm, perm.data(), perm.size() * 4, cudaMemcpyHostToDevice, t.stream));
-            launch_unpermute_rows(t, d_perm);
-        }
+        unpermute();
         QSR_CUDA(cudaStreamSynchronize(t.stream));
-        if (d_rq) cudaFree(d_rq);
-        if (d_perm) cudaFree(d_perm);
     }
+    if (d_perm) cudaFree(d_perm);
 
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));
