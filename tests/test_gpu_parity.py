@@ -273,11 +273,14 @@ def test_mixed_bell_and_random(q, oracle):
     np.testing.assert_array_equal(r.record_array, rec)
 
 
-@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_APPLY": "rows"}, {"QSR_PIVOTS": "fused"},
-                                 {"QSR_GATE_ENGINE": "segment"}])
+@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_GATE_ENGINE": "segment"},
+                                 {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"}, {"QSR_APPLY": "rows"},
+                                 {"QSR_PIVOTS": "fused"}])
 def test_alternate_collapse_paths_match(q, env):
-    """QSR_MEASURE_BATCH=0 (one collapse per pass) and QSR_APPLY=rows (row-major absorb, one V
-    at a time) must agree with the default (batched, table absorb) and the oracle."""
+    """Every alternate path must agree with the default and the oracle: QSR_MEASURE_BATCH=0 (one
+    collapse per pass), QSR_GATE_ENGINE=segment (temporally blocked gates), QSR_FUSE=0 (no gate
+    fusion), QSR_STREAM=0 (schedule first, then run), QSR_APPLY=rows (row-major absorb, one V at
+    a time), QSR_PIVOTS=fused (single-CTA pivot kernel)."""
     import subprocess
     import sys
     code = (
