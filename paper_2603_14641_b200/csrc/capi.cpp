@@ -145,6 +145,9 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
     QSR_CUDA(cudaMalloc(&ms.gconst, kMaxBatch * 4));
     QSR_CUDA(cudaMalloc(&ms.nz, (ng / 32 + 1) * 4));
     QSR_CUDA(cudaMalloc(&ms.pcount, 2 * kMaxBatch * sizeof(int)));
+    QSR_CUDA(cudaMalloc(&ms.d_pos, 4));
+    QSR_CUDA(cudaMallocHost(&ms.h_bctl, 2 * 4 * 4));
+    for (auto &e : ms.bev) QSR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
 }
@@ -152,6 +155,9 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
 DeviceTableau::~DeviceTableau() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    if (ms.h_bctl) cudaFreeHost(ms.h_bctl);
+    for (auto e : ms.bev)
+        if (e) cudaEventDestroy(e);
     for (uint64_t *p : {x, z, x2, z2}) plane_cache().release(device, plane_words * 8, p);
     if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf);
     gate_buf = nullptr;
@@ -160,7 +166,7 @@ DeviceTableau::~DeviceTableau() {
                     (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
                     (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
                     (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits,
-                    (void *)ms.batch_block, (void *)ms.partial, (void *)ms.gconst, (void *)ms.nz, (void *)ms.pcount, (void *)ms.fq,
+                    (void *)ms.batch_block, (void *)ms.partial, (void *)ms.gconst, (void *)ms.nz, (void *)ms.pcount, (void *)ms.d_pos, (void *)ms.fq,
                     (void *)ms.fidx, (void *)ms.coin_buf})
         if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
@@ -1002,8 +1008,13 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
             fail(QSR_INVALID_ARGUMENT, "sample: world must be in [1, ceil(shots/64)], 0 <= rank < world");
         const uint64_t w0 = kf_all * uint64_t(rank) / uint64_t(world);
         const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
-        Schedule sched = schedule_windows(*c, QSR_SAMPLING);
+        TraceScope tr_all("sample");
+        Schedule sched = [&] {
+            TraceScope tr("  schedule_windows");
+            return schedule_windows(*c, QSR_SAMPLING);
+        }();
         // Reference shot (frames.hpp:167): the full single-shot pipeline on the device.
+        TraceScope tr_ref("  reference shot");
         DeviceTableau t(c->num_qubits, device);
         auto ds = upload_schedule(t.n, sched, device, t.stream);
         const uint64_t nm = ds->measure_count;
@@ -1027,8 +1038,14 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
             fill_report(report, rt, *ds, ref, wall);
         }
         // Frames over the same device-resident schedule (frames.hpp:171-181).
-        auto f = make_frames(c->num_qubits, shots, seed, device, w0, nw);
+        auto f = [&] {
+            TraceScope tr("  make_frames");
+            auto ff = make_frames(c->num_qubits, shots, seed, device, w0, nw);
+            QSR_CUDA(cudaStreamSynchronize(ff->stream));
+            return ff;
+        }();
         QSR_CUDA(cudaStreamSynchronize(t.stream));
+        TraceScope tr_frames("  frames windows + fold");
         uint32_t epoch = 1;
         const uint64_t W = ds->is_meas.size();
         for (uint64_t w = 0; w < W;) {

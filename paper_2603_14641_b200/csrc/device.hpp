@@ -57,6 +57,9 @@ struct MeasureScratch {
     uint64_t vstride = 0;
     uint32_t *vinfo = nullptr;
     uint32_t *bctl = nullptr;
+    uint32_t *d_pos = nullptr;      // speculative batch position (k_batch.cu)
+    uint32_t *h_bctl = nullptr;     // pinned [2][4] batch control read-back slots
+    cudaEvent_t bev[2] = {nullptr, nullptr};
     uint8_t *partial = nullptr;     // [slices][2ng] per-(row, slice) phase bytes (k_batch.cu)
     uint64_t partial_bytes = 0;
     uint32_t *gconst = nullptr;     // [kMaxBatch] pair-parity matrix rows of the batch's V's
@@ -147,8 +150,12 @@ void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fid
 // column bits + stabilizer OR-mask (bctl[2]); pivots / V rows / coins / record (leader
 // shard only); every row absorbs its V's.
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b);
+// d_pos / expect: speculative batches (the batch is a no-op unless *d_pos == expect; on success
+// *d_pos = expect + len). nullptr: unconditional.
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                  uint64_t seed);
+                  uint64_t seed, uint32_t *d_pos = nullptr, uint32_t expect = 0);
+bool batch_speculation(); // the split pivot kernels support speculative batches
+void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st);
 void batch_apply(DeviceTableau &t);
 // Deterministic outcome of measuring q (measure.hpp:343-376), sharded form: this shard's
 // ordered partial product is written to `slot` ([x: rm_pitch][z: rm_pitch][e: 16 words]);

@@ -39,7 +39,7 @@ namespace {
 
 using u64 = unsigned long long;
 constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
-enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2 };
+enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2, BL_SKIP = 3 };
 // vinfo layout (u32 [5*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m
 enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_MC = 4 * kB };
 static_assert(5 * kB == kVinfoWords, "vinfo layout");
@@ -86,9 +86,12 @@ __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64
     uint32_t bits = 0;
     if (r < nrows) {
         const uint64_t *row = x + r * pitch;
+        uint32_t wi = 0xFFFFFFFFu;
+        uint64_t word = 0;
         for (uint32_t m = 0; m < b; ++m) {
             const uint32_t q = sq[m];
-            bits |= uint32_t((__ldcg(row + (q >> 6)) >> (q & 63)) & 1u) << m;
+            if ((q >> 6) != wi) { wi = q >> 6; word = __ldcg(row + wi); } // measure-all windows: one load per 64
+            bits |= uint32_t((word >> (q & 63)) & 1u) << m;
         }
         colbits[r] = bits;
     }
@@ -115,7 +118,7 @@ constexpr int kWin = kSelThreads * kSelRows;
 __global__ void __launch_bounds__(kSelThreads)
 k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
                uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
-               uint32_t *__restrict__ bctl) {
+               uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect) {
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
     __shared__ uint32_t s_scan[kSelThreads / 32];
@@ -123,6 +126,13 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nzw = (n_gen + 31) / 32;
     if (tid < kB) s_vbcol[tid] = 0;
+    // Speculative batches (measure_window_device): a batch enqueued behind one that stopped
+    // early starts at the wrong position and turns into a no-op.
+    if (d_pos && *d_pos != expect) {
+        if (tid < kB) vinfo[VI_C + tid] = 0xFFFFFFFFu;
+        if (tid == 0) { bctl[BL_LEN] = 0; bctl[BL_DET] = 0; bctl[BL_SKIP] = 1; }
+        return;
+    }
     if (tid == 0) { s_nwin = 0; s_next = uint32_t(n_gen); s_len = b; s_stop = 0; }
     __syncthreads();
     // Window: the first kWin active stabilizers in ascending order.
@@ -228,8 +238,13 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     if (tid == 0) {
         bctl[BL_LEN] = len;
         bctl[BL_DET] = s_stop;
+        if (d_pos) *d_pos = expect + len;
     }
 }
+
+
+
+__global__ void k_set_u32(uint32_t *p, uint32_t v) { *p = v; }
 
 // B2. Pivot rows, word-parallel: thread = word i of every V_m (m in order, V_j of the same
 // word kept in shared memory), with the telescoped phase pieces of each V_m reduced into
@@ -244,6 +259,7 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
              const uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
     __shared__ u64 sv[kB][2][kRowThreads];
     __shared__ uint32_t s_c[kB], s_mc[kB], s_q[kB];
+    __shared__ int8_t s_e[kB][kRowThreads], s_bend[kB][kRowThreads]; // per word: |e| <= 66, bend <= 64
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31;
@@ -280,12 +296,18 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
             Vx[uint64_t(m) * vstride + i] = cx;
             Vz[uint64_t(m) * vstride + i] = cz;
         }
-        const int es = warp_sum(e), bs = warp_sum(bend);
-        if (lane == 0) {
-            if (es) atomicAdd(pcount + m, es);
-            if (bs) atomicAdd(pcount + kB + m, bs);
-        }
+        s_e[m][tid] = int8_t(e);
+        s_bend[m][tid] = int8_t(bend);
     }
+    // Per-collapse sums over this CTA's words, off the sequential loop: thread m folds row m.
+    __syncthreads();
+    for (uint32_t m = tid; m < len; m += kRowThreads) {
+        int es = 0, bs = 0;
+        for (uint32_t u = 0; u < kRowThreads; ++u) es += s_e[m][u], bs += s_bend[m][u];
+        if (es) atomicAdd(pcount + m, es);
+        if (bs) atomicAdd(pcount + kB + m, bs);
+    }
+    (void)lane;
     if (!act) return;
     // Replace the pivot pairs: D_c <- V_m (bits), S_c <- Z_{q_m}.
     for (uint32_t m = 0; m < len; ++m) {
@@ -887,13 +909,21 @@ bool split_pivots() {
     return on;
 }
 
+void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st) {
+    k_set_u32<<<1, 1, 0, st>>>(p, v);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
+bool batch_speculation() { return split_pivots(); }
+
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                  uint64_t seed) {
+                  uint64_t seed, uint32_t *d_pos, uint32_t expect) {
     MeasureScratch &ms = t.ms;
     if (split_pivots()) {
         QSR_CUDA(cudaMemsetAsync(ms.pcount, 0, 2 * kB * sizeof(int), t.stream));
         k_pivot_select<<<1, kSelThreads, 0, t.stream>>>(ms.colbits, ms.nz, t.n_gen, t.ng, t.g0, b,
-                                                        ms.vinfo, ms.bctl);
+                                                        ms.vinfo, ms.bctl, d_pos, expect);
         QSR_CUDA(cudaGetLastError());
         k_pivot_rows<<<unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads), kRowThreads, 0, t.stream>>>(
             t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz, ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
