@@ -655,7 +655,7 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
         const bool streaming = !s && !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0');
         std::unique_ptr<DeviceSchedule> ds;
         if (!streaming) {
-            ds = s ? upload_schedule(t.n, *s, device, t.stream) : upload_circuit(*c, device, t.stream, true);
+            ds = s ? upload_schedule(t.n, *s, device, t.stream, true) : upload_circuit(*c, device, t.stream, true);
             if (ds->measure_count != nm)
                 fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
         }
@@ -711,7 +711,7 @@ qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int de
         REQUIRE_PTR(c); REQUIRE_PTR(out);
         auto e = std::make_unique<qsr_engine>();
         e->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
-        e->ds = s ? upload_schedule(e->t->n, *s, device, e->t->stream)
+        e->ds = s ? upload_schedule(e->t->n, *s, device, e->t->stream, true)
                   : upload_circuit(*c, device, e->t->stream, true);
         QSR_CUDA(cudaMalloc(&e->d_rec,
                             std::max<uint64_t>(e->ds->measure_count, 1) * sizeof(qsr_record_entry)));

@@ -7,8 +7,11 @@
 
 namespace qsr {
 
+void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint64_t G, int device,
+                   cudaStream_t st, bool fuse);
+
 std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
-                                                cudaStream_t st) {
+                                                cudaStream_t st, bool fuse) {
     // Validate every window first (apply_window / measure_window checks, gates.hpp:149-165,
     // measure.hpp:385-398) so no device state is touched by a schedule that would throw.
     std::vector<uint32_t> stamp(n, 0);
@@ -31,29 +34,18 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
         ds->measure_count += ds->mqubits[w].size();
     }
     const uint64_t G = s.gates.size();
-    QSR_CUDA(cudaSetDevice(device));
-    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(G, 1) * 8));
-    if (G) {
-        std::unique_ptr<uint64_t[]> packed(new uint64_t[G]);
-        for (uint64_t i = 0; i < G; ++i) packed[i] = pack_gate(s.gates[i]);
-        if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
-            sort_unitary_windows(packed.get(), s.offsets, s.is_meas);
-
-        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, packed.get(), G * 8, cudaMemcpyHostToDevice, st));
-        QSR_CUDA(cudaStreamSynchronize(st));
-    }
-    upload_offsets(*ds, st);
+    std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
+    for (uint64_t i = 0; i < G; ++i) packed[i] = pack_gate(s.gates[i]);
+    if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
+        sort_unitary_windows(packed.get(), s.offsets, s.is_meas);
+    upload_packed(*ds, uint32_t(n), packed.get(), G, device, st, fuse);
     return ds;
 }
 
-// Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
-// parallel stable scatter straight into packed device words, then one upload. Windows built
-// by the plan are operand-disjoint by construction; the only error the reference would raise
-// later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
 // Rewrites a planned schedule with the gate fusion of fuse.hpp: unitary windows go through the
 // Fuser, pending single-qubit operations are flushed in a window of their own before every
-// measurement window and at the end, measurement windows measure the physical rows of their
-// logical qubits. Windows that end up empty are dropped.
+// measurement window and at the end, and the rows return to logical order before every
+// measurement window (perm_at). Windows that end up empty are dropped.
 void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vector<uint64_t> &out,
                std::vector<uint32_t> &perms) {
     Fuser f(n);
@@ -111,6 +103,47 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
     }
 }
 
+// Packed gates of a planned / validated schedule -> device (optionally through the gate fusion).
+void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint64_t G, int device,
+                   cudaStream_t st, bool fuse) {
+    QSR_CUDA(cudaSetDevice(device));
+    const uint64_t *dev_gates = packed;
+    uint64_t DG = G;
+    std::vector<uint64_t> fused;
+    if (fuse && fusion_enabled()) {
+        TraceScope tr("  fuse");
+        std::vector<uint32_t> perms;
+        fused.reserve(G);
+        fuse_into(ds, n, packed, fused, perms);
+        dev_gates = fused.data();
+        DG = fused.size();
+        if (!perms.empty()) {
+            QSR_CUDA(cudaMalloc(&ds.d_perms, perms.size() * 4));
+            QSR_CUDA(cudaMemcpyAsync(ds.d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, st));
+        }
+    } else {
+        for (size_t w = 0; w + 1 < ds.offsets.size(); ++w) {
+            uint32_t words = 0;
+            if (!ds.is_meas[w])
+                for (uint64_t i = ds.offsets[w]; i < ds.offsets[w + 1]; ++i)
+                    words += uint32_t(__builtin_popcount(packed_reads(packed[i])) +
+                                      __builtin_popcount(packed_writes(packed[i])));
+            ds.wwords.push_back(words);
+        }
+    }
+    QSR_CUDA(cudaMalloc(&ds.d_gates, std::max<uint64_t>(DG, 1) * 8));
+    if (DG) {
+        TraceScope tr("  gates H2D");
+        QSR_CUDA(cudaMemcpyAsync(ds.d_gates, dev_gates, DG * 8, cudaMemcpyHostToDevice, st));
+    }
+    QSR_CUDA(cudaStreamSynchronize(st));
+    upload_offsets(ds, st);
+}
+
+// Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
+// parallel stable scatter straight into packed device words, then one upload. Windows built
+// by the plan are operand-disjoint by construction; the only error the reference would raise
+// later is the duplicate-qubit measurement window (measure.hpp:394-395), checked up front.
 std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st, bool fuse) {
     TraceScope tr_all("upload_circuit");
     WindowPlan p = [&] {
@@ -143,38 +176,7 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
         for (uint64_t i = b; i < e; ++i) ds->mqubits[w].push_back(packed_q0(packed[i]));
         ds->measure_count += e - b;
     }
-    QSR_CUDA(cudaSetDevice(device));
-    const uint64_t *dev_gates = packed.get();
-    uint64_t DG = G;
-    std::vector<uint64_t> fused;
-    if (fuse && fusion_enabled()) {
-        TraceScope tr("  fuse");
-        std::vector<uint32_t> perms;
-        fused.reserve(G);
-        fuse_into(*ds, c.num_qubits, packed.get(), fused, perms);
-        dev_gates = fused.data();
-        DG = fused.size();
-        if (!perms.empty()) {
-            QSR_CUDA(cudaMalloc(&ds->d_perms, perms.size() * 4));
-            QSR_CUDA(cudaMemcpyAsync(ds->d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, st));
-        }
-    } else {
-        for (size_t w = 0; w + 1 < ds->offsets.size(); ++w) {
-            uint32_t words = 0;
-            if (!ds->is_meas[w])
-                for (uint64_t i = ds->offsets[w]; i < ds->offsets[w + 1]; ++i)
-                    words += uint32_t(__builtin_popcount(packed_reads(packed[i])) +
-                                      __builtin_popcount(packed_writes(packed[i])));
-            ds->wwords.push_back(words);
-        }
-    }
-    QSR_CUDA(cudaMalloc(&ds->d_gates, std::max<uint64_t>(DG, 1) * 8));
-    if (DG) {
-        TraceScope tr("  gates H2D");
-        QSR_CUDA(cudaMemcpyAsync(ds->d_gates, dev_gates, DG * 8, cudaMemcpyHostToDevice, st));
-    }
-    QSR_CUDA(cudaStreamSynchronize(st));
-    upload_offsets(*ds, st);
+    upload_packed(*ds, c.num_qubits, packed.get(), G, device, st, fuse);
     return ds;
 }
 

@@ -38,7 +38,7 @@ struct DeviceSchedule {
 
 // Validates every window (apply_window / measure_window checks) and uploads the packed gates.
 std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, int device,
-                                                cudaStream_t st);
+                                                cudaStream_t st, bool fuse = false);
 // Circuit -> device schedule through the O(G) plan (no API Schedule materialised); with `fuse`
 // (and QSR_FUSE != 0) the windows are rewritten by the gate fusion of fuse.hpp.
 std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cudaStream_t st,

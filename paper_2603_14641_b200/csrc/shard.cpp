@@ -303,8 +303,7 @@ qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
             streams.push_back(sd.t->stream);
             e->sh.push_back(std::move(sd));
         }
-        e->ds = s ? upload_schedule(e->n, *s, cfg->device,
-                                    e->sh[0].t->stream)
+        e->ds = s ? upload_schedule(e->n, *s, cfg->device, e->sh[0].t->stream, true)
                   : upload_circuit(circ, cfg->device, e->sh[0].t->stream, true);
         if (e->ds->measure_count != circ.measure_count())
             fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
