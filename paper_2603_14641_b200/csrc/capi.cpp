@@ -103,9 +103,7 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
     cm_pitch = round_up(2 * kg, 16);
     rm_pitch = round_up(k, 16);
     plane_words = std::max(n_pad * cm_pitch, 2 * ng * rm_pitch);
-    cudaDeviceProp prop;
-    QSR_CUDA(cudaGetDeviceProperties(&prop, device));
-    num_sms = prop.multiProcessorCount;
+    QSR_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
     QSR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
     auto alloc = [&](uint64_t **p, uint64_t words) {
         QSR_CUDA(cudaMalloc(p, words * 8));
@@ -835,9 +833,7 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     auto f = std::make_unique<qsr_frames>();
     f->device = device;
     QSR_CUDA(cudaSetDevice(device));
-    cudaDeviceProp prop;
-    QSR_CUDA(cudaGetDeviceProperties(&prop, device));
-    f->num_sms = prop.multiProcessorCount;
+    QSR_CUDA(cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device));
     QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
     f->n = n;
     f->shots = shots;

@@ -79,7 +79,8 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
             ds.perm_at.resize(ds.is_meas.size() + 1, -1);
             if (f.identity_permutation()) return;
             ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
-            perms.insert(perms.end(), f.permutation().begin(), f.permutation().end());
+            const std::vector<uint32_t> pm = f.permutation();
+            perms.insert(perms.end(), pm.begin(), pm.end());
             f.reset_permutation();
         };
         unpermute_here();
@@ -99,7 +100,8 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
     ds.perm_at.resize(ds.is_meas.size() + 1, -1);
     if (!f.identity_permutation()) {
         ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
-        perms.insert(perms.end(), f.permutation().begin(), f.permutation().end());
+        const std::vector<uint32_t> pm = f.permutation();
+        perms.insert(perms.end(), pm.begin(), pm.end());
     }
 }
 

@@ -41,19 +41,24 @@ class Fuser {
     // All pending single-qubit operations as K_C1 gates (appended; one window's worth).
     void flush(std::vector<uint64_t> &out);
     bool pending() const { return !pend_list_.empty(); }
-    uint32_t phys(uint32_t q) const { return pi_[q]; }
-    const std::vector<uint32_t> &permutation() const { return pi_; } // logical -> physical
+    uint32_t phys(uint32_t q) const { return st_[q].pi; }
+    std::vector<uint32_t> permutation() const; // logical -> physical
     bool identity_permutation() const;
     // After the device rows were un-permuted to logical order.
     void reset_permutation();
 
   private:
-    std::vector<uint32_t> pi_;
-    std::vector<uint8_t> pend_;     // per logical qubit, 0 = identity
-    std::vector<uint8_t> listed_;
+    // One 8-byte record per logical qubit: an operand costs one cache access.
+    struct Q {
+        uint32_t pi;     // physical row
+        uint8_t pend;    // pending single-qubit Clifford, 0 = identity
+        uint8_t listed;  // in pend_list_
+        uint16_t pad;
+    };
+    std::vector<Q> st_;
     std::vector<uint32_t> pend_list_;
     void note(uint32_t q) {
-        if (!listed_[q]) { listed_[q] = 1; pend_list_.push_back(q); }
+        if (!st_[q].listed) { st_[q].listed = 1; pend_list_.push_back(q); }
     }
 };
 

@@ -233,7 +233,8 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
 // 4 = <4,2>.
 // QSR_GATE_VARIANT selects one for tuning runs; the default is the measured best
 // (profiles/r01_gate_tune.log: <2,3> 6.37 TB/s at c5, <1,4> 6.31, <2,4> 6.07 with spills).
-// Default: <1,4> for big windows (fused c5: 216.7 vs 226.2 ms per 100 windows at 180k qubits,
+// Default: <1,4> for windows of >= 16k gates (fused c5 windows, ~45k gates: 216.7 vs 226.2 ms per
+// 100 windows at 180k qubits,
 // no spills at 64 registers), <2,3> for small ones (20k qubits: 10.5 vs 11.1 ms per 300).
 int gate_variant(uint64_t ngates) {
     static int v = [] {
@@ -241,7 +242,7 @@ int gate_variant(uint64_t ngates) {
         return e ? atoi(e) : -1;
     }();
     if (v >= 0) return v;
-    return ngates >= (uint64_t(1) << 16) ? 1 : 0;
+    return ngates >= (uint64_t(1) << 14) ? 1 : 0;
 }
 
 template <bool kSigns, int U, int B>

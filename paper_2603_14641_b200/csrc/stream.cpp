@@ -16,6 +16,12 @@
 // behind another in one window, measure.hpp:394-395) are raised when the offending gate is
 // planned; the tableau being built is then discarded, so no caller-visible state was mutated.
 #include <algorithm>
+#include <thread>
+#include <mutex>
+#include <exception>
+#include <condition_variable>
+#include <array>
+#include <chrono>
 #include <cstring>
 
 #include "engine.hpp"
@@ -50,6 +56,27 @@ struct PinnedRing {
 
 } // namespace
 
+// Buckets of packed gates per window key, in pages that never move: the planner appends to keys
+// at or above the published limit while the emitter reads (and recycles) keys below it.
+class BucketDir {
+  public:
+    explicit BucketDir(uint64_t max_keys) : pages_((max_keys + kPage - 1) / kPage) {}
+    std::vector<uint64_t> &operator[](uint64_t key) {
+        auto &pg = pages_[key / kPage];
+        if (!pg) pg = std::make_unique<Page>();
+        return (*pg)[key % kPage];
+    }
+    std::vector<uint64_t> *find(uint64_t key) {
+        auto &pg = pages_[key / kPage];
+        return pg ? &(*pg)[key % kPage] : nullptr;
+    }
+
+  private:
+    static constexpr uint64_t kPage = 1024;
+    using Page = std::array<std::vector<uint64_t>, kPage>;
+    std::vector<std::unique_ptr<Page>> pages_;
+};
+
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                            qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts) {
     const uint64_t G = c.gates.size();
@@ -59,6 +86,8 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     static thread_local std::unique_ptr<PinnedRing> ring_store;
     if (!ring_store) ring_store = std::make_unique<PinnedRing>();
     PinnedRing &ring = *ring_store;
+    using clk = std::chrono::steady_clock;
+    auto since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
 
     cudaEvent_t e_start, e_end;
     QSR_CUDA(cudaEventCreate(&e_start));
@@ -68,171 +97,253 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     launch_zero_state(t, nullptr);
     QSR_CUDA(cudaMemsetAsync(t.ms.coin_index, 0, 8, t.stream));
 
-    const bool fuse = fusion_enabled();
-    Fuser fuser(fuse ? n : 0);
-    std::vector<uint64_t> dev;            // device gates of the window being emitted
-    std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
-    std::vector<std::vector<uint64_t>> buckets(2);
-    uint64_t next_key = 2, dev_off = 0, rec_off = 0;
-    std::vector<uint8_t> flags;
-    std::vector<uint32_t> mq;
-
-    // Stage one device window through the pinned ring (async H2D) and launch it.
-    // (No per-gate byte accounting here: the host is on the critical path of this pipeline; the
-    // resident engines report gate bytes.)
-    auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
-        for (uint64_t i = 0; i < cnt;) {
-            if (ring.fill == kRingGates) {
-                QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
-                ring.used[ring.cur] = true;
-                ring.cur ^= 1;
-                ring.fill = 0;
-                if (ring.used[ring.cur]) QSR_CUDA(cudaEventSynchronize(ring.done[ring.cur]));
+    // Keys are 2*round + is_measure with round <= gates on the wire + 1 <= G + 1.
+    BucketDir buckets(2 * G + 4);
+    std::mutex pool_mu;
+    std::vector<std::vector<uint64_t>> pool; // emptied buckets keep their capacity
+    auto fresh_bucket = [&](std::vector<uint64_t> &b) {
+        {
+            std::lock_guard<std::mutex> g(pool_mu);
+            if (!pool.empty()) {
+                b.swap(pool.back());
+                pool.pop_back();
+                return;
             }
-            const uint64_t take = std::min(cnt - i, kRingGates - ring.fill);
-            uint64_t *dst = ring.buf[ring.cur] + ring.fill;
-            std::memcpy(dst, src + i, take * 8);
-            QSR_CUDA(cudaMemcpyAsync(d_gates + dev_off + i, dst, take * 8, cudaMemcpyHostToDevice, t.stream));
-            ring.fill += take;
-            i += take;
         }
-        launch_gate_window(t, d_gates + dev_off, cnt);
-        ++rt.gate_launches;
-        dev_off += cnt;
+        b.reserve(size_t(n) * 3 / 4 + 16);
     };
 
-    // CM rows back to logical order (before a measurement window and at the end).
-    uint32_t *d_perm = nullptr;
-    auto unpermute = [&] {
-        if (fuser.identity_permutation()) return;
-        if (!d_perm) QSR_CUDA(cudaMalloc(&d_perm, uint64_t(n) * 4));
-        QSR_CUDA(cudaMemcpyAsync(d_perm, fuser.permutation().data(), uint64_t(n) * 4, cudaMemcpyHostToDevice,
-                                 t.stream));
-        QSR_CUDA(cudaStreamSynchronize(t.stream)); // the host map is reset right after
-        launch_unpermute_rows(t, d_perm);
-        fuser.reset_permutation();
-    };
+    // ---- emitter: fuse, stage and launch every final window, in key order ------------------
+    std::mutex mu;
+    std::condition_variable cv;
+    uint64_t limit = 2;       // keys below are final (guarded by mu)
+    bool done = false;        // the planner has published its last limit (guarded by mu)
+    bool stop = false;        // planner failed: emitter quits
+    std::exception_ptr emit_error;
+    double t_fuse = 0, t_stage = 0, t_ringwait = 0, t_meas = 0, t_plan = 0;
 
-    // Upload + launch every window with key in [next_key, limit).
-    auto emit = [&](uint64_t limit) {
-        limit = std::min<uint64_t>(limit, buckets.size());
-        bool in_run = false;
-        cudaEvent_t ra = nullptr, rb = nullptr;
-        auto open_run = [&] {
-            if (in_run) return;
-            QSR_CUDA(cudaEventCreate(&ra));
-            QSR_CUDA(cudaEventCreate(&rb));
-            QSR_CUDA(cudaEventRecord(ra, t.stream));
-            in_run = true;
-        };
-        auto close_run = [&] {
-            if (!in_run) return;
-            QSR_CUDA(cudaEventRecord(rb, t.stream));
-            to_events.emplace_back(ra, rb);
-            in_run = false;
-        };
-        for (; next_key < limit; ++next_key) {
-            std::vector<uint64_t> &b = buckets[next_key];
-            if (b.empty()) continue;
-            const uint64_t cnt = b.size();
-            ++counts.windows;
-            if ((next_key & 1) == 0) {
-                counts.unitary += cnt;
-                const uint64_t *src = b.data();
-                uint64_t ng = cnt;
-                if (fuse) {
-                    dev.clear();
-                    fuser.unitary(b.data(), cnt, dev);
-                    src = dev.data();
-                    ng = dev.size();
-                }
-                if (ng) {
-                    open_run();
-                    launch_staged(src, ng);
-                }
-            } else {
-                if (fuse) {
-                    dev.clear();
-                    fuser.flush(dev);
-                    if (!dev.empty()) {
-                        open_run();
-                        launch_staged(dev.data(), dev.size());
+    auto emitter = [&] {
+        try {
+            QSR_CUDA(cudaSetDevice(t.device));
+            const bool fuse = fusion_enabled();
+            Fuser fuser(fuse ? n : 0);
+            std::vector<uint64_t> dev; // device gates of the window being emitted
+            std::vector<uint8_t> flags;
+            std::vector<uint32_t> mq;
+            uint64_t next_key = 2, dev_off = 0, rec_off = 0;
+            uint32_t *d_perm = nullptr;
+            cudaEvent_t ra = nullptr, rb = nullptr;
+            bool in_run = false;
+            auto open_run = [&] {
+                if (in_run) return;
+                QSR_CUDA(cudaEventCreate(&ra));
+                QSR_CUDA(cudaEventCreate(&rb));
+                QSR_CUDA(cudaEventRecord(ra, t.stream));
+                in_run = true;
+            };
+            auto close_run = [&] {
+                if (!in_run) return;
+                QSR_CUDA(cudaEventRecord(rb, t.stream));
+                to_events.emplace_back(ra, rb);
+                in_run = false;
+            };
+            // Stage one device window through the pinned ring (async H2D) and launch it.
+            auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
+                const auto ts = clk::now();
+                open_run();
+                for (uint64_t i = 0; i < cnt;) {
+                    if (ring.fill == kRingGates) {
+                        QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
+                        ring.used[ring.cur] = true;
+                        ring.cur ^= 1;
+                        ring.fill = 0;
+                        if (ring.used[ring.cur]) {
+                            const auto tw = clk::now();
+                            QSR_CUDA(cudaEventSynchronize(ring.done[ring.cur]));
+                            t_ringwait += since(tw);
+                        }
                     }
-                    close_run();
-                    unpermute();
+                    const uint64_t take = std::min(cnt - i, kRingGates - ring.fill);
+                    uint64_t *dst = ring.buf[ring.cur] + ring.fill;
+                    std::memcpy(dst, src + i, take * 8);
+                    QSR_CUDA(cudaMemcpyAsync(d_gates + dev_off + i, dst, take * 8, cudaMemcpyHostToDevice,
+                                             t.stream));
+                    ring.fill += take;
+                    i += take;
                 }
-                close_run();
-                mq.resize(cnt);
-                for (uint64_t i = 0; i < cnt; ++i) mq[i] = packed_q0(b[i]);
-                t.ensure_window_cap(cnt);
-                QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
-                measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
-                QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, cnt * sizeof(qsr_record_entry),
-                                         cudaMemcpyDeviceToDevice, t.stream));
-                rec_off += cnt;
-                counts.measures += cnt;
+                launch_gate_window(t, d_gates + dev_off, cnt);
+                ++rt.gate_launches;
+                dev_off += cnt;
+                t_stage += since(ts);
+            };
+            // CM rows back to logical order (before a measurement window and at the end).
+            auto unpermute = [&] {
+                if (!fuse || fuser.identity_permutation()) return;
+                if (!d_perm) QSR_CUDA(cudaMalloc(&d_perm, uint64_t(n) * 4));
+                const std::vector<uint32_t> pm = fuser.permutation();
+                QSR_CUDA(cudaMemcpyAsync(d_perm, pm.data(), uint64_t(n) * 4, cudaMemcpyHostToDevice, t.stream));
+                QSR_CUDA(cudaStreamSynchronize(t.stream)); // pm is about to go away
+                launch_unpermute_rows(t, d_perm);
+                fuser.reset_permutation();
+            };
+            for (;;) {
+                uint64_t lim;
+                bool last;
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stop || done || limit > next_key; });
+                    if (stop) break;
+                    lim = limit;
+                    last = done;
+                }
+                for (; next_key < lim; ++next_key) {
+                    std::vector<uint64_t> *bp = buckets.find(next_key);
+                    if (!bp || bp->empty()) continue;
+                    std::vector<uint64_t> &b = *bp;
+                    const uint64_t cnt = b.size();
+                    ++counts.windows;
+                    if ((next_key & 1) == 0) {
+                        counts.unitary += cnt;
+                        if (fuse) {
+                            const auto tf = clk::now();
+                            dev.clear();
+                            fuser.unitary(b.data(), cnt, dev);
+                            t_fuse += since(tf);
+                            if (!dev.empty()) launch_staged(dev.data(), dev.size());
+                        } else {
+                            launch_staged(b.data(), cnt);
+                        }
+                    } else {
+                        if (fuse) {
+                            dev.clear();
+                            fuser.flush(dev);
+                            if (!dev.empty()) launch_staged(dev.data(), dev.size());
+                            close_run();
+                            unpermute();
+                        }
+                        close_run();
+                        mq.resize(cnt);
+                        for (uint64_t i = 0; i < cnt; ++i) mq[i] = packed_q0(b[i]);
+                        t.ensure_window_cap(cnt);
+                        const auto tm = clk::now();
+                        QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
+                        measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
+                        t_meas += since(tm);
+                        QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, cnt * sizeof(qsr_record_entry),
+                                                 cudaMemcpyDeviceToDevice, t.stream));
+                        rec_off += cnt;
+                        counts.measures += cnt;
+                    }
+                    b.clear();
+                    {
+                        std::lock_guard<std::mutex> g(pool_mu);
+                        if (pool.size() < 64) pool.push_back(std::move(b));
+                    }
+                    std::vector<uint64_t>().swap(b);
+                }
+                if (last) break; // the planner is done and everything is out
             }
-            std::vector<uint64_t>().swap(b);
+            close_run();
+            if (!stop && fuse) {
+                dev.clear();
+                fuser.flush(dev);
+                if (!dev.empty()) {
+                    launch_staged(dev.data(), dev.size());
+                    close_run();
+                }
+                unpermute();
+                QSR_CUDA(cudaStreamSynchronize(t.stream));
+            }
+            if (d_perm) cudaFree(d_perm);
+        } catch (...) {
+            emit_error = std::current_exception();
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
         }
-        close_run();
     };
 
-    const qsr_gate *gates = c.gates.data();
-    for (uint64_t i0 = 0; i0 < G; i0 += kPlanChunk) {
-        const uint64_t i1 = std::min(G, i0 + kPlanChunk);
-        for (uint64_t i = i0; i < i1; ++i) {
-            const qsr_gate g = gates[i];
-            const uint32_t kind = g.kind;
-            if (kind > QSR_MEASURE) fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
-            const bool two = kind >= QSR_CX && kind <= QSR_ISWAP;
-            const uint32_t q0 = g.q0, q1 = two ? g.q1 : g.q0;
-            if (q0 >= n || q1 >= n) fail(QSR_OUT_OF_RANGE, "gate operand out of range");
-            if (two && q0 == q1) fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
-            const uint32_t w0 = wire[q0], w1 = wire[q1];
-            const uint32_t r0 = w0 >> 1, r1 = w1 >> 1;
-            const uint32_t meas = kind == QSR_MEASURE;
-            const uint32_t r = meas ? (r0 > 1 ? r0 : 1) : 1 + (r0 > r1 ? r0 : r1);
-            if (meas & w0 & 1u) fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
-            wire[q0] = (r << 1) | meas;
-            wire[q1] = (r << 1) | meas;
-            const uint64_t key = 2 * uint64_t(r) + meas;
-            if (key >= buckets.size()) buckets.resize(key + 1);
-            buckets[key].push_back(pack_gate(g));
+    // ---- planner (this thread): the one-pass round closed form, chunk by chunk -------------
+    std::thread emit_thread(emitter);
+    auto publish = [&](uint64_t lim, bool final) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            limit = std::max(limit, lim);
+            done = final;
         }
-        if (i1 == G) break;
-        uint32_t rmin = 0xFFFFFFFFu;
-        for (uint32_t q = 0; q < n; ++q) rmin = std::min(rmin, wire[q] >> 1);
-        emit(2 * uint64_t(rmin) + 1);
-    }
-    emit(~uint64_t(0));
-    if (fuse) {
-        dev.clear();
-        fuser.flush(dev);
-        if (!dev.empty()) {
-            cudaEvent_t ra, rb;
-            QSR_CUDA(cudaEventCreate(&ra));
-            QSR_CUDA(cudaEventCreate(&rb));
-            QSR_CUDA(cudaEventRecord(ra, t.stream));
-            launch_staged(dev.data(), dev.size());
-            QSR_CUDA(cudaEventRecord(rb, t.stream));
-            to_events.emplace_back(ra, rb);
+        cv.notify_one();
+    };
+    uint64_t max_key = 0;
+    auto halt = [&] {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            stop = true;
         }
-        unpermute();
-        QSR_CUDA(cudaStreamSynchronize(t.stream));
+        cv.notify_one();
+        emit_thread.join();
+    };
+    try {
+        std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
+        const qsr_gate *gates = c.gates.data();
+        for (uint64_t i0 = 0; i0 < G; i0 += kPlanChunk) {
+            const uint64_t i1 = std::min(G, i0 + kPlanChunk);
+            const auto tp = clk::now();
+            for (uint64_t i = i0; i < i1; ++i) {
+                const qsr_gate g = gates[i];
+                const uint32_t kind = g.kind;
+                if (kind > QSR_MEASURE) fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
+                const bool two = kind >= QSR_CX && kind <= QSR_ISWAP;
+                const uint32_t q0 = g.q0, q1 = two ? g.q1 : g.q0;
+                if (q0 >= n || q1 >= n) fail(QSR_OUT_OF_RANGE, "gate operand out of range");
+                if (two && q0 == q1) fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
+                const uint32_t w0 = wire[q0], w1 = wire[q1];
+                const uint32_t r0 = w0 >> 1, r1 = w1 >> 1;
+                const uint32_t meas = kind == QSR_MEASURE;
+                const uint32_t r = meas ? (r0 > 1 ? r0 : 1) : 1 + (r0 > r1 ? r0 : r1);
+                if (meas & w0 & 1u) fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
+                wire[q0] = (r << 1) | meas;
+                wire[q1] = (r << 1) | meas;
+                const uint64_t key = 2 * uint64_t(r) + meas;
+                max_key = std::max(max_key, key);
+                std::vector<uint64_t> &bk = buckets[key];
+                if (bk.capacity() == 0) fresh_bucket(bk);
+                bk.push_back(pack_gate(g));
+            }
+            t_plan += since(tp);
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                if (stop) break; // the emitter failed
+            }
+            if (i1 == G) break;
+            uint32_t rmin = 0xFFFFFFFFu;
+            for (uint32_t q = 0; q < n; ++q) rmin = std::min(rmin, wire[q] >> 1);
+            publish(2 * uint64_t(rmin) + 1, false);
+        }
+    } catch (...) {
+        halt();
+        throw;
     }
-    if (d_perm) cudaFree(d_perm);
+    publish(max_key + 1, true);
+    emit_thread.join();
+    if (emit_error) std::rethrow_exception(emit_error);
 
+    if (trace_on()) {
+        trace("  stream: plan (thread 1)", t_plan);
+        trace("  stream: fuse (thread 2)", t_fuse);
+        trace("  stream: stage+launch", t_stage);
+        trace("  stream: (ring waits)", t_ringwait);
+        trace("  stream: measure windows", t_meas);
+    }
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));
     float total = 0;
     QSR_CUDA(cudaEventElapsedTime(&total, e_start, e_end));
     rt.total_ms = total;
-    for (auto &p : to_events) {
+    for (auto &pr : to_events) {
         float ms = 0;
-        QSR_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+        QSR_CUDA(cudaEventElapsedTime(&ms, pr.first, pr.second));
         rt.to_ms += ms;
-        cudaEventDestroy(p.first);
-        cudaEventDestroy(p.second);
+        cudaEventDestroy(pr.first);
+        cudaEventDestroy(pr.second);
     }
     cudaEventDestroy(e_start);
     cudaEventDestroy(e_end);
