@@ -284,8 +284,10 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     try {
         std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
         const qsr_gate *gates = c.gates.data();
-        for (uint64_t i0 = 0; i0 < G; i0 += kPlanChunk) {
-            const uint64_t i1 = std::min(G, i0 + kPlanChunk);
+        // Small chunks first (the device starts after ~a layer), then kPlanChunk.
+        uint64_t chunk = uint64_t(1) << 17;
+        for (uint64_t i0 = 0; i0 < G; i0 += chunk, chunk = std::min(chunk * 2, kPlanChunk)) {
+            const uint64_t i1 = std::min(G, i0 + chunk);
             const auto tp = clk::now();
             for (uint64_t i = i0; i < i1; ++i) {
                 const qsr_gate g = gates[i];
