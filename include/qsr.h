@@ -42,7 +42,8 @@ enum {
     QSR_CUDA_ERROR = 4,
     QSR_OUT_OF_MEMORY = 5,
     QSR_NCCL_ERROR = 6,
-    QSR_INTERNAL = 7
+    QSR_INTERNAL = 7,
+    QSR_PARSE_ERROR = 8       /* quasar::QasmError (qasm.hpp:33-40) */
 };
 
 /* GateKind, same numbering as circuit.hpp:29-42. */
@@ -115,6 +116,25 @@ qsr_status qsr_circuit_info(const qsr_circuit *c, uint32_t *num_qubits, uint64_t
                             uint64_t *nmeasure);
 const qsr_gate *qsr_circuit_gates(const qsr_circuit *c);
 void qsr_circuit_destroy(qsr_circuit *c);
+/* Circuit::num_clbits (circuit.hpp:103-105): classical bits named in the source, labels only.
+ * generate_random sets n (circuit.hpp:171), qsr_parse_qasm the last creg size, else 0. */
+qsr_status qsr_circuit_clbits(const qsr_circuit *c, uint32_t *num_clbits);
+qsr_status qsr_circuit_set_clbits(qsr_circuit *c, uint32_t num_clbits);
+
+/* Host worker threads of the parallel host passes (schedule scatter, QASM parse / emit,
+ * fusion); 0 = hardware default. Stands for set_num_threads (parallel.hpp:151). */
+void qsr_set_num_threads(unsigned threads);
+unsigned qsr_get_num_threads(void);
+
+/* ---- OpenQASM 2.0 subset (qasm.hpp:29-271) -------------------------------------- */
+/* parse_qasm (qasm.hpp:159-252): same grammar, same Circuit, same errors. On a syntax error
+ * returns QSR_PARSE_ERROR, qsr_last_error() = QasmError::what() ("qasm:L:C: reason") and
+ * *err = {line, column}. Large bodies are parsed on all host threads. */
+typedef struct qsr_qasm_error { int line; int column; } qsr_qasm_error;
+qsr_status qsr_parse_qasm(const char *text, uint64_t len, qsr_circuit **out, qsr_qasm_error *err);
+/* emit_qasm (qasm.hpp:254-271). Text outputs: buf == NULL -> *len = size in bytes; else
+ * cap >= size is required and exactly *len bytes are written (no NUL terminator). */
+qsr_status qsr_emit_qasm(const qsr_circuit *c, char *buf, uint64_t cap, uint64_t *len);
 
 /* ---- schedules (schedule.hpp:32-137) ------------------------------------------- */
 typedef struct qsr_schedule qsr_schedule;
@@ -130,6 +150,11 @@ const qsr_gate *qsr_schedule_gates(const qsr_schedule *s);
 const uint64_t *qsr_schedule_offsets(const qsr_schedule *s);      /* nwindows + 1 */
 const uint8_t *qsr_schedule_is_measurement(const qsr_schedule *s); /* nwindows */
 void qsr_schedule_destroy(qsr_schedule *s);
+/* schedule_to_text (schedule.hpp:235-249); text-output convention of qsr_emit_qasm. */
+qsr_status qsr_schedule_text(const qsr_schedule *s, char *buf, uint64_t cap, uint64_t *len);
+/* validate_schedule (schedule.hpp:143-233): "valid" or the reference's first violation. */
+qsr_status qsr_validate_schedule(const qsr_circuit *c, const qsr_schedule *s, char *buf,
+                                 uint64_t cap, uint64_t *len);
 
 /* ---- device tableau (tableau.hpp:62-131) --------------------------------------- */
 typedef struct qsr_tableau qsr_tableau;
@@ -147,6 +172,10 @@ qsr_status qsr_tableau_clone(const qsr_tableau *t, qsr_tableau **out);
 void qsr_tableau_destroy(qsr_tableau *t);
 
 /* Tableau::transpose_in_place (tableau.hpp:166-176). */
+/* Tableau::check_group_validity (tableau.hpp:184-213) on the device: "valid" or the reference's
+ * first violation, text-output convention of qsr_emit_qasm. O(n^2 k) word operations as a tiled
+ * GF(2) Gram product (seconds at c2, tens of seconds at c5). Whole tableaux only. */
+qsr_status qsr_tableau_check_validity(qsr_tableau *t, char *buf, uint64_t cap, uint64_t *len);
 qsr_status qsr_transpose_in_place(qsr_tableau *t);
 
 /* apply_window(tableau, window) (gates.hpp:147-197). */
@@ -234,6 +263,17 @@ qsr_status qsr_sample_shard(const qsr_circuit *c, uint64_t shots, uint64_t seed,
                             int rank, int device, qsr_frames **out, qsr_run_report *report);
 /* Global shot-word slice [j0, j0+nw) held by a frames object (j0 = 0, nw = kf unsharded). */
 qsr_status qsr_frames_shot_words(const qsr_frames *f, uint64_t *j0, uint64_t *nw);
+/* init_frames<W> / sample<W> for the reference's other word types, W = word_bits in
+ * {8, 16, 32, 64} (frames.hpp:46-72, 163-204): the Z frames are drawn exactly as the reference
+ * draws them for W (one Philox word per W-bit word, low W bits kept), so every shot matches
+ * sample<W>. Device and host records keep the 64-bit word layout: shot s is bit s%64 of word
+ * s/64 in either case, and the little-endian bytes of a row's first ceil(shots/W)*W/8 bytes are
+ * exactly the reference's ShotRecord<W> row. */
+qsr_status qsr_init_frames_word(uint64_t n, uint64_t shots, uint64_t seed, unsigned word_bits,
+                                int device, qsr_frames **out);
+qsr_status qsr_sample_word(const qsr_circuit *c, uint64_t shots, uint64_t seed, unsigned word_bits,
+                           int device, qsr_frames **out, qsr_run_report *report);
+qsr_status qsr_frames_word_bits(const qsr_frames *f, unsigned *word_bits);
 
 /* ---- generator-row-sharded engine (multi-GPU run_single_shot) ------
  * The tableau is split by generator-words: shard r of `world` holds generator-words

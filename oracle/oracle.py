@@ -35,6 +35,12 @@ class OracleError(RuntimeError):
         self.status = status
 
 
+class QasmFailure(Exception):
+    def __init__(self, msg, line, column):
+        super().__init__(msg)
+        self.msg, self.line, self.column = msg, line, column
+
+
 STATUS_NAMES = {1: "invalid_argument", 2: "out_of_range", 3: "logic_error", 7: "other"}
 
 
@@ -224,6 +230,69 @@ class Oracle:
         self._chk(self.lib.orc_sample(C.c_uint64(n), _p(gates), C.c_uint64(len(gates)), C.c_uint64(shots),
                                       C.c_uint64(seed), _p(measured), C.byref(nr), _p(words), C.byref(rep)))
         return measured[:nr.value].copy(), words[:nr.value * kf].copy(), rep
+
+    # -- reference-only: formats either side of the path (oracle/_ref only)
+    def _need_ref(self):
+        if self.kind != "reference":
+            raise NotImplementedError("reference-only oracle entry point")
+
+    def _text(self, fn, *args) -> str:
+        n = C.c_uint64()
+        self._chk(fn(*args, None, C.c_uint64(0), C.byref(n)))
+        buf = C.create_string_buffer(max(n.value, 1))
+        self._chk(fn(*args, buf, C.c_uint64(n.value), C.byref(n)))
+        return buf.raw[:n.value].decode()
+
+    def parse_qasm(self, text: str):
+        """-> (num_qubits, num_clbits, gates) or raises QasmFailure(msg, line, col)."""
+        self._need_ref()
+        data = text.encode()
+        n, ncl, cnt, line, col = C.c_uint32(), C.c_uint32(), C.c_uint64(), C.c_int(), C.c_int()
+        f = self.lib.orc_ref_parse_qasm
+        f.argtypes = [C.c_char_p, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p,
+                      C.c_void_p, C.c_void_p]
+        args = (data, len(data), C.byref(n), C.byref(ncl))
+        st = f(*args, None, 0, C.byref(cnt), C.byref(line), C.byref(col))
+        if st == 8:
+            raise QasmFailure((self.lib.orc_last_error() or b"").decode(), line.value, col.value)
+        self._chk(st)
+        out = np.zeros(cnt.value, dtype=GATE_DTYPE)
+        self._chk(f(*args, _p(out), cnt.value, C.byref(cnt), C.byref(line), C.byref(col)))
+        return n.value, ncl.value, out
+
+    def emit_qasm(self, n, gates) -> str:
+        self._need_ref()
+        return self._text(self.lib.orc_ref_emit_qasm, C.c_uint32(n), _p(gates), C.c_uint64(len(gates)))
+
+    def schedule_text(self, n, gates, mode=0) -> str:
+        self._need_ref()
+        return self._text(self.lib.orc_ref_schedule_text, C.c_uint32(n), _p(gates), C.c_uint64(len(gates)),
+                          C.c_int(mode))
+
+    def validate_schedule(self, n, gates, sgates, offsets, is_meas) -> str:
+        self._need_ref()
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        fl = np.ascontiguousarray(is_meas, dtype=np.uint8)
+        return self._text(self.lib.orc_ref_validate_schedule, C.c_uint32(n), _p(gates), C.c_uint64(len(gates)),
+                          _p(sgates), _p(off), _p(fl), C.c_uint64(len(fl)))
+
+    def sample_w(self, n, gates, shots, seed, wbits):
+        """sample<W>: (measured, kf, row bytes [nrows, kf*W/8]) for W in {8, 16, 32, 64}."""
+        self._need_ref()
+        kf64 = (shots + 63) // 64
+        measured = np.zeros(max(n, 1), dtype=np.uint32)
+        data = np.zeros(max(n, 1) * kf64 * 8 + 8, dtype=np.uint8)
+        nr, kf = C.c_uint64(), C.c_uint64()
+        self._chk(self.lib.orc_ref_sample_w(C.c_uint64(n), _p(gates), C.c_uint64(len(gates)), C.c_uint64(shots),
+                                            C.c_uint64(seed), C.c_uint(wbits), _p(measured), C.byref(nr),
+                                            C.byref(kf), _p(data)))
+        rb = kf.value * wbits // 8
+        return measured[:nr.value].copy(), kf.value, data[:nr.value * rb].reshape(nr.value, rb).copy()
+
+    def check_validity(self, n, layout, x, z) -> str:
+        self._need_ref()
+        return self._text(self.lib.orc_ref_check_validity, C.c_uint64(n), C.c_int(layout), _p(x), _p(z))
+
 
 
 def best_available() -> Optional[Oracle]:

@@ -86,6 +86,22 @@ int orc_measure_sample(uint64_t n, uint64_t shots, uint64_t *xf, uint64_t *zf, c
 int orc_sample(uint64_t n, const orc_gate *g, uint64_t ng, uint64_t shots, uint64_t seed,
                uint32_t *measured, uint64_t *nrows, uint64_t *words, orc_report *rep);
 
+/* ---- reference-only (oracle/_ref/libquasar_ref.so; the C port has no counterpart) ---- */
+/* parse_qasm: 0, or 8 = QasmError (orc_last_error() = what(), *line / *col set). */
+int orc_ref_parse_qasm(const char *text, uint64_t len, uint32_t *n, uint32_t *nclbits, orc_gate *out,
+                       uint64_t cap, uint64_t *count, int *line, int *col);
+/* Text results: *len = full size, min(cap, size) bytes copied to buf (may be NULL). */
+int orc_ref_emit_qasm(uint32_t n, const orc_gate *g, uint64_t ng, char *buf, uint64_t cap, uint64_t *len);
+int orc_ref_schedule_text(uint32_t n, const orc_gate *g, uint64_t ng, int mode, char *buf, uint64_t cap,
+                          uint64_t *len);
+int orc_ref_validate_schedule(uint32_t n, const orc_gate *g, uint64_t ng, const orc_gate *sg,
+                              const uint64_t *off, const uint8_t *is_meas, uint64_t nwin, char *buf,
+                              uint64_t cap, uint64_t *len);
+int orc_ref_sample_w(uint64_t n, const orc_gate *g, uint64_t ng, uint64_t shots, uint64_t seed,
+                     unsigned wbits, uint32_t *measured, uint64_t *nrows, uint64_t *kf, uint8_t *bytes);
+int orc_ref_check_validity(uint64_t n, int layout, const uint64_t *x, const uint64_t *z, char *buf,
+                           uint64_t cap, uint64_t *len);
+
 #ifdef __cplusplus
 }
 #endif

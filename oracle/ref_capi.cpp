@@ -4,6 +4,7 @@
 // copied) into oracle/_ref/libquasar_ref.so so that tests and bench.py's reference arm can
 // call the reference's own run_single_shot / measure_window / sample on the same inputs as
 // the CUDA engine. Build recipe: oracle/Makefile (target `ref`).
+#include <algorithm>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -11,6 +12,7 @@
 #include "orc.h"
 #include "quasar/frames.hpp"
 #include "quasar/measure.hpp"
+#include "quasar/qasm.hpp"
 #include "quasar/simulator.hpp"
 
 using namespace quasar;
@@ -343,6 +345,88 @@ int orc_sample(uint64_t n, const orc_gate *g, uint64_t ng, uint64_t shots, uint6
         if (words) std::memcpy(words, rec.words.data(), rec.words.size() * 8);
         report_of(r, rep);
     });
+}
+
+// ---- reference-only entry points (formats either side of the path; no C restatement) ----
+
+static int text_result(const std::string &t, char *buf, uint64_t cap, uint64_t *len) {
+    *len = t.size();
+    if (buf) std::memcpy(buf, t.data(), std::min<uint64_t>(cap, t.size()));
+    return 0;
+}
+
+int orc_ref_parse_qasm(const char *text, uint64_t len, uint32_t *n, uint32_t *nclbits, orc_gate *out,
+                       uint64_t cap, uint64_t *count, int *line, int *col) {
+    *line = *col = 0;
+    try {
+        Circuit c = parse_qasm(std::string_view(text, len));
+        *n = c.num_qubits;
+        *nclbits = c.num_clbits;
+        *count = c.gates.size();
+        if (out) std::memcpy(out, c.gates.data(), std::min<uint64_t>(cap, c.gates.size()) * sizeof(Gate));
+        return 0;
+    } catch (const QasmError &e) {
+        g_err = e.what();
+        *line = e.line;
+        *col = e.column;
+        return 8;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return 7;
+    }
+}
+
+int orc_ref_emit_qasm(uint32_t n, const orc_gate *g, uint64_t ng, char *buf, uint64_t cap, uint64_t *len) {
+    return guard([&] { text_result(emit_qasm(circuit_of(n, g, ng)), buf, cap, len); });
+}
+
+int orc_ref_schedule_text(uint32_t n, const orc_gate *g, uint64_t ng, int mode, char *buf, uint64_t cap,
+                          uint64_t *len) {
+    return guard([&] {
+        Circuit c = circuit_of(n, g, ng);
+        Schedule s = schedule_windows(c, mode ? ScheduleMode::sampling : ScheduleMode::single_shot);
+        text_result(schedule_to_text(s), buf, cap, len);
+    });
+}
+
+int orc_ref_validate_schedule(uint32_t n, const orc_gate *g, uint64_t ng, const orc_gate *sg,
+                              const uint64_t *off, const uint8_t *is_meas, uint64_t nwin, char *buf,
+                              uint64_t cap, uint64_t *len) {
+    return guard([&] {
+        text_result(validate_schedule(circuit_of(n, g, ng), schedule_of(sg, off, is_meas, nwin)), buf, cap,
+                    len);
+    });
+}
+
+// sample<W> for W in {8, 16, 32, 64}: rows of kf W-words, written as little-endian bytes.
+int orc_ref_sample_w(uint64_t n, const orc_gate *g, uint64_t ng, uint64_t shots, uint64_t seed,
+                     unsigned wbits, uint32_t *measured, uint64_t *nrows, uint64_t *kf, uint8_t *bytes) {
+    return guard([&] {
+        Circuit c = circuit_of(n, g, ng);
+        auto run = [&](auto w) {
+            using W = decltype(w);
+            auto rec = sample<W>(c, shots, seed);
+            *nrows = rec.measured.size();
+            *kf = rec.kf;
+            if (measured) std::memcpy(measured, rec.measured.data(), rec.measured.size() * 4);
+            if (bytes)
+                for (size_t i = 0; i < rec.words.size(); ++i)
+                    for (size_t b = 0; b < sizeof(W); ++b)
+                        bytes[i * sizeof(W) + b] = uint8_t((uint64_t(rec.words[i]) >> (8 * b)) & 0xFF);
+        };
+        switch (wbits) {
+        case 8: run(uint8_t{}); break;
+        case 16: run(uint16_t{}); break;
+        case 32: run(uint32_t{}); break;
+        case 64: run(uint64_t{}); break;
+        default: throw std::invalid_argument("word size must be one of 8, 16, 32, 64");
+        }
+    });
+}
+
+int orc_ref_check_validity(uint64_t n, int layout, const uint64_t *x, const uint64_t *z, char *buf,
+                           uint64_t cap, uint64_t *len) {
+    return guard([&] { text_result(load(n, layout, x, z, nullptr).check_group_validity(), buf, cap, len); });
 }
 
 } // extern "C"

@@ -11,7 +11,7 @@ import numpy as np
 LIB_PATH = Path(os.environ.get("QSR_LIB", Path(__file__).resolve().parent / "libqsr.so"))
 
 # Status codes (qsr.h)
-OK, INVALID_ARGUMENT, OUT_OF_RANGE, LOGIC_ERROR, CUDA_ERROR, OUT_OF_MEMORY, NCCL_ERROR, INTERNAL = range(8)
+OK, INVALID_ARGUMENT, OUT_OF_RANGE, LOGIC_ERROR, CUDA_ERROR, OUT_OF_MEMORY, NCCL_ERROR, INTERNAL, PARSE_ERROR = range(9)
 
 
 class QuasarError(RuntimeError):
@@ -41,7 +41,20 @@ class OutOfMemory(QuasarError, MemoryError):
     status = OUT_OF_MEMORY
 
 
-_ERRORS = {INVALID_ARGUMENT: InvalidArgument, OUT_OF_RANGE: OutOfRange, LOGIC_ERROR: LogicError,
+class QasmError(QuasarError):
+    """quasar::QasmError (qasm.hpp:33-40): what() = "qasm:L:C: reason", plus .line / .column."""
+    status = PARSE_ERROR
+
+    def __init__(self, msg: str, line: int = 0, column: int = 0):
+        super().__init__(msg)
+        self.line, self.column = line, column
+
+
+class QasmError_t(C.Structure):
+    _fields_ = [("line", C.c_int), ("column", C.c_int)]
+
+
+_ERRORS = {PARSE_ERROR: QasmError, INVALID_ARGUMENT: InvalidArgument, OUT_OF_RANGE: OutOfRange, LOGIC_ERROR: LogicError,
            CUDA_ERROR: CudaError, OUT_OF_MEMORY: OutOfMemory}
 
 
@@ -98,6 +111,14 @@ SIGNATURES = {
     "qsr_circuit_info": (i32, [P, pu32, pu64, pu64]),
     "qsr_circuit_gates": (P, [P]),
     "qsr_circuit_destroy": (None, [P]),
+    "qsr_circuit_clbits": (i32, [P, pu32]),
+    "qsr_circuit_set_clbits": (i32, [P, u32]),
+    "qsr_set_num_threads": (None, [C.c_uint]),
+    "qsr_get_num_threads": (C.c_uint, []),
+    "qsr_parse_qasm": (i32, [C.c_char_p, u64, C.POINTER(P), C.POINTER(QasmError_t)]),
+    "qsr_emit_qasm": (i32, [P, P, u64, pu64]),
+    "qsr_schedule_text": (i32, [P, P, u64, pu64]),
+    "qsr_validate_schedule": (i32, [P, P, P, u64, pu64]),
     "qsr_schedule_windows": (i32, [P, i32, C.POINTER(P)]),
     "qsr_schedule_create": (i32, [P, pu64, pu8, u64, i32, C.POINTER(P)]),
     "qsr_schedule_info": (i32, [P, pu64, pu64, pi32]),
@@ -113,6 +134,7 @@ SIGNATURES = {
     "qsr_tableau_clone": (i32, [P, C.POINTER(P)]),
     "qsr_tableau_destroy": (None, [P]),
     "qsr_transpose_in_place": (i32, [P]),
+    "qsr_tableau_check_validity": (i32, [P, P, u64, pu64]),
     "qsr_apply_window": (i32, [P, P, u64]),
     "qsr_find_probabilistic": (i32, [P, P, u64, pi64]),
     "qsr_find_and_compact_pivots": (i32, [P, u64, pi64, pu64]),
@@ -142,6 +164,9 @@ SIGNATURES = {
     "qsr_sample": (i32, [P, u64, u64, i32, C.POINTER(P), C.POINTER(Report_t)]),
     "qsr_sample_shard": (i32, [P, u64, u64, i32, i32, i32, C.POINTER(P), C.POINTER(Report_t)]),
     "qsr_frames_shot_words": (i32, [P, pu64, pu64]),
+    "qsr_init_frames_word": (i32, [u64, u64, u64, C.c_uint, i32, C.POINTER(P)]),
+    "qsr_sample_word": (i32, [P, u64, u64, C.c_uint, i32, C.POINTER(P), C.POINTER(Report_t)]),
+    "qsr_frames_word_bits": (i32, [P, C.POINTER(C.c_uint)]),
     "qsr_shard_range": (i32, [u64, i32, i32, pu64, pu64]),
     "qsr_nccl_unique_id": (i32, [pu8]),
     "qsr_sharded_create": (i32, [P, P, C.POINTER(ShardConfig_t), C.POINTER(P)]),
@@ -173,6 +198,15 @@ def check(status: int) -> None:
     if status != OK:
         msg = (lib.qsr_last_error() or b"").decode(errors="replace")
         raise _ERRORS.get(status, QuasarError)(msg)
+
+
+def text(fn, *args) -> bytes:
+    """Two-call text output convention of qsr.h (size query, then fill)."""
+    n = u64()
+    check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(max(n.value, 1))
+    check(fn(*args, buf, n.value, C.byref(n)))
+    return buf.raw[:n.value]
 
 
 def ptr(a: np.ndarray, ctype=None):

@@ -14,11 +14,13 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_obj"
 LIB = PKG / "libqsr.so"
+CLI_SRC = PKG / "cli" / "quasar_cli.cpp"
+CLI = PKG / "bin" / "quasar"   # the reference CLI (tools/quasar.cpp) on this engine
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", str(PKG.parent / "include")]
 SOURCES = ["host_circuit.cpp", "capi.cpp", "engine.cpp", "k_gates.cu", "k_transpose.cu", "k_measure.cu", "k_batch.cu",
-           "k_frames.cu", "exchange.cu", "shard.cpp", "stream.cpp", "fuse.cpp"]
+           "k_frames.cu", "exchange.cu", "shard.cpp", "stream.cpp", "fuse.cpp", "qasm.cpp", "k_validity.cu"]
 HEADERS = ["host.hpp", "device.hpp", "common.cuh", "abi.hpp", "engine.hpp", "exchange.hpp", "fuse.hpp"]
 
 
@@ -48,6 +50,13 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         subprocess.run(cmd, check=True)
     if force or not LIB.exists() or LIB.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    CLI.parent.mkdir(exist_ok=True)
+    if force or not CLI.exists() or CLI.stat().st_mtime < max(LIB.stat().st_mtime, CLI_SRC.stat().st_mtime):
+        cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-I", str(PKG.parent / "include"), str(CLI_SRC), "-o", str(CLI),
+               "-L", str(PKG), "-lqsr", "-Wl,-rpath,$ORIGIN/..", "-pthread"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

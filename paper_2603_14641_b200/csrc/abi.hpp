@@ -10,6 +10,7 @@
 namespace qsr {
 
 extern thread_local std::string g_err;
+extern thread_local int g_qasm_line, g_qasm_column; // position of the last QSR_PARSE_ERROR
 
 template <typename F>
 qsr_status guard(F &&f) {
@@ -19,6 +20,11 @@ qsr_status guard(F &&f) {
     } catch (const Error &e) {
         g_err = e.what();
         return e.status;
+    } catch (const QasmFailure &e) {
+        g_err = e.what();
+        g_qasm_line = e.line;
+        g_qasm_column = e.column;
+        return QSR_PARSE_ERROR;
     } catch (const std::bad_alloc &) {
         g_err = "host allocation failed";
         return QSR_OUT_OF_MEMORY;

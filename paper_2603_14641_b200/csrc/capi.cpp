@@ -19,6 +19,7 @@ namespace qsr {
 
 uint64_t g_launches = 0;
 thread_local std::string g_err;
+thread_local int g_qasm_line = 0, g_qasm_column = 0;
 
 void cuda_check(cudaError_t e, const char *what) {
     if (e == cudaSuccess) return;
@@ -297,6 +298,76 @@ qsr_status qsr_circuit_info(const qsr_circuit *c, uint32_t *nq, uint64_t *ng, ui
 const qsr_gate *qsr_circuit_gates(const qsr_circuit *c) { return c ? c->gates.data() : nullptr; }
 void qsr_circuit_destroy(qsr_circuit *c) { delete c; }
 
+qsr_status qsr_circuit_clbits(const qsr_circuit *c, uint32_t *num_clbits) {
+    return guard([&] {
+        REQUIRE_PTR(c); REQUIRE_PTR(num_clbits);
+        *num_clbits = c->num_clbits;
+    });
+}
+qsr_status qsr_circuit_set_clbits(qsr_circuit *c, uint32_t num_clbits) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        c->num_clbits = num_clbits;
+    });
+}
+
+void qsr_set_num_threads(unsigned threads) { set_host_threads(threads); }
+unsigned qsr_get_num_threads(void) { return host_threads(); }
+
+// ---- OpenQASM / schedule text -----------------------------------------------------
+extern "C++" {
+namespace {
+// Size query (buf == NULL) or fill; *len = bytes (no terminator is written).
+template <typename F>
+void text_out(F &&emit, char *buf, uint64_t cap, uint64_t *len) {
+    REQUIRE_PTR(len);
+    const uint64_t need = emit(nullptr);
+    *len = need;
+    if (!buf) return;
+    if (cap < need) fail(QSR_INVALID_ARGUMENT, "output buffer too small (" + std::to_string(need) + " bytes needed)");
+    emit(buf);
+}
+} // namespace
+}
+
+qsr_status qsr_parse_qasm(const char *text, uint64_t len, qsr_circuit **out, qsr_qasm_error *err) {
+    const qsr_status st = guard([&] {
+        REQUIRE_PTR(out);
+        if (len) REQUIRE_PTR(text);
+        auto c = std::make_unique<qsr_circuit>();
+        static_cast<Circuit &>(*c) = parse_qasm(text ? text : "", len);
+        *out = c.release();
+    });
+    if (err) *err = st == QSR_PARSE_ERROR ? qsr_qasm_error{g_qasm_line, g_qasm_column} : qsr_qasm_error{0, 0};
+    return st;
+}
+
+qsr_status qsr_emit_qasm(const qsr_circuit *c, char *buf, uint64_t cap, uint64_t *len) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        text_out([&](char *o) { return emit_qasm(*c, o); }, buf, cap, len);
+    });
+}
+
+qsr_status qsr_schedule_text(const qsr_schedule *s, char *buf, uint64_t cap, uint64_t *len) {
+    return guard([&] {
+        REQUIRE_PTR(s);
+        text_out([&](char *o) { return schedule_text(*s, o); }, buf, cap, len);
+    });
+}
+
+qsr_status qsr_validate_schedule(const qsr_circuit *c, const qsr_schedule *s, char *buf, uint64_t cap,
+                                 uint64_t *len) {
+    return guard([&] {
+        REQUIRE_PTR(c); REQUIRE_PTR(s);
+        const std::string v = validate_schedule(*c, *s);
+        text_out([&](char *o) {
+            if (o) std::memcpy(o, v.data(), v.size());
+            return uint64_t(v.size());
+        }, buf, cap, len);
+    });
+}
+
 // ---- schedules --------------------------------------------------------------------
 qsr_status qsr_schedule_windows(const qsr_circuit *c, int mode, qsr_schedule **out) {
     return guard([&] {
@@ -431,6 +502,19 @@ qsr_status qsr_tableau_clone(const qsr_tableau *h, qsr_tableau **out) {
 }
 
 void qsr_tableau_destroy(qsr_tableau *h) { delete h; }
+
+qsr_status qsr_tableau_check_validity(qsr_tableau *h, char *buf, uint64_t cap, uint64_t *len) {
+    return guard([&] {
+        REQUIRE_PTR(h);
+        DeviceTableau &t = *h->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        const std::string v = check_group_validity(t);
+        text_out([&](char *o) {
+            if (o) std::memcpy(o, v.data(), v.size());
+            return uint64_t(v.size());
+        }, buf, cap, len);
+    });
+}
 
 qsr_status qsr_transpose_in_place(qsr_tableau *h) {
     return guard([&] {
@@ -783,6 +867,7 @@ struct qsr_frames {
     int num_sms = 148;
     uint64_t n = 0, shots = 0, kf = 0, pitch = 0; // kf: shot-words held here
     uint64_t j0 = 0;                                // global index of the first one
+    uint32_t wbits = 64; // reference word type whose Philox draws the Z frames follow
     uint64_t *xf = nullptr, *zf = nullptr;
     uint64_t *rec = nullptr;  // record rows [cap][pitch]
     uint64_t rec_cap = 0;
@@ -826,8 +911,14 @@ struct qsr_frames {
 
 namespace {
 
+void check_word_bits(unsigned wbits) {
+    if (wbits != 8 && wbits != 16 && wbits != 32 && wbits != 64)
+        fail(QSR_INVALID_ARGUMENT, "word size must be one of 8, 16, 32, 64");
+}
+
 std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
-                                        uint64_t j0 = 0, uint64_t nw = 0) {
+                                        uint64_t j0 = 0, uint64_t nw = 0, unsigned wbits = 64) {
+    check_word_bits(wbits);
     if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "init_frames: n exceeds the supported maximum");
     auto f = std::make_unique<qsr_frames>();
@@ -847,7 +938,8 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     QSR_CUDA(cudaMemsetAsync(f->xf, 0, words * 8, f->stream));
     QSR_CUDA(cudaMemsetAsync(f->zf, 0, words * 8, f->stream));
     f->row_of.assign(n, -1);
-    if (n) launch_frames_init(f->zf, n, f->kf, f->j0, f->pitch, shots, seed, 0, f->stream);
+    f->wbits = wbits;
+    if (n) launch_frames_init(f->zf, n, f->kf, f->j0, f->pitch, shots, seed, 0, wbits, f->stream);
     return f;
 }
 
@@ -871,7 +963,7 @@ void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t 
     f.ensure_idx(ng);
     QSR_CUDA(cudaMemcpyAsync(f.d_idx, idx.data(), 2 * ng * 4, cudaMemcpyHostToDevice, f.stream));
     launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.j0, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
-                          seed, epoch, f.stream);
+                          seed, epoch, f.wbits, f.stream);
     QSR_CUDA(cudaStreamSynchronize(f.stream)); // idx staging reused next call
 }
 
@@ -894,9 +986,14 @@ void validate_frames_window(const qsr_frames &f, const qsr_gate *gates, uint64_t
 } // namespace
 
 qsr_status qsr_init_frames(uint64_t n, uint64_t shots, uint64_t seed, int device, qsr_frames **out) {
+    return qsr_init_frames_word(n, shots, seed, 64, device, out);
+}
+
+qsr_status qsr_init_frames_word(uint64_t n, uint64_t shots, uint64_t seed, unsigned word_bits, int device,
+                                qsr_frames **out) {
     return guard([&] {
         REQUIRE_PTR(out);
-        auto f = make_frames(n, shots, seed, device);
+        auto f = make_frames(n, shots, seed, device, 0, 0, word_bits);
         QSR_CUDA(cudaStreamSynchronize(f->stream));
         *out = f.release();
     });
@@ -994,8 +1091,9 @@ qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *mea
 void qsr_frames_destroy(qsr_frames *f) { delete f; }
 
 static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device, int world,
-                       int rank, qsr_frames **out, qsr_run_report *report) {
+                       int rank, qsr_frames **out, qsr_run_report *report, unsigned wbits = 64) {
     return guard([&] {
+        check_word_bits(wbits);
         auto wall0 = std::chrono::steady_clock::now();
         REQUIRE_PTR(c); REQUIRE_PTR(out);
         if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
@@ -1036,7 +1134,7 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         // Frames over the same device-resident schedule (frames.hpp:171-181).
         auto f = [&] {
             TraceScope tr("  make_frames");
-            auto ff = make_frames(c->num_qubits, shots, seed, device, w0, nw);
+            auto ff = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
             QSR_CUDA(cudaStreamSynchronize(ff->stream));
             return ff;
         }();
@@ -1089,6 +1187,18 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
 qsr_status qsr_sample(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device,
                       qsr_frames **out, qsr_run_report *report) {
     return sample_impl(c, shots, seed, device, 1, 0, out, report);
+}
+
+qsr_status qsr_sample_word(const qsr_circuit *c, uint64_t shots, uint64_t seed, unsigned word_bits,
+                           int device, qsr_frames **out, qsr_run_report *report) {
+    return sample_impl(c, shots, seed, device, 1, 0, out, report, word_bits);
+}
+
+qsr_status qsr_frames_word_bits(const qsr_frames *f, unsigned *word_bits) {
+    return guard([&] {
+        REQUIRE_PTR(f); REQUIRE_PTR(word_bits);
+        *word_bits = f->wbits;
+    });
 }
 
 qsr_status qsr_sample_shard(const qsr_circuit *c, uint64_t shots, uint64_t seed, int world, int rank,

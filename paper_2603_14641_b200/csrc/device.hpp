@@ -132,6 +132,8 @@ void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint6
 // CM <-> internal RM transposes (swap t.x/t.x2 etc).
 void transpose_to_rm(DeviceTableau &t);
 void transpose_to_cm(DeviceTableau &t);
+// Tableau::check_group_validity (tableau.hpp:184-213): "valid" or the reference's first violation.
+std::string check_group_validity(DeviceTableau &t);
 void launch_zero_state(DeviceTableau &t, const uint8_t *d_init /* nullable */);
 
 // Measurement window on a CM tableau (fused recipe, measure.hpp:381-442 semantics).
@@ -182,11 +184,12 @@ int read_error_flag(DeviceTableau &t); // syncs; returns and clears
 // Frames kernels. A frames object may hold a slice of the shot-words: kf words starting at
 // global word j0 (sampling sharded by shot); `shots` is the global count.
 void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t j0, uint64_t pitch,
-                        uint64_t shots, uint64_t seed, uint32_t epoch, cudaStream_t st);
+                        uint64_t shots, uint64_t seed, uint32_t epoch, uint32_t wbits, cudaStream_t st);
+// wbits = the reference word type's width (8/16/32/64): Z frames are drawn as sample<W> draws them.
 void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf, uint64_t j0,
                            uint64_t shots, uint64_t *rec, const uint32_t *qubits,
                            const uint32_t *rows, uint64_t m, uint64_t seed, uint32_t epoch,
-                           cudaStream_t st);
+                           uint32_t wbits, cudaStream_t st);
 void launch_record_fold(uint64_t *rec, uint64_t pitch, uint64_t kf, uint64_t j0, uint64_t shots,
                         const uint32_t *flip_rows, uint64_t nflip, cudaStream_t st);
 

@@ -191,7 +191,7 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
 void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
                           const std::vector<uint8_t> &is_meas) {
     const uint64_t W = is_meas.size();
-    const unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const unsigned nt = std::max(1u, std::min(16u, host_threads()));
     std::vector<std::thread> th;
     for (unsigned t = 0; t < nt; ++t)
         th.emplace_back([&, t] {

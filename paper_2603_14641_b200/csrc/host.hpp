@@ -58,6 +58,21 @@ inline uint32_t packed_kind(uint64_t w) { return uint32_t(w >> 24) & 0xF; }
 inline uint32_t packed_q1(uint64_t w) { return uint32_t(w >> 38) & 0xFFFFFFu; }
 constexpr uint64_t kMaxQubits = (uint64_t(1) << 24) - 1; // 16.7 M qubits (a 2.2 PB tableau)
 
+// Host worker threads for the parallel host passes (scheduler scatter, QASM parse / emit):
+// qsr_set_num_threads(t) (t = 0 restores the hardware default), like the reference's
+// set_num_threads (parallel.hpp).
+unsigned host_threads();
+void set_host_threads(unsigned t);
+// f(t, begin, end) over T contiguous chunks of [0, n) on T threads (the caller runs chunk 0).
+template <typename F>
+void parallel_chunks(uint64_t n, unsigned T, F &&f) {
+    if (T <= 1 || n < 2) { f(0u, uint64_t(0), n); return; }
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) th.emplace_back([&, t] { f(t, n * t / T, n * (t + 1) / T); });
+    f(0u, uint64_t(0), n / T);
+    for (auto &x : th) x.join();
+}
+
 // Philox-4x32-10 (reference rng.hpp:28-55), host side.
 void philox_block(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
 uint64_t philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t index);
@@ -65,6 +80,7 @@ uint64_t philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t inde
 struct Circuit {
     uint32_t num_qubits = 0;
     std::vector<qsr_gate> gates;
+    uint32_t num_clbits = 0; // classical bits named in the source (labels only, circuit.hpp:103-105)
     uint64_t measure_count() const;
     void check_valid() const; // circuit.hpp:108-115
 };
@@ -116,5 +132,18 @@ Schedule schedule_windows(const Circuit &c, int mode);
 // (gates.hpp:149-165, measure.hpp:385-398), before anything touches the device.
 void validate_window(uint64_t n, const qsr_gate *gates, uint64_t ngates, bool is_measurement,
                      std::vector<uint32_t> &stamp, uint32_t stamp_id);
+
+// OpenQASM 2.0 subset (qasm.hpp:29-271) and schedule text / validation (schedule.hpp:143-249).
+struct QasmFailure : std::runtime_error {
+    int line, column;
+    std::string reason;
+    QasmFailure(const std::string &r, int l, int c)
+        : std::runtime_error("qasm:" + std::to_string(l) + ":" + std::to_string(c) + ": " + r),
+          line(l), column(c), reason(r) {}
+};
+Circuit parse_qasm(const char *text, uint64_t len);         // throws QasmFailure
+uint64_t emit_qasm(const Circuit &c, char *out);             // out = NULL: size only
+uint64_t schedule_text(const Schedule &s, char *out);        // out = NULL: size only
+std::string validate_schedule(const Circuit &c, const Schedule &s);
 
 } // namespace qsr

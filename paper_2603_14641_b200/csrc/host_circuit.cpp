@@ -15,6 +15,7 @@
 // later makes measure_window reject the window is therefore preserved).
 #include <cstdio>
 #include <algorithm>
+#include <atomic>
 #include <cstring>
 #include <thread>
 
@@ -28,6 +29,15 @@ bool trace_on() {
         return e && e[0] == '1';
     }();
     return on;
+}
+
+namespace {
+std::atomic<unsigned> g_threads{0};
+}
+void set_host_threads(unsigned t) { g_threads = t; }
+unsigned host_threads() {
+    const unsigned t = g_threads.load();
+    return t ? t : std::max(1u, std::thread::hardware_concurrency());
 }
 
 void trace(const char *phase, double ms) { fprintf(stderr, "[qsr] %-28s %10.2f ms\n", phase, ms); }
@@ -114,6 +124,7 @@ Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measur
     Stream rng{seed, 2 /* kStreamGenerator */};
     Circuit c;
     c.num_qubits = n;
+    c.num_clbits = n; // circuit.hpp:171
     // ~0.6875 gates per qubit per layer for the uniform 11-kind draw.
     c.gates.reserve(size_t(double(n) * depth * 0.69) + n / 8 + 16);
     std::vector<uint32_t> order(n);
@@ -183,7 +194,7 @@ WindowPlan plan_windows(const Circuit &c) {
     p.nkeys = 2 * uint64_t(max_round) + 2;
     // Per-thread key histograms over contiguous gate chunks -> stable scatter offsets
     // (key-major, chunk-minor), so the parallel scatter keeps circuit index order per window.
-    const unsigned T = p.threads = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+    const unsigned T = p.threads = std::max(1u, std::min<unsigned>(host_threads(),
                                                                      unsigned(G / (1 << 16)) + 1));
     p.chunk_offsets.assign(uint64_t(T) * p.nkeys, 0);
     {

@@ -12,16 +12,30 @@ namespace qsr {
 
 namespace {
 
+// Z-frame word (q, j) of the 64-bit device layout for the reference word type W = wbits
+// (frames.hpp:55-66, 141-145): the reference keys one Philox word per W-bit word j_W and keeps its
+// low W bits, so a 64-bit device word is 64 / W such draws (j_W = j * 64 / W + i), shot order kept.
+__device__ __forceinline__ uint64_t frame_word(uint64_t seed, uint32_t epoch, uint64_t q, uint64_t jg,
+                                               uint32_t wbits) {
+    if (wbits == 64) return d_philox_word(seed, 1, epoch, (q << 24) | jg);
+    const uint32_t per = 64 / wbits;
+    const uint64_t m = (uint64_t(1) << wbits) - 1;
+    uint64_t w = 0;
+    for (uint32_t i = 0; i < per; ++i)
+        w |= (d_philox_word(seed, 1, epoch, (q << 24) | (jg * per + i)) & m) << (i * wbits);
+    return w;
+}
+
 // kf = shot-words held here, j0 = their global offset, jl = global index of the last word
 // (the one the last-word mask applies to). Unsharded: j0 = 0, jl = kf - 1.
 __global__ void k_frames_init(uint64_t *__restrict__ zf, uint64_t n, uint64_t kf, uint64_t j0,
                               uint64_t jl, uint64_t pitch, uint64_t last_mask, uint64_t seed,
-                              uint32_t epoch) {
+                              uint32_t epoch, uint32_t wbits) {
     const uint64_t total = n * kf;
     for (uint64_t idx = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
          idx += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t q = idx / kf, j = idx % kf, jg = j0 + j;
-        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | jg);
+        uint64_t w = frame_word(seed, epoch, q, jg, wbits);
         if (jg == jl) w &= last_mask;
         zf[q * pitch + j] = w;
     }
@@ -32,14 +46,14 @@ __global__ void k_measure_sample(const uint64_t *__restrict__ xf, uint64_t *__re
                                  uint64_t last_mask,
                                  uint64_t *__restrict__ rec, const uint32_t *__restrict__ qubits,
                                  const uint32_t *__restrict__ rows, uint64_t m, uint64_t seed,
-                                 uint32_t epoch) {
+                                 uint32_t epoch, uint32_t wbits) {
     const uint64_t total = m * kf;
     for (uint64_t item = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; item < total;
          item += uint64_t(gridDim.x) * blockDim.x) {
         uint64_t i = item / kf, j = item % kf, jg = j0 + j;
         uint64_t q = qubits[i];
         rec[uint64_t(rows[i]) * pitch + j] = xf[q * pitch + j];
-        uint64_t w = d_philox_word(seed, 1, epoch, (q << 24) | jg);
+        uint64_t w = frame_word(seed, epoch, q, jg, wbits);
         if (jg == jl) w &= last_mask;
         zf[q * pitch + j] = w;
     }
@@ -97,9 +111,9 @@ inline unsigned grid_for(uint64_t total, unsigned threads) {
 } // namespace
 
 void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t j0, uint64_t pitch,
-                        uint64_t shots, uint64_t seed, uint32_t epoch, cudaStream_t st) {
+                        uint64_t shots, uint64_t seed, uint32_t epoch, uint32_t wbits, cudaStream_t st) {
     k_frames_init<<<grid_for(n * kf, 256), 256, 0, st>>>(zf, n, kf, j0, (shots + 63) / 64 - 1, pitch,
-                                                         last_mask_for(shots), seed, epoch);
+                                                         last_mask_for(shots), seed, epoch, wbits);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
@@ -107,11 +121,11 @@ void launch_frames_init(uint64_t *zf, uint64_t n, uint64_t kf, uint64_t j0, uint
 void launch_measure_sample(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t kf, uint64_t j0,
                            uint64_t shots, uint64_t *rec, const uint32_t *qubits,
                            const uint32_t *rows, uint64_t m, uint64_t seed, uint32_t epoch,
-                           cudaStream_t st) {
+                           uint32_t wbits, cudaStream_t st) {
     if (m == 0) return;
     k_measure_sample<<<grid_for(m * kf, 256), 256, 0, st>>>(xf, zf, pitch, kf, j0, (shots + 63) / 64 - 1,
                                                             last_mask_for(shots), rec, qubits, rows,
-                                                            m, seed, epoch);
+                                                            m, seed, epoch, wbits);
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (ENTRY_DTYPE, GATE_DTYPE, CudaError, InvalidArgument, LogicError,  # noqa: F401
-                   OutOfRange, QuasarError, check, lib, ptr)
+                   OutOfRange, QasmError, QuasarError, check, lib, ptr)
 
 __all__ = [
     "GateKind", "Gate", "Circuit", "generate_random", "ScheduleMode", "Window", "Schedule",
@@ -24,7 +24,8 @@ __all__ = [
     "find_probabilistic", "find_and_compact_pivots", "parallel_ge", "swap_anti_commuting",
     "inject_x", "deterministic_outcome", "run_single_shot", "FrameTableau", "init_frames",
     "apply_window_frames", "ShotRecord", "measure_sample", "sample", "Engine", "ShardedEngine",
-    "shard_range", "nccl_unique_id", "sample_shard",
+    "shard_range", "nccl_unique_id", "sample_shard", "parse_qasm", "emit_qasm", "QasmError",
+    "validate_schedule", "set_num_threads", "check_group_validity",
     "kStreamMeasure", "kStreamFrames", "kStreamGenerator", "kGeBlockTargets",
     "InvalidArgument", "OutOfRange", "LogicError", "CudaError", "QuasarError",
 ]
@@ -125,6 +126,16 @@ class Circuit:
     def num_qubits(self) -> int:
         return self._info()[0]
 
+    @property
+    def num_clbits(self) -> int:  # circuit.hpp:103-105 (labels only; not part of ==)
+        v = C.c_uint32()
+        check(lib.qsr_circuit_clbits(self._h, C.byref(v)))
+        return v.value
+
+    @num_clbits.setter
+    def num_clbits(self, v: int) -> None:
+        check(lib.qsr_circuit_set_clbits(self._h, int(v)))
+
     def measure_count(self) -> int:
         return self._info()[2]
 
@@ -182,7 +193,7 @@ class Schedule:
             return
         windows = list(windows or [])
         arrs = [w.array() for w in windows]
-        gates = np.concatenate(arrs) if arrs else np.zeros(0, dtype=GATE_DTYPE)
+        gates = gates_array(np.concatenate(arrs)) if arrs else np.zeros(0, dtype=GATE_DTYPE)
         offsets = np.zeros(len(windows) + 1, dtype=np.uint64)
         offsets[1:] = np.cumsum([len(a) for a in arrs]) if arrs else []
         flags = np.array([1 if w.is_measurement else 0 for w in windows], dtype=np.uint8)
@@ -238,14 +249,34 @@ def schedule_windows(circuit: Circuit, mode=ScheduleMode.single_shot) -> Schedul
 
 
 def schedule_to_text(schedule: Schedule) -> str:  # schedule.hpp:235-249
-    names = ["x", "y", "z", "h", "s", "sdg", "cx", "cy", "cz", "swap", "iswap", "measure"]
-    out = []
-    for wi, w in enumerate(schedule.windows):
-        s = f"W{wi}" + (" M:" if w.is_measurement else " U:")
-        for g in w.gates:
-            s += f" {names[g.kind]}({g.q0}" + (f",{g.q1}" if g.arity() == 2 else "") + ")"
-        out.append(s + "\n")
-    return "".join(out)
+    return _lib.text(lib.qsr_schedule_text, schedule._h).decode()
+
+
+def validate_schedule(circuit: Circuit, schedule: Schedule) -> str:  # schedule.hpp:143-233
+    return _lib.text(lib.qsr_validate_schedule, circuit._h, schedule._h).decode()
+
+
+def parse_qasm(text) -> Circuit:
+    """parse_qasm (qasm.hpp:159-252). Raises QasmError (with .line / .column) like the reference."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    h, err = C.c_void_p(), _lib.QasmError_t()
+    st = lib.qsr_parse_qasm(data, len(data), C.byref(h), C.byref(err))
+    if st == _lib.PARSE_ERROR:
+        raise QasmError((lib.qsr_last_error() or b"").decode(errors="replace"), err.line, err.column)
+    check(st)
+    return Circuit(_handle=h)
+
+
+def emit_qasm(circuit: Circuit) -> str:  # qasm.hpp:254-271
+    return _lib.text(lib.qsr_emit_qasm, circuit._h).decode()
+
+
+def check_group_validity(t: "Tableau") -> str:  # tableau.hpp:184-213
+    return t.check_group_validity()
+
+
+def set_num_threads(threads: int) -> None:  # parallel.hpp:151 (host passes; 0 = hardware default)
+    lib.qsr_set_num_threads(int(threads))
 
 
 class Layout(enum.IntEnum):  # tableau.hpp:30
@@ -487,6 +518,9 @@ class Tableau:
         s = self.signs()
         half, idx = (0, g) if g < n else (k, g - n)
         return bool((int(s[half + idx // 64]) >> (idx % 64)) & 1)
+
+    def check_group_validity(self) -> str:  # tableau.hpp:184-213 (device kernel)
+        return _lib.text(lib.qsr_tableau_check_validity, self._h).decode()
 
     def transpose_in_place(self) -> None:  # tableau.hpp:166-176
         check(lib.qsr_transpose_in_place(self._h))
@@ -813,9 +847,10 @@ class FrameTableau:
         return ShotRecord(shots, kf, [int(q) for q in measured], words)
 
 
-def init_frames(n: int, shots: int, seed: int, device: int = 0) -> FrameTableau:
+def init_frames(n: int, shots: int, seed: int, device: int = 0, word_bits: int = 64) -> FrameTableau:
+    """init_frames<W> (frames.hpp:46-72), W = word_bits; the device layout stays 64-bit words."""
     h = C.c_void_p()
-    check(lib.qsr_init_frames(n, shots, seed, device, C.byref(h)))
+    check(lib.qsr_init_frames_word(n, shots, seed, word_bits, device, C.byref(h)))
     return FrameTableau(h)
 
 
@@ -834,6 +869,12 @@ class ShotRecord:  # frames.hpp:97-107
     def bit(self, row: int, shot: int) -> bool:
         return bool((int(self.words[row * self.kf + shot // 64]) >> (shot % 64)) & 1)
 
+    def row_bytes(self, word_bits: int = 64) -> np.ndarray:
+        """[rows, ceil(shots/W)*W/8] little-endian bytes = the reference's ShotRecord<W> rows."""
+        rb = -(-self.shots // word_bits) * word_bits // 8
+        b = np.ascontiguousarray(self.words.astype("<u8")).view(np.uint8)
+        return b.reshape(len(self.measured), self.kf * 8)[:, :rb]
+
 
 def measure_sample(f: FrameTableau, window: Window, record=None, seed: int = 0, epoch: int = 1) -> None:
     """measure_sample (frames.hpp:111-158); the ShotRecord lives in the frames object
@@ -843,11 +884,12 @@ def measure_sample(f: FrameTableau, window: Window, record=None, seed: int = 0, 
 
 
 def sample(circuit: Circuit, shots: int, seed: int, report: Optional[RunReport] = None,
-           device: int = 0) -> ShotRecord:
-    """sample<uint64_t>(circuit, shots, seed, report) (frames.hpp:163-204)."""
+           device: int = 0, word_bits: int = 64) -> ShotRecord:
+    """sample<W>(circuit, shots, seed, report) (frames.hpp:163-204), W = word_bits in {8, 16, 32,
+    64}. The record keeps 64-bit words; ShotRecord.row_bytes(W) gives the reference's W rows."""
     h = C.c_void_p()
     rep = _lib.Report_t()
-    check(lib.qsr_sample(circuit._h, shots, seed, device, C.byref(h), C.byref(rep)))
+    check(lib.qsr_sample_word(circuit._h, shots, seed, word_bits, device, C.byref(h), C.byref(rep)))
     f = FrameTableau(h)
     if report is not None:
         r = RunReport.from_c(rep)
