@@ -9,9 +9,11 @@
 //     auto r = quasar::gpu::run_single_shot<uint64_t>(circuit, seed);   // was quasar::
 //
 // Signatures, results (bit-exact) and exception types are the reference's: the C ABI status
-// is rethrown as std::invalid_argument / std::out_of_range / std::logic_error. Only the word
-// type uint64_t (the reference default) is provided. Host Tableau<uint64_t> arguments are
-// uploaded, processed on the GPU and downloaded in the reference's own storage layout.
+// is rethrown as std::invalid_argument / std::out_of_range / std::logic_error, parse errors as
+// quasar::QasmError with the reference's line / column. Tableau-valued calls take the word type
+// uint64_t (the reference default); sample<W> takes every W of the reference. Host
+// Tableau<uint64_t> arguments are uploaded, processed on the GPU and downloaded in the
+// reference's own storage layout.
 #ifndef QUASAR_GPU_HPP_
 #define QUASAR_GPU_HPP_
 
@@ -25,6 +27,7 @@
 #include "qsr.h"
 #include "quasar/frames.hpp"
 #include "quasar/measure.hpp"
+#include "quasar/qasm.hpp"
 #include "quasar/simulator.hpp"
 
 namespace quasar::gpu {
@@ -228,26 +231,78 @@ inline void measure_window(Tableau<uint64_t> &t, const Window &window, RandomStr
     }
 }
 
-// sample<uint64_t>(circuit, shots, seed, report)   (frames.hpp:163-204)
+// sample<W>(circuit, shots, seed, report)   (frames.hpp:163-204), every W of the reference. The
+// engine keeps 64-bit shot words and draws the Z frames as sample<W> does; the little-endian bytes
+// of a row are the W-words of the reference's row.
 template <Word W>
 ShotRecord<W> sample(const Circuit &circuit, size_t shots, uint64_t seed, RunReport *report = nullptr) {
-    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
     auto ch = detail::circuit(circuit);
     qsr_frames *fh = nullptr;
     qsr_run_report rep{};
-    check(qsr_sample(ch.get(), shots, seed, device(), &fh, &rep));
+    check(qsr_sample_word(ch.get(), shots, seed, unsigned(8 * sizeof(W)), device(), &fh, &rep));
     detail::FramesPtr fp(fh);
-    uint64_t nrows = 0, kf = 0;
+    uint64_t nrows = 0, kf64 = 0;
     check(qsr_frames_record(fh, &nrows, nullptr, nullptr));
-    check(qsr_frames_info(fh, nullptr, nullptr, &kf));
-    ShotRecord<uint64_t> r;
+    check(qsr_frames_info(fh, nullptr, nullptr, &kf64));
+    std::vector<uint64_t> words(nrows * kf64);
+    ShotRecord<W> r;
     r.shots = shots;
-    r.kf = kf;
+    r.kf = (shots + 8 * sizeof(W) - 1) / (8 * sizeof(W));
     r.measured.resize(nrows);
-    r.words.resize(nrows * kf);
-    check(qsr_frames_record(fh, &nrows, r.measured.data(), r.words.data()));
+    check(qsr_frames_record(fh, &nrows, r.measured.data(), words.data()));
+    r.words.resize(nrows * r.kf);
+    constexpr size_t per = 64 / (8 * sizeof(W));
+    for (uint64_t row = 0; row < nrows; ++row)
+        for (size_t j = 0; j < r.kf; ++j)
+            r.words[row * r.kf + j] =
+                static_cast<W>(words[row * kf64 + j / per] >> (8 * sizeof(W) * (j % per)));
     if (report) *report = detail::report(rep);
     return r;
+}
+
+// parse_qasm(text)   (qasm.hpp:159-252): same Circuit, same QasmError (line, column, reason);
+// large bodies are parsed on all host threads.
+inline Circuit parse_qasm(std::string_view text) {
+    qsr_circuit *h = nullptr;
+    qsr_qasm_error err{};
+    const qsr_status st = qsr_parse_qasm(text.data(), text.size(), &h, &err);
+    if (st == QSR_PARSE_ERROR) {
+        std::string what = qsr_last_error(); // "qasm:L:C: reason"
+        size_t p = what.find(": ");
+        throw QasmError(p == std::string::npos ? what : what.substr(p + 2), err.line, err.column);
+    }
+    check(st);
+    detail::CircuitPtr cp(h);
+    uint32_t nq = 0, ncl = 0;
+    uint64_t ng = 0;
+    check(qsr_circuit_info(h, &nq, &ng, nullptr));
+    check(qsr_circuit_clbits(h, &ncl));
+    Circuit c;
+    c.num_qubits = nq;
+    c.num_clbits = ncl;
+    const Gate *g = reinterpret_cast<const Gate *>(qsr_circuit_gates(h));
+    c.gates.assign(g, g + ng);
+    return c;
+}
+
+// emit_qasm(circuit)   (qasm.hpp:254-271)
+inline std::string emit_qasm(const Circuit &circuit) {
+    auto ch = detail::circuit(circuit);
+    uint64_t len = 0;
+    check(qsr_emit_qasm(ch.get(), nullptr, 0, &len));
+    std::string out(len, '\0');
+    check(qsr_emit_qasm(ch.get(), out.data(), len, &len));
+    return out;
+}
+
+// Tableau::check_group_validity()   (tableau.hpp:184-213) on the device.
+inline std::string check_group_validity(const Tableau<uint64_t> &t) {
+    auto h = detail::upload(t);
+    uint64_t len = 0;
+    check(qsr_tableau_check_validity(h.get(), nullptr, 0, &len));
+    std::string out(len, '\0');
+    check(qsr_tableau_check_validity(h.get(), out.data(), len, &len));
+    return out;
 }
 
 } // namespace quasar::gpu

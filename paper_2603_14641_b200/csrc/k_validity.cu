@@ -5,10 +5,10 @@
 // iff i == j), returning the first violation in that order; O(n^2 k) words, days at c5 on a CPU.
 // Here the needed half of the 2n x 2n symplectic Gram matrix is computed as a tiled GF(2)
 // product over the generator-major (RM) planes, where each generator's qubit words are
-// contiguous: a CTA owns a 64 x 128 block of generator pairs, stages 16 qubit-words of both
+// contiguous: a CTA owns a 64 x 128 block of generator pairs, stages 8 qubit-words of both
 // blocks' X and Z rows in shared memory, and each thread XOR-accumulates a 4 x 8 pair block
 // (rows strided by 16 so a half-warp reads 16 consecutive words: no bank conflicts)
-// acc ^= (xa & zb) ^ (za & xb) (two LOP3 per 32-bit half); parity(popc(acc)) is the inner
+// acc ^= (xa & zb) ^ (za & xb) (four LOP3 per pair-word); parity(popc(acc)) is the inner
 // product (the parity of a sum of popcounts is the popcount of the XOR). Violations are
 // reduced to the reference's first one with one atomicMin on the key (i*n + j)*3 + check.
 #include <algorithm>
@@ -20,9 +20,9 @@ namespace qsr {
 
 namespace {
 
-constexpr int kRowsA = 64, kRowsB = 128, kWords = 16, kThreads = 256;
+constexpr int kRowsA = 64, kRowsB = 128, kWords = 8, kThreads = 256;
 
-__global__ void __launch_bounds__(kThreads) k_sympl_gram(const uint64_t *__restrict__ x,
+__global__ void __launch_bounds__(kThreads, 2) k_sympl_gram(const uint64_t *__restrict__ x,
                                                          const uint64_t *__restrict__ z, uint64_t pitch,
                                                          uint64_t kw, uint64_t ng, uint64_t n,
                                                          unsigned long long *__restrict__ first) {
@@ -36,13 +36,15 @@ __global__ void __launch_bounds__(kThreads) k_sympl_gram(const uint64_t *__restr
     __shared__ uint64_t ax[kWords][kRowsA + 1], az[kWords][kRowsA + 1];
     __shared__ uint64_t bx[kWords][kRowsB + 1], bz[kWords][kRowsB + 1];
     const int t = threadIdx.x, ta = t / 16, tb = t % 16;
-    uint64_t acc[4][8];
+    // parity(popc(v)) = parity(popc(lo(v) ^ hi(v))): 32-bit accumulators suffice (and free the
+    // registers for two CTAs per SM).
+    uint32_t acc[4][8];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0;
     for (uint64_t c = 0; c < kw; c += kWords) {
-        // Stage: 16 contiguous words (128 B) per row; RM rows are padded to pitch (multiple of
+        // Stage: 8 contiguous words (64 B) per row; RM rows are padded to pitch (multiple of
         // 16) with zeros, so no word-bound checks are needed.
 #pragma unroll
         for (int i = 0; i < kRowsA * kWords / kThreads; ++i) {
@@ -75,7 +77,10 @@ __global__ void __launch_bounds__(kThreads) k_sympl_gram(const uint64_t *__restr
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
-                for (int j = 0; j < 8; ++j) acc[i][j] ^= (xa[i] & zb[j]) ^ (za[i] & xb[j]);
+                for (int j = 0; j < 8; ++j) {
+                    const uint64_t v = (xa[i] & zb[j]) ^ (za[i] & xb[j]);
+                    acc[i][j] ^= uint32_t(v) ^ uint32_t(v >> 32);
+                }
         }
         __syncthreads();
     }
@@ -95,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) k_sympl_gram(const uint64_t *__restr
             else if (!da && !db) { ci = ia; cj = ib; check = 0; } // stabilizers i, j
             else if (ib >= ia) { ci = ia; cj = ib; check = 2; expect = ia == ib; } // D_i vs S_j, j >= i
             else continue;                                        // j < i: not checked
-            const int bit = __popcll(acc[i][j]) & 1;
+            const int bit = __popc(acc[i][j]) & 1;
             if (bit != expect) {
                 const unsigned long long key = (ci * n + cj) * 3 + check;
                 best = key < best ? key : best;

@@ -119,6 +119,46 @@ int main() {
             CHECK(rc.probabilistic_count == rg.probabilistic_count);
         }
     }
+    // sample<W> for the reference's other word types
+    for (uint64_t seed = 0; seed < 3; ++seed) {
+        Circuit c = generate_random(uint32_t(6 + seed * 7), 12, 300 + seed, 0.7);
+        for (size_t shots : {size_t(1), size_t(9), size_t(777)}) {
+            auto a8 = sample<uint8_t>(c, shots, seed);
+            auto b8 = gpu::sample<uint8_t>(c, shots, seed);
+            CHECK(a8.measured == b8.measured && a8.words == b8.words && a8.kf == b8.kf);
+            auto a16 = sample<uint16_t>(c, shots, seed);
+            auto b16 = gpu::sample<uint16_t>(c, shots, seed);
+            CHECK(a16.measured == b16.measured && a16.words == b16.words && a16.kf == b16.kf);
+            auto a32 = sample<uint32_t>(c, shots, seed);
+            auto b32 = gpu::sample<uint32_t>(c, shots, seed);
+            CHECK(a32.measured == b32.measured && a32.words == b32.words && a32.kf == b32.kf);
+        }
+    }
+    // parse_qasm / emit_qasm (qasm.hpp), QasmError position and reason
+    for (uint64_t seed : {1ull, 2ull, 99ull}) {
+        Circuit c = generate_random(100, 60, seed, 0.5);
+        std::string text = emit_qasm(c);
+        CHECK(gpu::emit_qasm(c) == text);
+        Circuit p = gpu::parse_qasm(text);
+        CHECK(p == parse_qasm(text) && p.num_clbits == parse_qasm(text).num_clbits);
+    }
+    for (const char *bad : {"OPENQASM 2.0;\nqreg q[1];\nt q[0];\n", "OPENQASM 2.0;\nqreg q[2];\ncx q[1],q[1];\n",
+                            "qreg q[2];\n", "OPENQASM 2.0;\nqreg q[2];\nh q[0]\n"}) {
+        std::string ref_what, gpu_what;
+        int rl = -1, rc = -1, gl = -2, gc = -2;
+        try { parse_qasm(bad); } catch (const QasmError &e) { ref_what = e.what(); rl = e.line; rc = e.column; }
+        try { gpu::parse_qasm(bad); } catch (const QasmError &e) { gpu_what = e.what(); gl = e.line; gc = e.column; }
+        CHECK(!ref_what.empty() && ref_what == gpu_what && rl == gl && rc == gc);
+    }
+    // check_group_validity on evolved and on corrupted tableaux
+    for (uint64_t seed = 0; seed < 8; ++seed) {
+        Circuit c = generate_random(uint32_t(5 + seed * 19), 12, 500 + seed, 0.4);
+        auto r = run_single_shot<uint64_t>(c, seed);
+        CHECK(gpu::check_group_validity(r.tableau) == "valid");
+        auto t = r.tableau;
+        t.x_plane()[(seed * 7) % t.num_qubits() * 2 * t.num_words()] ^= uint64_t(1) << (seed % 5);
+        CHECK(gpu::check_group_validity(t) == t.check_group_validity());
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "dropin ok", failures);
     return failures ? 1 : 0;
 }
