@@ -42,6 +42,19 @@ def test_generate_random_matches_oracle(q, oracles, n, depth, seed, p):
         np.testing.assert_array_equal(c.gate_array, o.generate_random(n, depth, seed, p))
 
 
+@pytest.mark.parametrize("threads", [2, 3, 8])
+@pytest.mark.parametrize("n,depth,seed,p", [(5001, 300, 3, 0.3), (4096, 257, 9, 1.0), (4097, 256, 11, 0.5)])
+def test_parallel_generator_matches_oracle(q, oracles, threads, n, depth, seed, p):
+    """Sizes that take the multi-threaded generator (Philox words drawn ahead on workers, kind
+    scan by chunk sums, layers emitted in place by several threads)."""
+    q.set_num_threads(threads)
+    try:
+        c = q.generate_random(n, depth, seed, p)
+    finally:
+        q.set_num_threads(0)
+    np.testing.assert_array_equal(c.gate_array, oracles[0].generate_random(n, depth, seed, p))
+
+
 def test_generator_errors(q):
     with pytest.raises(q.InvalidArgument):
         q.generate_random(0, 5, 1, 0.5)
