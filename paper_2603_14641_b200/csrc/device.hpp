@@ -114,6 +114,11 @@ struct DeviceTableau {
 // ---- launchers --------------------------------------------------------------------
 // Gate window on a CM tableau: `gates` is a device array of packed gate words.
 void launch_gate_window(DeviceTableau &t, const uint64_t *gates, uint64_t ngates);
+// Two consecutive windows as component records (pair.hpp; k_gates.cu K1p).
+constexpr int kPairRows = 6, kPairGates = 8, kPairRecWords = 16;
+void launch_gate_pairs(DeviceTableau &t, const uint64_t *recs, uint64_t nrec);
+void launch_frame_pairs(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *recs, uint64_t nrec,
+                        int num_sms, cudaStream_t st);
 // All windows of a unitary segment in one persistent launch (temporally blocked, L2-resident
 // slabs; k_gates.cu). d_woff = device window offsets into `gates` (nwin + 1 entries).
 bool gate_segment_enabled();

@@ -1,6 +1,7 @@
 // Device-resident schedules, the single-shot driver and layout conversion (engine.hpp).
 #include "engine.hpp"
 #include "fuse.hpp"
+#include "pair.hpp"
 
 #include <algorithm>
 #include <thread>
@@ -53,17 +54,61 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
     const std::vector<uint8_t> is_meas = ds.is_meas;
     ds.offsets.assign(1, 0);
     ds.is_meas.clear();
+    ds.wkind.clear();
     ds.mqubits.clear();
     ds.wwords.clear();
-    auto close_unitary = [&](size_t s0) {
-        if (out.size() == s0) return;
+    auto gate_words = [](const uint64_t *g, size_t cnt) {
         uint32_t words = 0;
-        for (size_t i = s0; i < out.size(); ++i)
-            words += uint32_t(__builtin_popcount(packed_reads(out[i])) + __builtin_popcount(packed_writes(out[i])));
+        for (size_t i = 0; i < cnt; ++i)
+            words += uint32_t(__builtin_popcount(packed_reads(g[i])) + __builtin_popcount(packed_writes(g[i])));
+        return words;
+    };
+    auto push_window = [&](uint8_t kind, uint64_t words) {
         ds.offsets.push_back(out.size());
         ds.is_meas.push_back(0);
+        ds.wkind.push_back(kind);
         ds.mqubits.emplace_back();
-        ds.wwords.push_back(words);
+        ds.wwords.push_back(uint32_t(words));
+    };
+    // Window pairing (pair.hpp): a finished unitary window is held until the next one, and the
+    // two are rewritten as component records + the two windows' oversized remainders.
+    const bool pairing = pairing_enabled() && !gate_segment_enabled();
+    Pairer pairer(pairing ? n : 0);
+    PairOut po;
+    size_t held = SIZE_MAX; // start of the held window in `out` (it runs to out.size())
+    auto flush_held = [&] {
+        if (held == SIZE_MAX) return;
+        push_window(0, gate_words(out.data() + held, out.size() - held));
+        held = SIZE_MAX;
+    };
+    auto close_unitary = [&](size_t s0) {
+        if (out.size() == s0) return;
+        if (!pairing) {
+            push_window(0, gate_words(out.data() + s0, out.size() - s0));
+            return;
+        }
+        if (held == SIZE_MAX) {
+            held = s0;
+            return;
+        }
+        const std::vector<uint64_t> A(out.begin() + long(held), out.begin() + long(s0));
+        const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
+        out.resize(held);
+        held = SIZE_MAX;
+        pairer.pair(A.data(), A.size(), B.data(), B.size(), po);
+        if (!po.records.empty()) {
+            if (out.size() & 1) out.push_back(0); // records start 16-byte aligned (see dispatch)
+            out.insert(out.end(), po.records.begin(), po.records.end());
+            push_window(1, po.record_words);
+        }
+        if (!po.rest_a.empty()) {
+            out.insert(out.end(), po.rest_a.begin(), po.rest_a.end());
+            push_window(0, gate_words(po.rest_a.data(), po.rest_a.size()));
+        }
+        if (!po.rest_b.empty()) {
+            out.insert(out.end(), po.rest_b.begin(), po.rest_b.end());
+            push_window(0, gate_words(po.rest_b.data(), po.rest_b.size()));
+        }
     };
     for (size_t w = 0; w + 1 < offsets.size(); ++w) {
         const uint64_t b = offsets[w], e = offsets[w + 1];
@@ -75,6 +120,7 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         }
         f.flush(out);
         close_unitary(s0);
+        flush_held();
         auto unpermute_here = [&] {
             ds.perm_at.resize(ds.is_meas.size() + 1, -1);
             if (f.identity_permutation()) return;
@@ -91,12 +137,14 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         }
         ds.offsets.push_back(out.size());
         ds.is_meas.push_back(1);
+        ds.wkind.push_back(0);
         ds.mqubits.push_back(std::move(qs));
         ds.wwords.push_back(0);
     }
     const size_t s0 = out.size();
     f.flush(out);
     close_unitary(s0);
+    flush_held();
     ds.perm_at.resize(ds.is_meas.size() + 1, -1);
     if (!f.identity_permutation()) {
         ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
@@ -227,8 +275,14 @@ uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_
         launch_gate_segment(t, ds.d_gates, ds.d_offsets + w0, uint32_t(w1 - w0));
         return 1;
     }
-    for (uint64_t w = w0; w < w1; ++w)
-        launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+    for (uint64_t w = w0; w < w1; ++w) {
+        const uint64_t cnt = ds.offsets[w + 1] - ds.offsets[w];
+        if (w < ds.wkind.size() && ds.wkind[w] == 1) {
+            const uint64_t b = ds.offsets[w] + (ds.offsets[w] & 1); // a pad word keeps 16-B alignment
+            launch_gate_pairs(t, ds.d_gates + b, (ds.offsets[w + 1] - b) / kPairRecWords);
+        } else
+            launch_gate_window(t, ds.d_gates + ds.offsets[w], cnt);
+    }
     return w1 - w0;
 }
 

@@ -17,6 +17,7 @@ struct DeviceSchedule {
     uint64_t *d_offsets = nullptr; // device copy of offsets (segment kernel)
     std::vector<uint64_t> offsets;
     std::vector<uint8_t> is_meas;
+    std::vector<uint8_t> wkind; // unitary windows: 0 = packed gates, 1 = pair records (pair.hpp)
     std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
     uint64_t measure_count = 0, unitary_count = 0; // of the circuit (before fusion)
     // Gate fusion (fuse.hpp): per-window device words moved per generator-word (reads + writes,

@@ -83,21 +83,52 @@ __device__ __forceinline__ V2 rule2(uint32_t kind, V2 &x0, V2 &z0, V2 &x1, V2 &z
 
 __device__ __forceinline__ uint64_t bitmask(uint32_t c, int b) { return 0ull - uint64_t((c >> b) & 1u); }
 
-// One of the 24 single-qubit Cliffords (kCliff1) on a word pair; returns the sign-flip words.
-__device__ __forceinline__ V2 cliff1_apply(uint32_t e, V2 &x, V2 &z) {
-    const uint32_t c = kCliff1[e];
-    const uint64_t m00 = bitmask(c, 0), m01 = bitmask(c, 1), m10 = bitmask(c, 2), m11 = bitmask(c, 3);
-    const uint64_t fx = bitmask(c, 4), fz = bitmask(c, 5), fy = bitmask(c, 6);
-    V2 f, nx, nz;
-    f.a = (fx & x.a & ~z.a) ^ (fz & z.a & ~x.a) ^ (fy & x.a & z.a);
-    f.b = (fx & x.b & ~z.b) ^ (fz & z.b & ~x.b) ^ (fy & x.b & z.b);
-    nx.a = (m00 & x.a) ^ (m01 & z.a);
-    nx.b = (m00 & x.b) ^ (m01 & z.b);
-    nz.a = (m10 & x.a) ^ (m11 & z.a);
-    nz.b = (m10 & x.b) ^ (m11 & z.b);
+// One of the 24 single-qubit Cliffords (kCliff1 encoding: bits 0-3 matrix m00 m01 m10 m11, bits
+// 4-6 sign flips of the images of X, Z, Y) on a word pair; returns the sign-flip words. Each
+// element is a compile-time instance (the masks fold away: 2-6 logic ops per word instead of
+// table-driven masking), selected by a warp-uniform switch.
+template <uint32_t C>
+__device__ __forceinline__ V2 cliff1_fixed(V2 &x, V2 &z) {
+    V2 f{0, 0}, nx{0, 0}, nz{0, 0};
+    if (C & 16u) f ^= x & ~z;
+    if (C & 32u) f ^= z & ~x;
+    if (C & 64u) f ^= x & z;
+    if (C & 1u) nx ^= x;
+    if (C & 2u) nx ^= z;
+    if (C & 4u) nz ^= x;
+    if (C & 8u) nz ^= z;
     x = nx;
     z = nz;
     return f;
+}
+
+__device__ __forceinline__ V2 cliff1_apply(uint32_t e, V2 &x, V2 &z) {
+    switch (e) { // kCliff1 (common.cuh), element 0 = identity
+    case 1: return cliff1_fixed<105>(x, z);
+    case 2: return cliff1_fixed<57>(x, z);
+    case 3: return cliff1_fixed<89>(x, z);
+    case 4: return cliff1_fixed<70>(x, z);
+    case 5: return cliff1_fixed<77>(x, z);
+    case 6: return cliff1_fixed<29>(x, z);
+    case 7: return cliff1_fixed<38>(x, z);
+    case 8: return cliff1_fixed<45>(x, z);
+    case 9: return cliff1_fixed<125>(x, z);
+    case 10: return cliff1_fixed<118>(x, z);
+    case 11: return cliff1_fixed<22>(x, z);
+    case 12: return cliff1_fixed<14>(x, z);
+    case 13: return cliff1_fixed<110>(x, z);
+    case 14: return cliff1_fixed<87>(x, z);
+    case 15: return cliff1_fixed<7>(x, z);
+    case 16: return cliff1_fixed<55>(x, z);
+    case 17: return cliff1_fixed<103>(x, z);
+    case 18: return cliff1_fixed<62>(x, z);
+    case 19: return cliff1_fixed<94>(x, z);
+    case 20: return cliff1_fixed<43>(x, z);
+    case 21: return cliff1_fixed<75>(x, z);
+    case 22: return cliff1_fixed<123>(x, z);
+    case 23: return cliff1_fixed<27>(x, z);
+    default: return V2{0, 0};
+    }
 }
 
 // A packed gate on its operand words: the fused single-qubit pre-operations, then the rule.
@@ -113,6 +144,62 @@ __device__ __forceinline__ V2 gate2(uint64_t gw, V2 &x0, V2 &z0, V2 &x1, V2 &z1)
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kTileWords = 64;
+
+// Per-CTA sign fold: shared-memory XOR tree over the 8 warps (the reference's collapse_signs /
+// reduce_xor, bitplane.hpp:96-122, done per CTA); with several gate chunks per tile the last
+// CTA of the tile to arrive folds the per-chunk partials into S[j].
+__device__ __forceinline__ void fold_tile_signs(V2 sacc, uint32_t warp, uint32_t lane, uint64_t j, bool active,
+                                                uint64_t pitch, uint64_t *__restrict__ partials,
+                                                uint32_t *__restrict__ counters, uint64_t *__restrict__ s) {
+    __shared__ uint64_t red[kWarps][kTileWords];
+    __shared__ bool last;
+    red[warp][lane * 2] = sacc.a;
+    red[warp][lane * 2 + 1] = sacc.b;
+    __syncthreads();
+#pragma unroll
+    for (int h = kWarps / 2; h >= 1; h >>= 1) {
+        if (warp < uint32_t(h)) {
+            red[warp][lane * 2] ^= red[warp + h][lane * 2];
+            red[warp][lane * 2 + 1] ^= red[warp + h][lane * 2 + 1];
+        }
+        __syncthreads();
+    }
+    if (gridDim.y == 1) {
+        if (warp == 0 && active) {
+            s[j] ^= red[0][lane * 2];
+            s[j + 1] ^= red[0][lane * 2 + 1];
+        }
+        return;
+    }
+    if (warp == 0 && active) {
+        uint64_t *p = partials + uint64_t(blockIdx.y) * pitch + j;
+        __stcg(reinterpret_cast<ulonglong2 *>(p),
+               make_ulonglong2(red[0][lane * 2], red[0][lane * 2 + 1]));
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t prev = atomicAdd(counters + blockIdx.x, 1u);
+        last = prev == gridDim.y - 1;
+    }
+    __syncthreads();
+    if (last && warp == 0) {
+        __threadfence();
+        if (active) {
+            uint64_t a = 0, b = 0;
+            for (uint32_t c = 0; c < gridDim.y; ++c) {
+                ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2 *>(
+                    partials + uint64_t(c) * pitch + j));
+                a ^= v.x;
+                b ^= v.y;
+            }
+            s[j] ^= a;
+            s[j + 1] ^= b;
+        }
+        if (lane == 0)
+            counters[blockIdx.x] = 0; // re-armed for the next window
+    }
+}
 
 template <bool kSigns, int U, int kMinBlocks>
 __global__ void __launch_bounds__(kThreads, kMinBlocks)
@@ -139,8 +226,8 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
                 const uint64_t gw = gws[u] = __ldg(gates + g + kWarps * u);
                 rd[u] = gate_reads(gw, kSigns);
                 wr[u] = gate_writes(gw);
-                o0[u] = uint64_t(gate_q0(gw)) * pitch + j;
-                o1[u] = uint64_t(gate_q1(gw)) * pitch + j;
+                o0[u] = uint64_t(gate_q0(gw)) * uint32_t(pitch) + j;
+                o1[u] = uint64_t(gate_q1(gw)) * uint32_t(pitch) + j;
                 X0[u] = Z0[u] = X1[u] = Z1[u] = V2{0, 0};
                 if (rd[u] & 1) X0[u] = ld2(x + o0[u]);
                 if (rd[u] & 2) Z0[u] = ld2(z + o0[u]);
@@ -160,7 +247,7 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
         for (; g < g_end; g += kWarps) {
             uint64_t gw = __ldg(gates + g);
             uint32_t rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
-            uint64_t a0 = uint64_t(gate_q0(gw)) * pitch + j, a1 = uint64_t(gate_q1(gw)) * pitch + j;
+            uint64_t a0 = uint64_t(gate_q0(gw)) * uint32_t(pitch) + j, a1 = uint64_t(gate_q1(gw)) * uint32_t(pitch) + j;
             V2 X0{0, 0}, Z0{0, 0}, X1{0, 0}, Z1{0, 0};
             if (rd & 1) X0 = ld2(x + a0);
             if (rd & 2) Z0 = ld2(z + a0);
@@ -175,58 +262,7 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
         }
     }
 
-    if constexpr (kSigns) {
-        // Shared-memory XOR tree over the 8 warps (the reference's collapse_signs /
-        // reduce_xor, bitplane.hpp:96-122, done per CTA).
-        __shared__ uint64_t red[kWarps][kTileWords];
-        __shared__ bool last;
-        red[warp][lane * 2] = sacc.a;
-        red[warp][lane * 2 + 1] = sacc.b;
-        __syncthreads();
-#pragma unroll
-        for (int h = kWarps / 2; h >= 1; h >>= 1) {
-            if (warp < uint32_t(h)) {
-                red[warp][lane * 2] ^= red[warp + h][lane * 2];
-                red[warp][lane * 2 + 1] ^= red[warp + h][lane * 2 + 1];
-            }
-            __syncthreads();
-        }
-        if (gridDim.y == 1) {
-            if (warp == 0 && active) {
-                s[j] ^= red[0][lane * 2];
-                s[j + 1] ^= red[0][lane * 2 + 1];
-            }
-            return;
-        }
-        if (warp == 0 && active) {
-            uint64_t *p = partials + uint64_t(blockIdx.y) * pitch + j;
-            __stcg(reinterpret_cast<ulonglong2 *>(p),
-                   make_ulonglong2(red[0][lane * 2], red[0][lane * 2 + 1]));
-        }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t prev = atomicAdd(counters + blockIdx.x, 1u);
-            last = prev == gridDim.y - 1;
-        }
-        __syncthreads();
-        if (last && warp == 0) {
-            __threadfence();
-            if (active) {
-                uint64_t a = 0, b = 0;
-                for (uint32_t c = 0; c < gridDim.y; ++c) {
-                    ulonglong2 v = __ldcg(reinterpret_cast<const ulonglong2 *>(
-                        partials + uint64_t(c) * pitch + j));
-                    a ^= v.x;
-                    b ^= v.y;
-                }
-                s[j] ^= a;
-                s[j + 1] ^= b;
-            }
-            if (lane == 0)
-                counters[blockIdx.x] = 0; // re-armed for the next window
-        }
-    }
+    if constexpr (kSigns) fold_tile_signs(sacc, warp, lane, j, active, pitch, partials, counters, s);
 }
 
 // Kernel variants (unroll U, min resident CTAs): 0 = <2,3>, 1 = <1,4>, 2 = <2,4>, 3 = <2,2>,
@@ -245,24 +281,15 @@ int gate_variant(uint64_t ngates) {
     return ngates >= (uint64_t(1) << 14) ? 1 : 0;
 }
 
-template <bool kSigns, int U, int B>
-void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates,
-                    uint64_t ngates, int num_sms, cudaStream_t st, uint64_t **partials,
-                    uint64_t *partial_chunks, uint32_t *counters, uint64_t *s) {
-    static int bps = 0;
-    if (bps == 0) {
-        QSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &bps, k_gate_window<kSigns, U, B>, kThreads, 0));
-        if (bps < 1)
-            bps = 1;
-    }
+// Grid of a window launch: tiles x chunks CTAs. Every CTA does the same work, so the grid should
+// be a whole number of waves: pick the chunk count (>= ~4 waves when the window is big enough)
+// whose tiles x chunks leaves the smallest partial last wave. At least 16 items per warp per
+// chunk keep the XOR tree and the tile fold negligible. Grows the sign partials as needed.
+void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool signs, uint64_t **partials,
+                 uint64_t *partial_chunks, uint64_t *tiles_out, uint64_t *chunk_out, uint64_t *chunks_out) {
     const uint64_t tiles = (pitch + kTileWords - 1) / kTileWords;
     const uint64_t slots = uint64_t(num_sms) * uint64_t(bps);
-    // Every CTA does the same work, so the grid should be a whole number of waves: pick the
-    // chunk count (>= ~4 waves when the window is big enough) whose tiles x chunks leaves the
-    // smallest partial last wave. At least 16 gates per warp per chunk keep the XOR tree and
-    // the tile fold negligible.
-    const uint64_t max_chunks = std::max<uint64_t>(1, ngates / (kWarps * 16));
+    const uint64_t max_chunks = std::max<uint64_t>(1, nitems / (kWarps * 16));
     uint64_t c_min = std::max<uint64_t>(1, (4 * slots + tiles - 1) / tiles);
     if (c_min > max_chunks) c_min = max_chunks;
     uint64_t chunks = c_min;
@@ -274,14 +301,32 @@ void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *ga
         if (eff_time < best * 0.999) { best = eff_time; chunks = c; }
     }
     if (chunks > 65535) chunks = 65535;
-    uint64_t chunk = (ngates + chunks - 1) / chunks;
-    chunks = (ngates + chunk - 1) / chunk;
-    if (kSigns && chunks > 1 && chunks > *partial_chunks) {
+    uint64_t chunk = (nitems + chunks - 1) / chunks;
+    chunks = (nitems + chunk - 1) / chunk;
+    if (signs && chunks > 1 && chunks > *partial_chunks) {
         if (*partials)
             QSR_CUDA(cudaFree(*partials));
         QSR_CUDA(cudaMalloc(partials, chunks * pitch * sizeof(uint64_t)));
         *partial_chunks = chunks;
     }
+    *tiles_out = tiles;
+    *chunk_out = chunk;
+    *chunks_out = chunks;
+}
+
+template <bool kSigns, int U, int B>
+void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates,
+                    uint64_t ngates, int num_sms, cudaStream_t st, uint64_t **partials,
+                    uint64_t *partial_chunks, uint32_t *counters, uint64_t *s) {
+    static int bps = 0;
+    if (bps == 0) {
+        QSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &bps, k_gate_window<kSigns, U, B>, kThreads, 0));
+        if (bps < 1)
+            bps = 1;
+    }
+    uint64_t tiles, chunk, chunks;
+    pick_chunks(pitch, ngates, num_sms, bps, kSigns, partials, partial_chunks, &tiles, &chunk, &chunks);
     dim3 grid{unsigned(tiles), unsigned(chunks)};
     k_gate_window<kSigns, U, B><<<grid, kThreads, 0, st>>>(
         x, z, pitch, gates, uint32_t(ngates), uint32_t(chunk), kSigns ? *partials : nullptr,
@@ -318,6 +363,113 @@ void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uin
                                      partial_chunks, counters, s);
         break;
     }
+}
+
+
+// ---- K1p: two consecutive windows as components ------------------------------------------
+// Two consecutive unitary windows A, B are each a matching on the qubit rows, so their union
+// splits into small paths and cycles. A component of <= kPairRows rows and <= kPairGates gates
+// is one record (pair.hpp): its rows are loaded once, A's gates then B's gates are applied, and
+// the rows are stored once — a row touched by both windows moves once instead of twice. The
+// rows of the component live in the warp's slice of shared memory (lane-private 16-byte slots,
+// conflict-free), so the record's local operand indices are plain shared-memory addresses.
+// Same tile / chunk / sign-fold structure as k_gate_window.
+constexpr int kPairSmemV2 = kWarps * kPairRows * 2 * 32;
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = unsigned(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+constexpr size_t kPairSmemBytes = size_t(kPairSmemV2) * sizeof(V2);
+
+template <bool kSigns, int kMinBlocks>
+__global__ void __launch_bounds__(kThreads, kMinBlocks)
+k_gate_pairs(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
+             const uint64_t *__restrict__ recs, uint32_t nrec, uint32_t chunk,
+             uint64_t *__restrict__ partials, uint32_t *__restrict__ counters,
+             uint64_t *__restrict__ s) {
+    extern __shared__ V2 pair_smem[];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    V2 *slot = pair_smem + warp * (kPairRows * 2 * 32) + lane; // slot[(row * 2 + plane) * 32]
+    const uint64_t j = uint64_t(blockIdx.x) * kTileWords + lane * 2;
+    const bool active = j < pitch;
+    const uint32_t c_begin = blockIdx.y * chunk;
+    const uint32_t c_end = min(c_begin + chunk, nrec);
+    V2 sacc{0, 0};
+    // Lane l < 16 holds word l of the record (one coalesced 128-byte load per record, the next
+    // record's in flight while this one is processed); fields are shuffled out on demand.
+    uint32_t c = c_begin + warp;
+    uint64_t nxt = (c < c_end && lane < uint32_t(kPairRecWords)) ? __ldg(recs + uint64_t(c) * kPairRecWords + lane) : 0;
+    for (; c < c_end; c += kWarps) {
+        const uint64_t cur = nxt;
+        const uint32_t cn = c + kWarps;
+        nxt = (cn < c_end && lane < uint32_t(kPairRecWords)) ? __ldg(recs + uint64_t(cn) * kPairRecWords + lane) : 0;
+        const uint64_t hdr = __shfl_sync(0xFFFFFFFFu, cur, 0);
+        const uint32_t ng = uint32_t(hdr >> 4) & 15u;
+        const uint32_t rmask = uint32_t(hdr >> 8) & 0xFFFFu, wmask = uint32_t(hdr >> 24) & 0xFFFFu;
+        // Row offsets once per record (32 x 32 -> 64-bit multiplies), all loads in flight at
+        // once, straight into shared memory.
+        uint64_t off[kPairRows];
+#pragma unroll
+        for (int k = 0; k < (kPairRows + 1) / 2; ++k) {
+            const uint64_t rw = __shfl_sync(0xFFFFFFFFu, cur, 1 + k);
+            off[2 * k] = uint64_t(uint32_t(rw)) * uint32_t(pitch) + j;
+            off[2 * k + 1] = uint64_t(uint32_t(rw >> 32)) * uint32_t(pitch) + j;
+        }
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < kPairRows; ++i) {
+                if ((rmask >> (2 * i)) & 1u) cp_async16(slot + (2 * i) * 32, x + off[i]);
+                if ((rmask >> (2 * i + 1)) & 1u) cp_async16(slot + (2 * i + 1) * 32, z + off[i]);
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        for (uint32_t gi = 0; gi < ng; ++gi) {
+            const uint64_t gw = __shfl_sync(0xFFFFFFFFu, cur, 5 + gi);
+            const uint32_t a = gate_q0(gw), b = gate_q1(gw), rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
+            V2 X0{0, 0}, Z0{0, 0}, X1{0, 0}, Z1{0, 0};
+            if (rd & 1u) X0 = slot[(a * 2) * 32];
+            if (rd & 2u) Z0 = slot[(a * 2 + 1) * 32];
+            if (rd & 4u) X1 = slot[(b * 2) * 32];
+            if (rd & 8u) Z1 = slot[(b * 2 + 1) * 32];
+            const V2 sg = gate2(gw, X0, Z0, X1, Z1);
+            if (kSigns) sacc ^= sg;
+            if (wr & 1u) slot[(a * 2) * 32] = X0;
+            if (wr & 2u) slot[(a * 2 + 1) * 32] = Z0;
+            if (wr & 4u) slot[(b * 2) * 32] = X1;
+            if (wr & 8u) slot[(b * 2 + 1) * 32] = Z1;
+        }
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < kPairRows; ++i) {
+                if ((wmask >> (2 * i)) & 1u) st2(x + off[i], slot[(2 * i) * 32]);
+                if ((wmask >> (2 * i + 1)) & 1u) st2(z + off[i], slot[(2 * i + 1) * 32]);
+            }
+        }
+    }
+    if constexpr (kSigns) fold_tile_signs(sacc, warp, lane, j, active, pitch, partials, counters, s);
+}
+
+template <bool kSigns>
+void launch_pairs(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *recs, uint64_t nrec, int num_sms,
+                  cudaStream_t st, uint64_t **partials, uint64_t *partial_chunks, uint32_t *counters,
+                  uint64_t *s) {
+    if (nrec == 0) return;
+    constexpr int B = 4;
+    static int bps = 0;
+    if (bps == 0) {
+        QSR_CUDA(cudaFuncSetAttribute(k_gate_pairs<kSigns, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      int(kPairSmemBytes)));
+        QSR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_gate_pairs<kSigns, B>, kThreads,
+                                                               kPairSmemBytes));
+        if (bps < 1) bps = 1;
+    }
+    uint64_t tiles, chunk, chunks;
+    pick_chunks(pitch, nrec, num_sms, bps, kSigns, partials, partial_chunks, &tiles, &chunk, &chunks);
+    dim3 grid{unsigned(tiles), unsigned(chunks)};
+    k_gate_pairs<kSigns, B><<<grid, kThreads, kPairSmemBytes, st>>>(x, z, pitch, recs, uint32_t(nrec), uint32_t(chunk),
+                                                       kSigns ? *partials : nullptr, counters, s);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
 }
 
 
@@ -593,6 +745,16 @@ void launch_gate_window(DeviceTableau &t, const uint64_t *gates, uint64_t ngates
 void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *gates,
                          uint64_t ngates, int num_sms, cudaStream_t st) {
     launch<false>(xf, zf, pitch, gates, ngates, num_sms, st, nullptr, nullptr, nullptr, nullptr);
+}
+
+void launch_gate_pairs(DeviceTableau &t, const uint64_t *recs, uint64_t nrec) {
+    launch_pairs<true>(t.x, t.z, t.cm_pitch, recs, nrec, t.num_sms, t.stream, &t.sign_partials,
+                       &t.sign_partial_chunks, t.tile_counters, t.s);
+}
+
+void launch_frame_pairs(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *recs, uint64_t nrec,
+                        int num_sms, cudaStream_t st) {
+    launch_pairs<false>(xf, zf, pitch, recs, nrec, num_sms, st, nullptr, nullptr, nullptr, nullptr);
 }
 
 } // namespace qsr

@@ -1,0 +1,129 @@
+// Window pairing (pair.hpp).
+#include "pair.hpp"
+
+#include <cstdlib>
+
+#include "device.hpp"
+#include "fuse.hpp"
+#include "host.hpp"
+
+namespace qsr {
+
+namespace {
+inline bool two_rows(uint64_t w) {
+    const uint32_t k = packed_kind(w);
+    return (k >= QSR_CX && k <= QSR_ISWAP) || k == kDevIswapR;
+}
+constexpr uint64_t kQMask = (uint64_t(0xFFFFFF)) | (uint64_t(0xFFFFFF) << 38);
+} // namespace
+
+// Opt-in (QSR_PAIR=1): the records cut DRAM bytes by ~18 % at c5 but the component kernel
+// streams at ~4.9 TB/s vs 6.2 TB/s for the per-window kernel (bytes in flight are bounded by
+// the fixed per-record shared-memory buffers), so it is slower end to end; see DESIGN.md §9.
+bool pairing_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("QSR_PAIR");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+
+Pairer::Pairer(uint32_t rows) : ia_(rows, -1), ib_(rows, -1), stamp_(rows, 0) {}
+
+void Pairer::pair(const uint64_t *a, uint64_t na, const uint64_t *b, uint64_t nb, PairOut &out) {
+    out.records.clear();
+    out.rest_a.clear();
+    out.rest_b.clear();
+    out.record_words = 0;
+    seen_a_.assign(na, 0);
+    seen_b_.assign(nb, 0);
+    for (uint64_t i = 0; i < na; ++i) {
+        ia_[packed_q0(a[i])] = int32_t(i);
+        if (two_rows(a[i])) ia_[packed_q1(a[i])] = int32_t(i);
+    }
+    for (uint64_t i = 0; i < nb; ++i) {
+        ib_[packed_q0(b[i])] = int32_t(i);
+        if (two_rows(b[i])) ib_[packed_q1(b[i])] = int32_t(i);
+    }
+    std::vector<std::pair<int, uint32_t>> stack;
+    std::vector<uint64_t> ga, gb;
+    std::vector<uint32_t> rows;
+    auto walk = [&](int layer, uint32_t start) {
+        ga.clear();
+        gb.clear();
+        rows.clear();
+        if (++cur_ == 0) { // stamp wrap: clear and restart the epoch
+            std::fill(stamp_.begin(), stamp_.end(), 0u);
+            cur_ = 1;
+        }
+        stack.assign(1, {layer, start});
+        (layer ? seen_b_ : seen_a_)[start] = 1;
+        while (!stack.empty()) {
+            const auto [L, g] = stack.back();
+            stack.pop_back();
+            const uint64_t w = L ? b[g] : a[g];
+            (L ? gb : ga).push_back(w);
+            const uint32_t ops[2] = {packed_q0(w), packed_q1(w)};
+            for (int o = 0; o < (two_rows(w) ? 2 : 1); ++o) {
+                const uint32_t r = ops[o];
+                if (stamp_[r] != cur_) {
+                    stamp_[r] = cur_;
+                    rows.push_back(r);
+                }
+                const int32_t other = L ? ia_[r] : ib_[r];
+                if (other >= 0) {
+                    uint8_t &seen = (L ? seen_a_ : seen_b_)[uint32_t(other)];
+                    if (!seen) {
+                        seen = 1;
+                        stack.push_back({1 - L, uint32_t(other)});
+                    }
+                }
+            }
+        }
+        if (rows.size() > size_t(kPairRows) || ga.size() + gb.size() > size_t(kPairGates)) {
+            out.rest_a.insert(out.rest_a.end(), ga.begin(), ga.end());
+            out.rest_b.insert(out.rest_b.end(), gb.begin(), gb.end());
+            return;
+        }
+        auto local = [&](uint32_t r) {
+            uint32_t i = 0;
+            while (rows[i] != r) ++i;
+            return i;
+        };
+        uint64_t rec[kPairRecWords] = {};
+        uint32_t rmask = 0, wmask = 0, ng = 0;
+        auto add = [&](uint64_t w) {
+            const uint32_t l0 = local(packed_q0(w));
+            const bool two = two_rows(w);
+            const uint32_t l1 = two ? local(packed_q1(w)) : 0;
+            const uint32_t rd = packed_reads(w), wr = packed_writes(w);
+            rmask |= (rd & 3u) << (2 * l0);
+            wmask |= (wr & 3u) << (2 * l0);
+            if (two) {
+                rmask |= ((rd >> 2) & 3u) << (2 * l1);
+                wmask |= ((wr >> 2) & 3u) << (2 * l1);
+            }
+            rec[5 + ng++] = (w & ~kQMask) | uint64_t(l0) | (uint64_t(l1) << 38);
+        };
+        for (uint64_t w : ga) add(w); // window A's gates first: the original order per row
+        for (uint64_t w : gb) add(w);
+        for (size_t i = 0; i < rows.size(); ++i) rec[1 + i / 2] |= uint64_t(rows[i]) << (32 * (i % 2));
+        rec[0] = uint64_t(rows.size()) | (uint64_t(ng) << 4) | (uint64_t(rmask) << 8) | (uint64_t(wmask) << 24);
+        out.records.insert(out.records.end(), rec, rec + kPairRecWords);
+        out.record_words += uint64_t(__builtin_popcount(rmask) + __builtin_popcount(wmask));
+    };
+    for (uint64_t i = 0; i < na; ++i)
+        if (!seen_a_[i]) walk(0, uint32_t(i));
+    for (uint64_t i = 0; i < nb; ++i)
+        if (!seen_b_[i]) walk(1, uint32_t(i));
+    for (uint64_t i = 0; i < na; ++i) {
+        ia_[packed_q0(a[i])] = -1;
+        if (two_rows(a[i])) ia_[packed_q1(a[i])] = -1;
+    }
+    for (uint64_t i = 0; i < nb; ++i) {
+        ib_[packed_q0(b[i])] = -1;
+        if (two_rows(b[i])) ib_[packed_q1(b[i])] = -1;
+    }
+}
+
+} // namespace qsr
