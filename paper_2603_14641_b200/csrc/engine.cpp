@@ -91,6 +91,14 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
             held = s0;
             return;
         }
+        if (!pair_windows_of(s0 - held, out.size() - s0)) { // the held one goes alone, hold this one
+            const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
+            out.resize(s0);
+            push_window(0, gate_words(out.data() + held, s0 - held));
+            out.insert(out.end(), B.begin(), B.end());
+            held = s0;
+            return;
+        }
         const std::vector<uint64_t> A(out.begin() + long(held), out.begin() + long(s0));
         const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
         out.resize(held);

@@ -374,7 +374,7 @@ void launch(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates, uin
 // rows of the component live in the warp's slice of shared memory (lane-private 16-byte slots,
 // conflict-free), so the record's local operand indices are plain shared-memory addresses.
 // Same tile / chunk / sign-fold structure as k_gate_window.
-constexpr int kPairSmemV2 = kWarps * kPairRows * 2 * 32;
+constexpr int kPairSmemV2 = kWarps * 2 * kPairRows * 2 * 32; // two record buffers per warp
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
     const unsigned sa = unsigned(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
@@ -389,62 +389,77 @@ k_gate_pairs(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
              uint64_t *__restrict__ s) {
     extern __shared__ V2 pair_smem[];
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    V2 *slot = pair_smem + warp * (kPairRows * 2 * 32) + lane; // slot[(row * 2 + plane) * 32]
+    // Two record buffers per warp: the next record's rows load while this one is computed.
+    V2 *const buf0 = pair_smem + warp * (2 * kPairRows * 2 * 32) + lane; // [(row * 2 + plane) * 32]
+    V2 *const buf1 = buf0 + kPairRows * 2 * 32;
     const uint64_t j = uint64_t(blockIdx.x) * kTileWords + lane * 2;
     const bool active = j < pitch;
     const uint32_t c_begin = blockIdx.y * chunk;
     const uint32_t c_end = min(c_begin + chunk, nrec);
     V2 sacc{0, 0};
-    // Lane l < 16 holds word l of the record (one coalesced 128-byte load per record, the next
-    // record's in flight while this one is processed); fields are shuffled out on demand.
-    uint32_t c = c_begin + warp;
-    uint64_t nxt = (c < c_end && lane < uint32_t(kPairRecWords)) ? __ldg(recs + uint64_t(c) * kPairRecWords + lane) : 0;
-    for (; c < c_end; c += kWarps) {
-        const uint64_t cur = nxt;
-        const uint32_t cn = c + kWarps;
-        nxt = (cn < c_end && lane < uint32_t(kPairRecWords)) ? __ldg(recs + uint64_t(cn) * kPairRecWords + lane) : 0;
-        const uint64_t hdr = __shfl_sync(0xFFFFFFFFu, cur, 0);
-        const uint32_t ng = uint32_t(hdr >> 4) & 15u;
-        const uint32_t rmask = uint32_t(hdr >> 8) & 0xFFFFu, wmask = uint32_t(hdr >> 24) & 0xFFFFu;
-        // Row offsets once per record (32 x 32 -> 64-bit multiplies), all loads in flight at
-        // once, straight into shared memory.
-        uint64_t off[kPairRows];
+    // Lane l < 16 holds word l of a record (one coalesced 128-byte load); fields are shuffled
+    // out on demand.
+    auto fetch = [&](uint32_t cc) -> uint64_t {
+        return (cc < c_end && lane < uint32_t(kPairRecWords)) ? __ldg(recs + uint64_t(cc) * kPairRecWords + lane) : 0;
+    };
+    auto offsets = [&](uint64_t rec, uint64_t (&off)[kPairRows]) {
 #pragma unroll
         for (int k = 0; k < (kPairRows + 1) / 2; ++k) {
-            const uint64_t rw = __shfl_sync(0xFFFFFFFFu, cur, 1 + k);
+            const uint64_t rw = __shfl_sync(0xFFFFFFFFu, rec, 1 + k);
             off[2 * k] = uint64_t(uint32_t(rw)) * uint32_t(pitch) + j;
-            off[2 * k + 1] = uint64_t(uint32_t(rw >> 32)) * uint32_t(pitch) + j;
+            if (2 * k + 1 < kPairRows) off[2 * k + 1] = uint64_t(uint32_t(rw >> 32)) * uint32_t(pitch) + j;
         }
+    };
+    auto issue = [&](uint64_t rec, V2 *buf) { // the record's read planes -> buf (cp.async)
+        const uint32_t rmask = uint32_t(__shfl_sync(0xFFFFFFFFu, rec, 0) >> 8) & 0xFFFFu;
+        uint64_t off[kPairRows];
+        offsets(rec, off);
         if (active) {
 #pragma unroll
             for (int i = 0; i < kPairRows; ++i) {
-                if ((rmask >> (2 * i)) & 1u) cp_async16(slot + (2 * i) * 32, x + off[i]);
-                if ((rmask >> (2 * i + 1)) & 1u) cp_async16(slot + (2 * i + 1) * 32, z + off[i]);
+                if ((rmask >> (2 * i)) & 1u) cp_async16(buf + (2 * i) * 32, x + off[i]);
+                if ((rmask >> (2 * i + 1)) & 1u) cp_async16(buf + (2 * i + 1) * 32, z + off[i]);
             }
         }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    uint32_t c = c_begin + warp;
+    uint64_t cur = fetch(c), nxt = fetch(c + kWarps);
+    if (c < c_end) issue(cur, buf0);
+    for (uint32_t it = 0; c < c_end; c += kWarps, ++it) {
+        V2 *const b = (it & 1) ? buf1 : buf0;
+        const uint64_t nn = fetch(c + 2 * kWarps);
+        if (c + kWarps < c_end) issue(nxt, (it & 1) ? buf0 : buf1);
+        else asm volatile("cp.async.commit_group;\n" ::: "memory");
+        asm volatile("cp.async.wait_group 1;\n" ::: "memory"); // this record's group is complete
+        const uint64_t hdr = __shfl_sync(0xFFFFFFFFu, cur, 0);
+        const uint32_t ng = uint32_t(hdr >> 4) & 15u, wmask = uint32_t(hdr >> 24) & 0xFFFFu;
         for (uint32_t gi = 0; gi < ng; ++gi) {
             const uint64_t gw = __shfl_sync(0xFFFFFFFFu, cur, 5 + gi);
-            const uint32_t a = gate_q0(gw), b = gate_q1(gw), rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
+            const uint32_t a = gate_q0(gw), bq = gate_q1(gw), rd = gate_reads(gw, kSigns), wr = gate_writes(gw);
             V2 X0{0, 0}, Z0{0, 0}, X1{0, 0}, Z1{0, 0};
-            if (rd & 1u) X0 = slot[(a * 2) * 32];
-            if (rd & 2u) Z0 = slot[(a * 2 + 1) * 32];
-            if (rd & 4u) X1 = slot[(b * 2) * 32];
-            if (rd & 8u) Z1 = slot[(b * 2 + 1) * 32];
+            if (rd & 1u) X0 = b[(a * 2) * 32];
+            if (rd & 2u) Z0 = b[(a * 2 + 1) * 32];
+            if (rd & 4u) X1 = b[(bq * 2) * 32];
+            if (rd & 8u) Z1 = b[(bq * 2 + 1) * 32];
             const V2 sg = gate2(gw, X0, Z0, X1, Z1);
             if (kSigns) sacc ^= sg;
-            if (wr & 1u) slot[(a * 2) * 32] = X0;
-            if (wr & 2u) slot[(a * 2 + 1) * 32] = Z0;
-            if (wr & 4u) slot[(b * 2) * 32] = X1;
-            if (wr & 8u) slot[(b * 2 + 1) * 32] = Z1;
+            if (wr & 1u) b[(a * 2) * 32] = X0;
+            if (wr & 2u) b[(a * 2 + 1) * 32] = Z0;
+            if (wr & 4u) b[(bq * 2) * 32] = X1;
+            if (wr & 8u) b[(bq * 2 + 1) * 32] = Z1;
         }
+        uint64_t off[kPairRows];
+        offsets(cur, off); // all lanes (the shuffles need the full warp)
         if (active) {
 #pragma unroll
             for (int i = 0; i < kPairRows; ++i) {
-                if ((wmask >> (2 * i)) & 1u) st2(x + off[i], slot[(2 * i) * 32]);
-                if ((wmask >> (2 * i + 1)) & 1u) st2(z + off[i], slot[(2 * i + 1) * 32]);
+                if ((wmask >> (2 * i)) & 1u) st2(x + off[i], b[(2 * i) * 32]);
+                if ((wmask >> (2 * i + 1)) & 1u) st2(z + off[i], b[(2 * i + 1) * 32]);
             }
         }
+        cur = nxt;
+        nxt = nn;
     }
     if constexpr (kSigns) fold_tile_signs(sacc, warp, lane, j, active, pitch, partials, counters, s);
 }
@@ -454,7 +469,7 @@ void launch_pairs(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *recs
                   cudaStream_t st, uint64_t **partials, uint64_t *partial_chunks, uint32_t *counters,
                   uint64_t *s) {
     if (nrec == 0) return;
-    constexpr int B = 4;
+    constexpr int B = 2;
     static int bps = 0;
     if (bps == 0) {
         QSR_CUDA(cudaFuncSetAttribute(k_gate_pairs<kSigns, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,

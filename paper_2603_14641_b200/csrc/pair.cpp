@@ -17,15 +17,20 @@ inline bool two_rows(uint64_t w) {
 constexpr uint64_t kQMask = (uint64_t(0xFFFFFF)) | (uint64_t(0xFFFFFF) << 38);
 } // namespace
 
-// Opt-in (QSR_PAIR=1): the records cut DRAM bytes by ~18 % at c5 but the component kernel
-// streams at ~4.9 TB/s vs 6.2 TB/s for the per-window kernel (bytes in flight are bounded by
-// the fixed per-record shared-memory buffers), so it is slower end to end; see DESIGN.md §9.
-bool pairing_enabled() {
-    static const bool on = [] {
+// Opt-in. QSR_PAIR=1 pairs windows of every size (parity tests), QSR_PAIR=2 only windows of
+// >= kPairMinGates gates. Measured at c5: 18 % fewer gate-phase bytes, equal
+// time — back-to-back per-window launches already reuse the previous window's rows from L2.
+int pairing_mode() {
+    static const int mode = [] {
         const char *e = getenv("QSR_PAIR");
-        return e && e[0] == '1';
+        return e ? (e[0] == '1' ? 2 : e[0] == '2' ? 1 : 0) : 0;
     }();
-    return on;
+    return mode;
+}
+bool pairing_enabled() { return pairing_mode() != 0; }
+bool pair_windows_of(uint64_t na, uint64_t nb) {
+    const int m = pairing_mode();
+    return m == 2 || (m == 1 && na >= kPairMinGates && nb >= kPairMinGates);
 }
 
 Pairer::Pairer(uint32_t rows) : ia_(rows, -1), ib_(rows, -1), stamp_(rows, 0) {}

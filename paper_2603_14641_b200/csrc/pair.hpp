@@ -41,7 +41,11 @@ class Pairer {
     std::vector<uint8_t> seen_a_, seen_b_;
 };
 
-// QSR_PAIR=1 enables window pairing (opt-in; measured slower than per-window launches, pair.cpp).
+// Pairing pays where windows are big enough for the saved bytes to outweigh the extra launches
+// of the remainder windows (c5: ~56 k gates per fused window; c2's ~14 k-gate windows do not).
+constexpr uint64_t kPairMinGates = 16384;
+// Opt-in: QSR_PAIR=1 pairs windows of every size (tests), QSR_PAIR=2 windows >= kPairMinGates.
 bool pairing_enabled();
+bool pair_windows_of(uint64_t na, uint64_t nb);
 
 } // namespace qsr

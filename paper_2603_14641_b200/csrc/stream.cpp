@@ -26,6 +26,7 @@
 
 #include "engine.hpp"
 #include "fuse.hpp"
+#include "pair.hpp"
 
 namespace qsr {
 
@@ -147,10 +148,15 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                 to_events.emplace_back(ra, rb);
                 in_run = false;
             };
-            // Stage one device window through the pinned ring (async H2D) and launch it.
-            auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
+            // Stage one device window through the pinned ring (async H2D) and launch it. The device
+            // gate buffer is used as a ring too: copies and kernels share t.stream, so a copy
+            // into a recycled region runs after every kernel that read it.
+            // kind 1 = pair records (pair.hpp), 16-byte aligned.
+            auto launch_staged = [&](const uint64_t *src, uint64_t cnt, int kind = 0) {
                 const auto ts = clk::now();
                 open_run();
+                if (kind == 1 && (dev_off & 1)) ++dev_off;
+                if (dev_off + cnt > t.gate_buf_cap) dev_off = 0;
                 for (uint64_t i = 0; i < cnt;) {
                     if (ring.fill == kRingGates) {
                         QSR_CUDA(cudaEventRecord(ring.done[ring.cur], t.stream));
@@ -171,10 +177,43 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                     ring.fill += take;
                     i += take;
                 }
-                launch_gate_window(t, d_gates + dev_off, cnt);
+                if (kind == 1) launch_gate_pairs(t, d_gates + dev_off, cnt / kPairRecWords);
+                else launch_gate_window(t, d_gates + dev_off, cnt);
                 ++rt.gate_launches;
                 dev_off += cnt;
                 t_stage += since(ts);
+            };
+            // Window pairing (pair.hpp): each finished unitary window is held until the next.
+            Pairer pairer(fuse && pairing_enabled() && !gate_segment_enabled() ? n : 0);
+            const bool pairing = fuse && pairing_enabled() && !gate_segment_enabled();
+            std::vector<uint64_t> held;
+            PairOut po;
+            auto unitary_window = [&](std::vector<uint64_t> &w) {
+                if (w.empty()) return;
+                if (!pairing) {
+                    launch_staged(w.data(), w.size());
+                    return;
+                }
+                if (held.empty()) {
+                    held.swap(w);
+                    return;
+                }
+                if (!pair_windows_of(held.size(), w.size())) {
+                    launch_staged(held.data(), held.size());
+                    held.swap(w);
+                    return;
+                }
+                const auto tf = clk::now();
+                pairer.pair(held.data(), held.size(), w.data(), w.size(), po);
+                t_fuse += since(tf);
+                if (!po.records.empty()) launch_staged(po.records.data(), po.records.size(), 1);
+                if (!po.rest_a.empty()) launch_staged(po.rest_a.data(), po.rest_a.size());
+                if (!po.rest_b.empty()) launch_staged(po.rest_b.data(), po.rest_b.size());
+                held.clear();
+            };
+            auto flush_held = [&] {
+                if (!held.empty()) launch_staged(held.data(), held.size());
+                held.clear();
             };
             // CM rows back to logical order (before a measurement window and at the end).
             auto unpermute = [&] {
@@ -209,7 +248,7 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                             dev.clear();
                             fuser.unitary(b.data(), cnt, dev);
                             t_fuse += since(tf);
-                            if (!dev.empty()) launch_staged(dev.data(), dev.size());
+                            unitary_window(dev);
                         } else {
                             launch_staged(b.data(), cnt);
                         }
@@ -217,7 +256,8 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                         if (fuse) {
                             dev.clear();
                             fuser.flush(dev);
-                            if (!dev.empty()) launch_staged(dev.data(), dev.size());
+                            unitary_window(dev);
+                            flush_held();
                             close_run();
                             unpermute();
                         }
@@ -247,10 +287,9 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             if (!stop && fuse) {
                 dev.clear();
                 fuser.flush(dev);
-                if (!dev.empty()) {
-                    launch_staged(dev.data(), dev.size());
-                    close_run();
-                }
+                unitary_window(dev);
+                flush_held();
+                close_run();
                 unpermute();
                 QSR_CUDA(cudaStreamSynchronize(t.stream));
             }
