@@ -879,24 +879,26 @@ struct qsr_frames {
     uint64_t *xs = nullptr, *zs = nullptr; // slab-major scratch planes of the segment kernel
     uint32_t *d_idx = nullptr;   // qubits + rows staging
     uint64_t idx_cap = 0;
+    uint64_t plane_bytes = 0; // xf / zf come from the plane cache (no cudaMalloc per sample())
     ~qsr_frames() {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        for (void *p : {(void *)xf, (void *)zf, (void *)rec, (void *)gate_buf, (void *)d_idx, (void *)seg_bar,
-                        (void *)xs, (void *)zs})
+        plane_cache().release(device, plane_bytes, xf);
+        plane_cache().release(device, plane_bytes, zf);
+        if (rec) plane_cache().release(device, rec_cap * pitch * 8, rec);
+        for (void *p : {(void *)gate_buf, (void *)d_idx, (void *)seg_bar, (void *)xs, (void *)zs})
             if (p) cudaFree(p);
         if (stream) cudaStreamDestroy(stream);
     }
     void ensure_rows(uint64_t rows) {
         if (rows <= rec_cap) return;
         uint64_t cap = std::max<uint64_t>(rows, std::min<uint64_t>(n, std::max<uint64_t>(rec_cap * 2, 64)));
-        uint64_t *nr = nullptr;
-        QSR_CUDA(cudaMalloc(&nr, cap * pitch * 8));
+        uint64_t *nr = static_cast<uint64_t *>(plane_cache().acquire(device, cap * pitch * 8));
         QSR_CUDA(cudaMemsetAsync(nr, 0, cap * pitch * 8, stream));
         if (rec) {
             QSR_CUDA(cudaMemcpyAsync(nr, rec, rec_cap * pitch * 8, cudaMemcpyDeviceToDevice, stream));
             QSR_CUDA(cudaStreamSynchronize(stream));
-            QSR_CUDA(cudaFree(rec));
+            plane_cache().release(device, rec_cap * pitch * 8, rec);
         }
         rec = nr;
         rec_cap = cap;
@@ -933,8 +935,9 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     if (f->j0 + f->kf > (shots + 63) / 64) fail(QSR_INVALID_ARGUMENT, "init_frames: shot slice out of range");
     f->pitch = round_up(f->kf, 16);
     uint64_t words = std::max<uint64_t>(n, 1) * f->pitch;
-    QSR_CUDA(cudaMalloc(&f->xf, words * 8));
-    QSR_CUDA(cudaMalloc(&f->zf, words * 8));
+    f->plane_bytes = words * 8;
+    f->xf = static_cast<uint64_t *>(plane_cache().acquire(device, words * 8));
+    f->zf = static_cast<uint64_t *>(plane_cache().acquire(device, words * 8));
     QSR_CUDA(cudaMemsetAsync(f->xf, 0, words * 8, f->stream));
     QSR_CUDA(cudaMemsetAsync(f->zf, 0, words * 8, f->stream));
     f->row_of.assign(n, -1);
@@ -1081,8 +1084,19 @@ qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *mea
         if (measured) std::memcpy(measured, f->measured.data(), f->measured.size() * 4);
         if (words && !f->measured.empty()) {
             QSR_CUDA(cudaSetDevice(f->device));
-            QSR_CUDA(cudaMemcpy2DAsync(words, f->kf * 8, f->rec, f->pitch * 8, f->kf * 8,
-                                       f->measured.size(), cudaMemcpyDeviceToHost, f->stream));
+            const uint64_t rows = f->measured.size();
+            if (f->pitch == f->kf) {
+                QSR_CUDA(cudaMemcpyAsync(words, f->rec, rows * f->kf * 8, cudaMemcpyDeviceToHost, f->stream));
+            } else {
+                // Strip the row padding on the device (a pitched copy into pageable host memory
+                // runs at a fraction of PCIe bandwidth), then one linear download.
+                uint64_t *packed = nullptr;
+                QSR_CUDA(cudaMallocAsync(&packed, rows * f->kf * 8, f->stream));
+                QSR_CUDA(cudaMemcpy2DAsync(packed, f->kf * 8, f->rec, f->pitch * 8, f->kf * 8, rows,
+                                           cudaMemcpyDeviceToDevice, f->stream));
+                QSR_CUDA(cudaMemcpyAsync(words, packed, rows * f->kf * 8, cudaMemcpyDeviceToHost, f->stream));
+                QSR_CUDA(cudaFreeAsync(packed, f->stream));
+            }
             QSR_CUDA(cudaStreamSynchronize(f->stream));
         }
     });
@@ -1135,6 +1149,14 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         auto f = [&] {
             TraceScope tr("  make_frames");
             auto ff = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
+            // One record allocation: the distinct measured qubits of the schedule.
+            std::vector<uint8_t> seen(c->num_qubits, 0);
+            uint64_t distinct = 0;
+            for (uint64_t w = 0; w < sched.num_windows(); ++w)
+                if (sched.is_meas[w])
+                    for (uint64_t i = sched.offsets[w]; i < sched.offsets[w + 1]; ++i)
+                        if (!seen[sched.gates[i].q0]) { seen[sched.gates[i].q0] = 1; ++distinct; }
+            if (distinct) ff->ensure_rows(distinct);
             QSR_CUDA(cudaStreamSynchronize(ff->stream));
             return ff;
         }();

@@ -26,5 +26,6 @@ for i in range(runs):
     gc.collect()
     print(f"  (record freed in {(time.perf_counter() - t1) * 1e3:.1f} ms)", flush=True)
     print(f"run {i}: sample {dt * 1e3:.1f} ms (reference shot {rep.total_seconds * 1e3:.1f} ms), "
-          f"{len(c)} gates x {shots} shots = {len(c) * shots / dt / 1e9:.2f} G gate-shots/s, "
-          f"", flush=True)
+          f"{len(c)} gates x {shots} shots = {len(c) * shots / dt / 1e9:.2f} G gate-shots/s; "
+          f"reference-shot device phases: to {rep.timers.to_seconds * 1e3:.1f} t {rep.timers.t_seconds * 1e3:.1f} "
+          f"ge {rep.timers.ge_seconds * 1e3:.1f} cmp {rep.timers.cmp_seconds * 1e3:.1f} ms", flush=True)
