@@ -950,11 +950,11 @@ void frames_window(qsr_frames &f, const uint64_t *d_gates, uint64_t ng) {
     launch_frame_window(f.xf, f.zf, f.pitch, d_gates, ng, f.num_sms, f.stream);
 }
 
-void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t seed,
-                    uint32_t epoch) {
+extern "C++" template <typename QubitOf>
+void frames_measure_q(qsr_frames &f, QubitOf qubit_of, uint64_t ng, uint64_t seed, uint32_t epoch) {
     std::vector<uint32_t> idx(2 * ng);
     for (uint64_t i = 0; i < ng; ++i) {
-        uint32_t q = gates[i].q0;
+        uint32_t q = qubit_of(i);
         if (f.row_of[q] < 0) {
             f.row_of[q] = int64_t(f.measured.size());
             f.measured.push_back(q);
@@ -968,6 +968,10 @@ void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t 
     launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.j0, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
                           seed, epoch, f.wbits, f.stream);
     QSR_CUDA(cudaStreamSynchronize(f.stream)); // idx staging reused next call
+}
+
+void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t seed, uint32_t epoch) {
+    frames_measure_q(f, [&](uint64_t i) { return gates[i].q0; }, ng, seed, epoch);
 }
 
 void validate_frames_window(const qsr_frames &f, const qsr_gate *gates, uint64_t ng, bool meas,
@@ -1079,6 +1083,7 @@ qsr_status qsr_measure_sample(qsr_frames *f, const qsr_gate *gates, uint64_t ng,
 qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *measured,
                              uint64_t *words) {
     return guard([&] {
+        TraceScope tr(words ? "frames_record (download)" : "frames_record (size)");
         REQUIRE_PTR(f); REQUIRE_PTR(nrows);
         *nrows = f->measured.size();
         if (measured) std::memcpy(measured, f->measured.data(), f->measured.size() * 4);
@@ -1102,7 +1107,10 @@ qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *mea
     });
 }
 
-void qsr_frames_destroy(qsr_frames *f) { delete f; }
+void qsr_frames_destroy(qsr_frames *f) {
+    TraceScope tr("frames_destroy");
+    delete f;
+}
 
 static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t seed, int device, int world,
                        int rank, qsr_frames **out, qsr_run_report *report, unsigned wbits = 64) {
@@ -1117,14 +1125,12 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         const uint64_t w0 = kf_all * uint64_t(rank) / uint64_t(world);
         const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
         TraceScope tr_all("sample");
-        Schedule sched = [&] {
-            TraceScope tr("  schedule_windows");
-            return schedule_windows(*c, QSR_SAMPLING);
-        }();
-        // Reference shot (frames.hpp:167): the full single-shot pipeline on the device.
+        // Reference shot (frames.hpp:167): the full single-shot pipeline on the device, on the
+        // O(G) plan scattered straight into packed device gates (schedule_windows' windows; the
+        // sampling mode is only a tag, schedule.hpp:37-42). The frames reuse the same windows.
         TraceScope tr_ref("  reference shot");
         DeviceTableau t(c->num_qubits, device);
-        auto ds = upload_schedule(t.n, sched, device, t.stream);
+        auto ds = upload_circuit(*c, device, t.stream, /*fuse=*/false);
         const uint64_t nm = ds->measure_count;
         qsr_record_entry *d_rec = nullptr;
         QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
@@ -1152,10 +1158,9 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
             // One record allocation: the distinct measured qubits of the schedule.
             std::vector<uint8_t> seen(c->num_qubits, 0);
             uint64_t distinct = 0;
-            for (uint64_t w = 0; w < sched.num_windows(); ++w)
-                if (sched.is_meas[w])
-                    for (uint64_t i = sched.offsets[w]; i < sched.offsets[w + 1]; ++i)
-                        if (!seen[sched.gates[i].q0]) { seen[sched.gates[i].q0] = 1; ++distinct; }
+            for (const auto &mq : ds->mqubits)
+                for (uint32_t q : mq)
+                    if (!seen[q]) { seen[q] = 1; ++distinct; }
             if (distinct) ff->ensure_rows(distinct);
             QSR_CUDA(cudaStreamSynchronize(ff->stream));
             return ff;
@@ -1167,7 +1172,8 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         for (uint64_t w = 0; w < W;) {
             const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
             if (ds->is_meas[w]) {
-                frames_measure(*f, sched.gates.data() + b, e - b, seed, epoch++);
+                const auto &mq = ds->mqubits[w];
+                frames_measure_q(*f, [&](uint64_t i) { return mq[i]; }, e - b, seed, epoch++);
                 ++w;
                 continue;
             }
