@@ -776,6 +776,15 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
 }
 
 // ---- resident engine --------------------------------------------------------------
+// QSR_GRAPHS=0 keeps the resident engine on per-window launches.
+static bool graphs_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("QSR_GRAPHS");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 struct qsr_engine {
     std::unique_ptr<DeviceTableau> t;
     std::unique_ptr<DeviceSchedule> ds;
@@ -795,6 +804,7 @@ qsr_status qsr_engine_create(const qsr_circuit *c, const qsr_schedule *s, int de
         e->t = std::make_unique<DeviceTableau>(c->num_qubits, device);
         e->ds = s ? upload_schedule(e->t->n, *s, device, e->t->stream, true)
                   : upload_circuit(*c, device, e->t->stream, true);
+        e->ds->use_graphs = graphs_enabled();
         QSR_CUDA(cudaMalloc(&e->d_rec,
                             std::max<uint64_t>(e->ds->measure_count, 1) * sizeof(qsr_record_entry)));
         *out = e.release();

@@ -274,11 +274,8 @@ void upload_offsets(DeviceSchedule &ds, cudaStream_t st) {
     QSR_CUDA(cudaStreamSynchronize(st));
 }
 
-uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1,
-                             double *bytes) {
-    if (w1 <= w0) return 0;
-    if (bytes && ds.wwords.size() >= w1)
-        for (uint64_t w = w0; w < w1; ++w) *bytes += (8.0 * ds.wwords[w] + 16.0) * 2.0 * double(t.kg);
+namespace {
+uint64_t launch_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1) {
     if (gate_segment_enabled() && w1 - w0 >= 2) {
         launch_gate_segment(t, ds.d_gates, ds.d_offsets + w0, uint32_t(w1 - w0));
         return 1;
@@ -288,9 +285,46 @@ uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_
         if (w < ds.wkind.size() && ds.wkind[w] == 1) {
             const uint64_t b = ds.offsets[w] + (ds.offsets[w] & 1); // a pad word keeps 16-B alignment
             launch_gate_pairs(t, ds.d_gates + b, (ds.offsets[w + 1] - b) / kPairRecWords);
-        } else
+        } else {
             launch_gate_window(t, ds.d_gates + ds.offsets[w], cnt);
+        }
     }
+    return w1 - w0;
+}
+} // namespace
+
+uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1,
+                             double *bytes) {
+    if (w1 <= w0) return 0;
+    if (bytes && ds.wwords.size() >= w1)
+        for (uint64_t w = w0; w < w1; ++w) *bytes += (8.0 * ds.wwords[w] + 16.0) * 2.0 * double(t.kg);
+    if (!ds.use_graphs || ds.runs == 0 || w1 - w0 < 2) return launch_unitary_windows(t, ds, w0, w1);
+    for (const auto &g : ds.graphs)
+        if (g.w0 == w0 && g.w1 == w1 && g.x == t.x && g.z == t.z) {
+            QSR_CUDA(cudaGraphLaunch(g.exec, t.stream));
+            count_launch(g.kernels);
+            return w1 - w0;
+        }
+    // Capture (kernels are recorded, not run), instantiate, then replay.
+    const uint64_t l0 = g_launches;
+    cudaGraph_t graph = nullptr;
+    QSR_CUDA(cudaStreamBeginCapture(t.stream, cudaStreamCaptureModeThreadLocal));
+    try {
+        launch_unitary_windows(t, ds, w0, w1);
+    } catch (...) {
+        cudaStreamEndCapture(t.stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    QSR_CUDA(cudaStreamEndCapture(t.stream, &graph));
+    const uint64_t kernels = g_launches - l0;
+    g_launches = l0;
+    cudaGraphExec_t exec = nullptr;
+    QSR_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    QSR_CUDA(cudaGraphDestroy(graph));
+    ds.graphs.push_back({w0, w1, t.x, t.z, exec, kernels});
+    QSR_CUDA(cudaGraphLaunch(exec, t.stream));
+    count_launch(kernels);
     return w1 - w0;
 }
 
@@ -345,6 +379,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
     for (auto e : {e_start, e_end, a, b}) cudaEventDestroy(e);
     if (read_error_flag(t))
         fail(QSR_LOGIC_ERROR, "product of anti-commuting rows (corrupted tableau)");
+    ++const_cast<DeviceSchedule &>(ds).runs;
 }
 
 void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,

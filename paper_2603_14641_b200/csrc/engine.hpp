@@ -27,8 +27,21 @@ struct DeviceSchedule {
     // rows with the logical -> physical map at d_perms + perm_at[w].
     std::vector<int64_t> perm_at;
     uint32_t *d_perms = nullptr;
+    // Resident engines replay each maximal unitary run as a CUDA graph (captured on the second
+    // run, when every lazily sized buffer exists). Keyed by the run and the plane pointers the
+    // kernels were captured with (x / x2 trade places across runs with an odd swap count).
+    bool use_graphs = false;
+    uint64_t runs = 0;
+    struct Graph {
+        uint64_t w0, w1;
+        const uint64_t *x, *z;
+        cudaGraphExec_t exec;
+        uint64_t kernels;
+    };
+    mutable std::vector<Graph> graphs;
     ~DeviceSchedule() {
         cudaSetDevice(device);
+        for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
         for (void *p : {(void *)d_gates, (void *)d_offsets, (void *)d_perms})
             if (p) cudaFree(p);
     }
