@@ -788,14 +788,24 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         __syncthreads();
         const uint64_t i = w0 + 2 * lane;
         const bool act = i < pitch;
+        // Memberships of the next row group are loaded one iteration ahead (their L2 round
+        // trip overlaps this group's loads and table lookups).
+        uint32_t Mn[kARows];
+        {
+            const uint64_t b0 = r_begin + uint64_t(warp) * kARows;
+#pragma unroll
+            for (int q = 0; q < kARows; ++q) Mn[q] = b0 + q < r_end ? member[b0 + q] : 0u;
+        }
         for (uint64_t base = r_begin + uint64_t(warp) * kARows; base < r_end;
              base += uint64_t(kAWarps) * kARows) {
             uint32_t M[kARows];
             uint32_t U = 0;
+            const uint64_t nb = base + uint64_t(kAWarps) * kARows;
 #pragma unroll
             for (int q = 0; q < kARows; ++q) {
-                M[q] = base + q < r_end ? member[base + q] : 0u;
+                M[q] = Mn[q];
                 U |= M[q];
+                Mn[q] = nb + q < r_end ? member[nb + q] : 0u;
             }
             if (U == 0) continue;
             ulonglong2 x0[kARows], z0[kARows], dx[kARows], dz[kARows];
