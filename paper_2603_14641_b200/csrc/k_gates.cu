@@ -289,7 +289,11 @@ void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool sig
                  uint64_t *partial_chunks, uint64_t *tiles_out, uint64_t *chunk_out, uint64_t *chunks_out) {
     const uint64_t tiles = (pitch + kTileWords - 1) / kTileWords;
     const uint64_t slots = uint64_t(num_sms) * uint64_t(bps);
-    const uint64_t max_chunks = std::max<uint64_t>(1, nitems / (kWarps * 16));
+    static const uint64_t per_warp = [] { // QSR_GATE_MINPW: tuning knob (default 16)
+        const char *e = getenv("QSR_GATE_MINPW");
+        return e ? std::max<uint64_t>(1, uint64_t(atoll(e))) : uint64_t(16);
+    }();
+    const uint64_t max_chunks = std::max<uint64_t>(1, nitems / (kWarps * per_warp));
     uint64_t c_min = std::max<uint64_t>(1, (4 * slots + tiles - 1) / tiles);
     if (c_min > max_chunks) c_min = max_chunks;
     uint64_t chunks = c_min;
