@@ -81,8 +81,12 @@ struct Circuit {
     uint32_t num_qubits = 0;
     std::vector<qsr_gate> gates;
     uint32_t num_clbits = 0; // classical bits named in the source (labels only, circuit.hpp:103-105)
-    uint64_t measure_count() const;
+    uint64_t measure_count() const; // cached (keyed by the gate vector's size and storage)
     void check_valid() const; // circuit.hpp:108-115
+
+  private:
+    mutable uint64_t cached_measures_ = 0, cached_measures_for_ = ~uint64_t(0);
+    mutable const qsr_gate *cached_data_ = nullptr;
 };
 
 // generate_random (circuit.hpp:132-173): same Philox stream, same draw order.

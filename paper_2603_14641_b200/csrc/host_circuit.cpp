@@ -74,9 +74,21 @@ uint64_t philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t inde
 }
 
 uint64_t Circuit::measure_count() const {
+    // Cached: a c5 circuit is 1.5 GB of gates, and the count is asked for by every run.
+    if (cached_measures_for_ == gates.size() && cached_data_ == gates.data()) return cached_measures_;
+    const uint64_t G = gates.size();
+    const unsigned T = std::max(1u, std::min<unsigned>(host_threads(), unsigned(G >> 20) + 1));
+    std::vector<uint64_t> part(T, 0);
+    parallel_chunks(G, T, [&](unsigned t, uint64_t b, uint64_t e) {
+        uint64_t m = 0;
+        for (uint64_t i = b; i < e; ++i) m += gates[i].kind == QSR_MEASURE;
+        part[t] = m;
+    });
     uint64_t m = 0;
-    for (const auto &g : gates)
-        m += g.kind == QSR_MEASURE;
+    for (uint64_t v : part) m += v;
+    cached_measures_ = m;
+    cached_measures_for_ = G;
+    cached_data_ = gates.data();
     return m;
 }
 
