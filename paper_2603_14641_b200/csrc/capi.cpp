@@ -501,7 +501,10 @@ qsr_status qsr_tableau_clone(const qsr_tableau *h, qsr_tableau **out) {
     });
 }
 
-void qsr_tableau_destroy(qsr_tableau *h) { delete h; }
+void qsr_tableau_destroy(qsr_tableau *h) {
+    TraceScope tr("tableau destroy");
+    delete h;
+}
 
 qsr_status qsr_tableau_check_validity(qsr_tableau *h, char *buf, uint64_t cap, uint64_t *len) {
     return guard([&] {
@@ -721,6 +724,7 @@ qsr_status qsr_run_single_shot(const qsr_circuit *c, const qsr_schedule *s, uint
                                int device, qsr_tableau **out_tableau, qsr_record_entry *record,
                                qsr_run_report *report) {
     return guard([&] {
+        TraceScope tr_all("run_single_shot");
         auto wall0 = std::chrono::steady_clock::now();
         REQUIRE_PTR(c);
         const uint64_t nm = c->measure_count();
