@@ -88,7 +88,32 @@ PlaneCache &plane_cache() {
     static PlaneCache *c = new PlaneCache(); // leaked on purpose: outlives static destructors
     return *c;
 }
+
+// Pinned 32-byte read-back slots (batch control words), recycled across tableaux.
+std::mutex g_pinned_mu;
+std::vector<uint32_t *> g_pinned_free;
+uint32_t *pinned_slot() {
+    {
+        std::lock_guard<std::mutex> g(g_pinned_mu);
+        if (!g_pinned_free.empty()) {
+            uint32_t *p = g_pinned_free.back();
+            g_pinned_free.pop_back();
+            return p;
+        }
+    }
+    uint32_t *p = nullptr;
+    QSR_CUDA(cudaMallocHost(&p, 2 * 4 * 4));
+    return p;
+}
+void pinned_slot_release(uint32_t *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    g_pinned_free.push_back(p);
+}
 } // namespace
+
+void *cache_acquire(int device, uint64_t bytes) { return plane_cache().acquire(device, bytes); }
+void cache_release(int device, uint64_t bytes, void *p) { plane_cache().release(device, bytes, p); }
 
 DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : device(dev), n(n_) {
     if (n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
@@ -106,46 +131,49 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
     plane_words = std::max(n_pad * cm_pitch, 2 * ng * rm_pitch);
     QSR_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
     QSR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    auto alloc = [&](uint64_t **p, uint64_t words) {
-        QSR_CUDA(cudaMalloc(p, words * 8));
-        QSR_CUDA(cudaMemsetAsync(*p, 0, words * 8, stream));
-    };
     for (uint64_t **pp : {&x, &z, &x2, &z2}) {
         *pp = static_cast<uint64_t *>(plane_cache().acquire(device, plane_words * 8));
         QSR_CUDA(cudaMemsetAsync(*pp, 0, plane_words * 8, stream));
     }
-    alloc(&s, cm_pitch);
-    QSR_CUDA(cudaMalloc(&tile_counters, (cm_pitch / 64 + 2) * 4));
-    QSR_CUDA(cudaMemsetAsync(tile_counters, 0, (cm_pitch / 64 + 2) * 4, stream));
-    alloc(&ms.mask, 2 * kg + 2);
-    QSR_CUDA(cudaMalloc(&ms.rows, 2 * ng * 4));
-    QSR_CUDA(cudaMalloc(&ms.ctl, 64));
-    QSR_CUDA(cudaMemsetAsync(ms.ctl, 0, 64, stream));
-    alloc(&ms.partial_x, 128 * rm_pitch);
-    alloc(&ms.partial_z, 128 * rm_pitch);
-    QSR_CUDA(cudaMalloc(&ms.partial_e, 128 * 8));
-    QSR_CUDA(cudaMemsetAsync(ms.partial_e, 0, 128 * 8, stream));
-    QSR_CUDA(cudaMalloc(&ms.coin_index, 8));
-    QSR_CUDA(cudaMemsetAsync(ms.coin_index, 0, 8, stream));
-    QSR_CUDA(cudaMalloc(&ms.err, 4));
-    QSR_CUDA(cudaMemsetAsync(ms.err, 0, 4, stream));
-    QSR_CUDA(cudaMalloc(&ms.colbits, 2 * ng * 4));
-    {
-        const uint64_t vwords = uint64_t(kMaxBatch) * 2 * rm_pitch;
-        const uint64_t info_words = (kVinfoWords + 4 + 1) / 2;
-        ms.batch_block_bytes = (vwords + info_words) * 8;
-        alloc(&ms.batch_block, vwords + info_words);
-        ms.Vx = ms.batch_block;
-        ms.Vz = ms.batch_block + rm_pitch;
-        ms.vstride = 2 * rm_pitch;
-        ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
-        ms.bctl = ms.vinfo + kVinfoWords;
+    // The fixed-size scratch lives in ONE arena from the plane cache (one acquire / release per
+    // tableau instead of ~20 cudaMalloc / cudaFree), zeroed once.
+    const uint64_t vwords = uint64_t(kMaxBatch) * 2 * rm_pitch;
+    const uint64_t info_words = (kVinfoWords + 4 + 1) / 2;
+    ms.batch_block_bytes = (vwords + info_words) * 8;
+    struct Piece { void **p; uint64_t bytes; };
+    const Piece pieces[] = {
+        {reinterpret_cast<void **>(&s), cm_pitch * 8},
+        {reinterpret_cast<void **>(&tile_counters), (cm_pitch / 64 + 2) * 4},
+        {reinterpret_cast<void **>(&ms.mask), (2 * kg + 2) * 8},
+        {reinterpret_cast<void **>(&ms.rows), 2 * ng * 4},
+        {reinterpret_cast<void **>(&ms.ctl), 64},
+        {reinterpret_cast<void **>(&ms.partial_x), 128 * rm_pitch * 8},
+        {reinterpret_cast<void **>(&ms.partial_z), 128 * rm_pitch * 8},
+        {reinterpret_cast<void **>(&ms.partial_e), 128 * 8},
+        {reinterpret_cast<void **>(&ms.coin_index), 8},
+        {reinterpret_cast<void **>(&ms.err), 4},
+        {reinterpret_cast<void **>(&ms.colbits), 2 * ng * 4},
+        {reinterpret_cast<void **>(&ms.batch_block), ms.batch_block_bytes},
+        {reinterpret_cast<void **>(&ms.gconst), kMaxBatch * 4},
+        {reinterpret_cast<void **>(&ms.nz), (ng / 32 + 1) * 4},
+        {reinterpret_cast<void **>(&ms.pcount), 2 * kMaxBatch * sizeof(int)},
+        {reinterpret_cast<void **>(&ms.d_pos), 4},
+    };
+    arena_bytes = 0;
+    for (const Piece &pc : pieces) arena_bytes += round_up(pc.bytes, 256);
+    arena = static_cast<uint8_t *>(plane_cache().acquire(device, arena_bytes));
+    QSR_CUDA(cudaMemsetAsync(arena, 0, arena_bytes, stream));
+    uint64_t off = 0;
+    for (const Piece &pc : pieces) {
+        *pc.p = arena + off;
+        off += round_up(pc.bytes, 256);
     }
-    QSR_CUDA(cudaMalloc(&ms.gconst, kMaxBatch * 4));
-    QSR_CUDA(cudaMalloc(&ms.nz, (ng / 32 + 1) * 4));
-    QSR_CUDA(cudaMalloc(&ms.pcount, 2 * kMaxBatch * sizeof(int)));
-    QSR_CUDA(cudaMalloc(&ms.d_pos, 4));
-    QSR_CUDA(cudaMallocHost(&ms.h_bctl, 2 * 4 * 4));
+    ms.Vx = ms.batch_block;
+    ms.Vz = ms.batch_block + rm_pitch;
+    ms.vstride = 2 * rm_pitch;
+    ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
+    ms.bctl = ms.vinfo + kVinfoWords;
+    ms.h_bctl = pinned_slot();
     for (auto &e : ms.bev) QSR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     configure_measure_kernels(*this);
     QSR_CUDA(cudaStreamSynchronize(stream));
@@ -154,20 +182,18 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
 DeviceTableau::~DeviceTableau() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
-    if (ms.h_bctl) cudaFreeHost(ms.h_bctl);
+    pinned_slot_release(ms.h_bctl);
     for (auto e : ms.bev)
         if (e) cudaEventDestroy(e);
     for (uint64_t *p : {x, z, x2, z2}) plane_cache().release(device, plane_words * 8, p);
     if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf);
     gate_buf = nullptr;
-    for (void *p : {(void *)s, (void *)sign_partials, (void *)seg_bar,
-                    (void *)tile_counters, (void *)ms.mask, (void *)ms.rows,
-                    (void *)ms.ctl, (void *)ms.partial_x, (void *)ms.partial_z,
-                    (void *)ms.partial_e, (void *)ms.flags, (void *)ms.out, (void *)ms.mqubits,
-                    (void *)ms.coin_index, (void *)ms.err, (void *)ms.colbits,
-                    (void *)ms.batch_block, (void *)ms.partial, (void *)ms.gconst, (void *)ms.nz, (void *)ms.pcount, (void *)ms.d_pos, (void *)ms.fq,
-                    (void *)ms.fidx, (void *)ms.coin_buf})
-        if (p) cudaFree(p);
+    plane_cache().release(device, arena_bytes, arena);
+    // Lazily sized scratch returns to the cache too (the next tableau of this shape reuses it).
+    plane_cache().release(device, sign_partial_chunks * cm_pitch * 8, sign_partials);
+    plane_cache().release(device, 256, seg_bar);
+    plane_cache().release(device, ms.partial_bytes, ms.partial);
+    release_window_cap();
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -178,21 +204,34 @@ void DeviceTableau::ensure_gate_buf(uint64_t ng) {
     gate_buf = static_cast<uint64_t *>(plane_cache().acquire(device, gate_buf_cap * 8));
 }
 
+// Per-window measurement scratch: six arrays of window_cap entries in one cached block.
+static uint64_t window_block_bytes(uint64_t cap) { return cap * (1 + 1 + sizeof(qsr_record_entry) + 4 + 4 + 4) + 256; }
+
+void DeviceTableau::release_window_cap() {
+    if (ms.window_cap) plane_cache().release(device, window_block_bytes(ms.window_cap), ms.coin_buf);
+    ms.coin_buf = ms.flags = nullptr;
+    ms.out = nullptr;
+    ms.mqubits = ms.fq = ms.fidx = nullptr;
+    ms.window_cap = 0;
+}
+
 void DeviceTableau::ensure_window_cap(uint64_t m) {
     if (m <= ms.window_cap) return;
-    if (ms.flags) QSR_CUDA(cudaFree(ms.flags));
-    if (ms.out) QSR_CUDA(cudaFree(ms.out));
-    if (ms.mqubits) QSR_CUDA(cudaFree(ms.mqubits));
-    if (ms.fq) QSR_CUDA(cudaFree(ms.fq));
-    if (ms.fidx) QSR_CUDA(cudaFree(ms.fidx));
-    if (ms.coin_buf) QSR_CUDA(cudaFree(ms.coin_buf));
-    ms.window_cap = std::max<uint64_t>(m, 64);
-    QSR_CUDA(cudaMalloc(&ms.coin_buf, ms.window_cap));
-    QSR_CUDA(cudaMalloc(&ms.flags, ms.window_cap));
-    QSR_CUDA(cudaMalloc(&ms.out, ms.window_cap * sizeof(qsr_record_entry)));
-    QSR_CUDA(cudaMalloc(&ms.mqubits, ms.window_cap * 4));
-    QSR_CUDA(cudaMalloc(&ms.fq, ms.window_cap * 4));
-    QSR_CUDA(cudaMalloc(&ms.fidx, ms.window_cap * 4));
+    release_window_cap();
+    const uint64_t cap = std::max<uint64_t>(m, 64);
+    uint8_t *b = static_cast<uint8_t *>(plane_cache().acquire(device, window_block_bytes(cap)));
+    ms.window_cap = cap;
+    // coin_buf first (the block's base pointer), 4-byte arrays 16-byte aligned.
+    ms.coin_buf = b;
+    ms.flags = b + cap;
+    uint64_t off = round_up(2 * cap, 16);
+    ms.out = reinterpret_cast<qsr_record_entry *>(b + off);
+    off += round_up(cap * sizeof(qsr_record_entry), 16);
+    ms.mqubits = reinterpret_cast<uint32_t *>(b + off);
+    off += round_up(cap * 4, 16);
+    ms.fq = reinterpret_cast<uint32_t *>(b + off);
+    off += round_up(cap * 4, 16);
+    ms.fidx = reinterpret_cast<uint32_t *>(b + off);
 }
 
 void DeviceTableau::sync() { QSR_CUDA(cudaStreamSynchronize(stream)); }

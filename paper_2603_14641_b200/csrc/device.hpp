@@ -22,6 +22,10 @@
 namespace qsr {
 
 void cuda_check(cudaError_t e, const char *what);
+// The per-device caching allocator behind tableau planes and scratch (capi.cpp): a released
+// block is reused by the next acquire of the same size on the same device.
+void *cache_acquire(int device, uint64_t bytes);
+void cache_release(int device, uint64_t bytes, void *p);
 #define QSR_CUDA(call) ::qsr::cuda_check((call), #call)
 
 extern uint64_t g_launches; // kernel launches issued by the library
@@ -102,12 +106,15 @@ struct DeviceTableau {
     uint64_t *gate_buf = nullptr;          // staging for single-window API calls
     uint64_t gate_buf_cap = 0;
     MeasureScratch ms;
+    uint8_t *arena = nullptr; // fixed-size scratch (signs, counters, measurement scratch), one block
+    uint64_t arena_bytes = 0;
     int num_sms = 148;
 
     DeviceTableau(uint64_t n, int device, uint64_t j0 = 0, uint64_t kg = 0);
     ~DeviceTableau();
     void ensure_gate_buf(uint64_t ngates);
     void ensure_window_cap(uint64_t m);
+    void release_window_cap();
     void sync();
 };
 

@@ -986,9 +986,9 @@ void batch_apply(DeviceTableau &t) {
     }
     const uint64_t nslices = (t.rm_pitch + kSlice - 1) / kSlice;
     if (!ms.partial || ms.partial_bytes < nslices * nrows) {
-        if (ms.partial) QSR_CUDA(cudaFree(ms.partial));
+        if (ms.partial) cache_release(t.device, ms.partial_bytes, ms.partial);
         ms.partial_bytes = nslices * nrows;
-        QSR_CUDA(cudaMalloc(&ms.partial, ms.partial_bytes));
+        ms.partial = static_cast<uint8_t *>(cache_acquire(t.device, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
     k_batch_member<<<row_blocks + kB, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,

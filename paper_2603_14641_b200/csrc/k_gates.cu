@@ -307,10 +307,11 @@ void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool sig
     if (chunks > 65535) chunks = 65535;
     uint64_t chunk = (nitems + chunks - 1) / chunks;
     chunks = (nitems + chunk - 1) / chunk;
-    if (signs && chunks > 1 && chunks > *partial_chunks) {
-        if (*partials)
-            QSR_CUDA(cudaFree(*partials));
-        QSR_CUDA(cudaMalloc(partials, chunks * pitch * sizeof(uint64_t)));
+    if (signs && chunks > 1 && chunks > *partial_chunks) { // (the owner's device is current)
+        int dev = 0;
+        QSR_CUDA(cudaGetDevice(&dev));
+        if (*partials) cache_release(dev, *partial_chunks * pitch * sizeof(uint64_t), *partials);
+        *partials = static_cast<uint64_t *>(cache_acquire(dev, chunks * pitch * sizeof(uint64_t)));
         *partial_chunks = chunks;
     }
     *tiles_out = tiles;
@@ -784,7 +785,7 @@ bool gate_segment_enabled() { return segment_enabled(); }
 
 void launch_gate_segment(DeviceTableau &t, const uint64_t *gates, const uint64_t *d_woff,
                          uint32_t nwin) {
-    if (!t.seg_bar) QSR_CUDA(cudaMalloc(&t.seg_bar, 256));
+    if (!t.seg_bar) t.seg_bar = static_cast<unsigned int *>(cache_acquire(t.device, 256));
     // x2 / z2 (the transpose targets) are free during unitary windows: slab-major copies.
     launch_segment<true>(t.x, t.z, t.cm_pitch, t.n_pad, gates, d_woff, nwin, t.device, t.num_sms,
                          t.stream, t.seg_bar, t.s, t.x2, t.z2);
