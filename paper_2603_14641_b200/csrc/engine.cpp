@@ -176,7 +176,8 @@ void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint6
         dev_gates = fused.data();
         DG = fused.size();
         if (!perms.empty()) {
-            QSR_CUDA(cudaMalloc(&ds.d_perms, perms.size() * 4));
+            ds.d_perms_bytes = perms.size() * 4;
+            ds.d_perms = static_cast<uint32_t *>(cache_acquire(device, ds.d_perms_bytes));
             QSR_CUDA(cudaMemcpyAsync(ds.d_perms, perms.data(), perms.size() * 4, cudaMemcpyHostToDevice, st));
         }
     } else {
@@ -189,7 +190,8 @@ void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint6
             ds.wwords.push_back(words);
         }
     }
-    QSR_CUDA(cudaMalloc(&ds.d_gates, std::max<uint64_t>(DG, 1) * 8));
+    ds.d_gates_bytes = std::max<uint64_t>(DG, 1) * 8;
+    ds.d_gates = static_cast<uint64_t *>(cache_acquire(device, ds.d_gates_bytes));
     if (DG) {
         TraceScope tr("  gates H2D");
         QSR_CUDA(cudaMemcpyAsync(ds.d_gates, dev_gates, DG * 8, cudaMemcpyHostToDevice, st));
@@ -268,7 +270,8 @@ void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets
 }
 
 void upload_offsets(DeviceSchedule &ds, cudaStream_t st) {
-    QSR_CUDA(cudaMalloc(&ds.d_offsets, ds.offsets.size() * 8));
+    ds.d_offsets_bytes = ds.offsets.size() * 8;
+    ds.d_offsets = static_cast<uint64_t *>(cache_acquire(ds.device, ds.d_offsets_bytes));
     QSR_CUDA(cudaMemcpyAsync(ds.d_offsets, ds.offsets.data(), ds.offsets.size() * 8,
                              cudaMemcpyHostToDevice, st));
     QSR_CUDA(cudaStreamSynchronize(st));

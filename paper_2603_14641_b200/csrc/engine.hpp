@@ -39,11 +39,13 @@ struct DeviceSchedule {
         uint64_t kernels;
     };
     mutable std::vector<Graph> graphs;
+    uint64_t d_gates_bytes = 0, d_offsets_bytes = 0, d_perms_bytes = 0; // cached blocks
     ~DeviceSchedule() {
         cudaSetDevice(device);
         for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
-        for (void *p : {(void *)d_gates, (void *)d_offsets, (void *)d_perms})
-            if (p) cudaFree(p);
+        cache_release(device, d_gates_bytes, d_gates);
+        cache_release(device, d_offsets_bytes, d_offsets);
+        cache_release(device, d_perms_bytes, d_perms);
     }
     const uint32_t *perm_before(uint64_t w) const {
         return (w < perm_at.size() && perm_at[w] >= 0) ? d_perms + perm_at[w] : nullptr;
