@@ -936,10 +936,9 @@ struct qsr_frames {
     ~qsr_frames() {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
-        plane_cache().release(device, plane_bytes, xf);
-        plane_cache().release(device, plane_bytes, zf);
+        for (uint64_t *p : {xf, zf, xs, zs}) plane_cache().release(device, plane_bytes, p);
         if (rec) plane_cache().release(device, rec_cap * pitch * 8, rec);
-        for (void *p : {(void *)gate_buf, (void *)d_idx, (void *)seg_bar, (void *)xs, (void *)zs})
+        for (void *p : {(void *)gate_buf, (void *)d_idx, (void *)seg_bar})
             if (p) cudaFree(p);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -1004,7 +1003,9 @@ void frames_window(qsr_frames &f, const uint64_t *d_gates, uint64_t ng) {
 }
 
 extern "C++" template <typename QubitOf>
-void frames_measure_q(qsr_frames &f, QubitOf qubit_of, uint64_t ng, uint64_t seed, uint32_t epoch) {
+void frames_measure_q(qsr_frames &f, QubitOf qubit_of, uint64_t ng, uint64_t seed, uint32_t epoch,
+                      cudaStream_t st = nullptr) {
+    if (!st) st = f.stream;
     std::vector<uint32_t> idx(2 * ng);
     for (uint64_t i = 0; i < ng; ++i) {
         uint32_t q = qubit_of(i);
@@ -1017,10 +1018,10 @@ void frames_measure_q(qsr_frames &f, QubitOf qubit_of, uint64_t ng, uint64_t see
     }
     f.ensure_rows(f.measured.size());
     f.ensure_idx(ng);
-    QSR_CUDA(cudaMemcpyAsync(f.d_idx, idx.data(), 2 * ng * 4, cudaMemcpyHostToDevice, f.stream));
+    QSR_CUDA(cudaMemcpyAsync(f.d_idx, idx.data(), 2 * ng * 4, cudaMemcpyHostToDevice, st));
     launch_measure_sample(f.xf, f.zf, f.pitch, f.kf, f.j0, f.shots, f.rec, f.d_idx, f.d_idx + ng, ng,
-                          seed, epoch, f.wbits, f.stream);
-    QSR_CUDA(cudaStreamSynchronize(f.stream)); // idx staging reused next call
+                          seed, epoch, f.wbits, st);
+    QSR_CUDA(cudaStreamSynchronize(st)); // idx staging reused next call
 }
 
 void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t seed, uint32_t epoch) {
@@ -1178,74 +1179,123 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         const uint64_t w0 = kf_all * uint64_t(rank) / uint64_t(world);
         const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
         TraceScope tr_all("sample");
-        // Reference shot (frames.hpp:167): the full single-shot pipeline on the device, on the
-        // O(G) plan scattered straight into packed device gates (schedule_windows' windows; the
-        // sampling mode is only a tag, schedule.hpp:37-42). The frames reuse the same windows.
-        TraceScope tr_ref("  reference shot");
+        // One record allocation: the distinct measured qubits of the circuit.
+        auto distinct_measured = [&] {
+            std::vector<uint8_t> seen(c->num_qubits, 0);
+            uint64_t distinct = 0;
+            for (const qsr_gate &g : c->gates)
+                if (g.kind == QSR_MEASURE && g.q0 < c->num_qubits && !seen[g.q0]) { seen[g.q0] = 1; ++distinct; }
+            return distinct;
+        };
         DeviceTableau t(c->num_qubits, device);
-        auto ds = upload_circuit(*c, device, t.stream, /*fuse=*/false);
-        const uint64_t nm = ds->measure_count;
+        const uint64_t nm = c->measure_count();
         qsr_record_entry *d_rec = nullptr;
         QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
-        RunTimes rt;
         std::vector<qsr_record_entry> ref(nm);
+        std::unique_ptr<qsr_frames> f;
+        const bool streaming = !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0') &&
+                               !gate_segment_enabled();
         try {
-            run_device(t, *ds, seed, d_rec, rt);
-            if (nm)
-                QSR_CUDA(cudaMemcpyAsync(ref.data(), d_rec, nm * sizeof(qsr_record_entry),
-                                         cudaMemcpyDeviceToHost, t.stream));
-            t.sync();
+            if (streaming) {
+                // The reference shot (frames.hpp:167) streamed as in run_single_shot (schedule
+                // overlapped with the device, fused windows), and the frames (frames.hpp:171-181)
+                // riding the same device windows, row un-permutes and measurement windows on the
+                // tableau's stream: the Pauli frames follow the same Clifford conjugation, so
+                // fusion is exact for them too.
+                TraceScope tr("  reference shot + frames (streamed)");
+                f = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
+                if (const uint64_t d = distinct_measured()) f->ensure_rows(d);
+                QSR_CUDA(cudaStreamSynchronize(f->stream));
+                struct Sink final : FramesSink {
+                    qsr_frames &f;
+                    uint64_t seed;
+                    uint32_t epoch = 1;
+                    Sink(qsr_frames &ff, uint64_t s) : f(ff), seed(s) {}
+                    void unitary(const uint64_t *g, uint64_t cnt, cudaStream_t st) override {
+                        launch_frame_window(f.xf, f.zf, f.pitch, g, cnt, f.num_sms, st);
+                    }
+                    void unpermute(const uint32_t *perm, cudaStream_t st) override {
+                        if (!f.xs) {
+                            f.xs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
+                            f.zs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
+                        }
+                        launch_unpermute_frame_rows(f.xf, f.xs, f.pitch, f.n, perm, f.num_sms, st);
+                        launch_unpermute_frame_rows(f.zf, f.zs, f.pitch, f.n, perm, f.num_sms, st);
+                        std::swap(f.xf, f.xs);
+                        std::swap(f.zf, f.zs);
+                    }
+                    void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) override {
+                        frames_measure_q(f, [&](uint64_t i) { return qubits[i]; }, m, seed, epoch++, st);
+                    }
+                } sink(*f, seed);
+                RunTimes rt;
+                StreamCounts sc;
+                run_circuit_streaming(t, *c, seed, d_rec, rt, sc, &sink);
+                if (nm)
+                    QSR_CUDA(cudaMemcpyAsync(ref.data(), d_rec, nm * sizeof(qsr_record_entry),
+                                             cudaMemcpyDeviceToHost, t.stream));
+                t.sync();
+                if (report) {
+                    DeviceSchedule cnt;
+                    cnt.device = device;
+                    cnt.unitary_count = sc.unitary;
+                    cnt.measure_count = sc.measures;
+                    cnt.is_meas.resize(sc.windows);
+                    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+                    fill_report(report, rt, cnt, ref, wall);
+                }
+            } else {
+                // Reference shot on the O(G) plan scattered straight into packed device gates
+                // (schedule_windows' windows; the sampling mode is only a tag, schedule.hpp:37-42);
+                // the frames then replay the same device-resident windows.
+                TraceScope tr_ref("  reference shot");
+                auto ds = upload_circuit(*c, device, t.stream, /*fuse=*/false);
+                RunTimes rt;
+                run_device(t, *ds, seed, d_rec, rt);
+                if (nm)
+                    QSR_CUDA(cudaMemcpyAsync(ref.data(), d_rec, nm * sizeof(qsr_record_entry),
+                                             cudaMemcpyDeviceToHost, t.stream));
+                t.sync();
+                if (report) {
+                    double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+                    fill_report(report, rt, *ds, ref, wall);
+                }
+                f = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
+                if (const uint64_t d = distinct_measured()) f->ensure_rows(d);
+                QSR_CUDA(cudaStreamSynchronize(f->stream));
+                TraceScope tr_frames("  frames windows");
+                uint32_t epoch = 1;
+                const uint64_t W = ds->is_meas.size();
+                for (uint64_t w = 0; w < W;) {
+                    const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
+                    if (ds->is_meas[w]) {
+                        const auto &mq = ds->mqubits[w];
+                        frames_measure_q(*f, [&](uint64_t i) { return mq[i]; }, e - b, seed, epoch++);
+                        ++w;
+                        continue;
+                    }
+                    uint64_t w1 = w;
+                    while (w1 < W && !ds->is_meas[w1]) ++w1;
+                    if (gate_segment_enabled() && w1 - w >= 2 && f->n) {
+                        if (!f->seg_bar) QSR_CUDA(cudaMalloc(&f->seg_bar, 256));
+                        if (!f->xs) {
+                            f->xs = static_cast<uint64_t *>(plane_cache().acquire(f->device, f->plane_bytes));
+                            f->zs = static_cast<uint64_t *>(plane_cache().acquire(f->device, f->plane_bytes));
+                        }
+                        launch_frame_segment(f->xf, f->zf, f->pitch, f->n, ds->d_gates, ds->d_offsets + w,
+                                             uint32_t(w1 - w), f->num_sms, f->stream, f->seg_bar, f->xs, f->zs);
+                    } else {
+                        for (uint64_t v = w; v < w1; ++v)
+                            frames_window(*f, ds->d_gates + ds->offsets[v], ds->offsets[v + 1] - ds->offsets[v]);
+                    }
+                    w = w1;
+                }
+            }
         } catch (...) {
             cudaFree(d_rec);
             throw;
         }
         cudaFree(d_rec);
-        if (report) {
-            double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-            fill_report(report, rt, *ds, ref, wall);
-        }
-        // Frames over the same device-resident schedule (frames.hpp:171-181).
-        auto f = [&] {
-            TraceScope tr("  make_frames");
-            auto ff = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
-            // One record allocation: the distinct measured qubits of the schedule.
-            std::vector<uint8_t> seen(c->num_qubits, 0);
-            uint64_t distinct = 0;
-            for (const auto &mq : ds->mqubits)
-                for (uint32_t q : mq)
-                    if (!seen[q]) { seen[q] = 1; ++distinct; }
-            if (distinct) ff->ensure_rows(distinct);
-            QSR_CUDA(cudaStreamSynchronize(ff->stream));
-            return ff;
-        }();
-        QSR_CUDA(cudaStreamSynchronize(t.stream));
-        TraceScope tr_frames("  frames windows + fold");
-        uint32_t epoch = 1;
-        const uint64_t W = ds->is_meas.size();
-        for (uint64_t w = 0; w < W;) {
-            const uint64_t b = ds->offsets[w], e = ds->offsets[w + 1];
-            if (ds->is_meas[w]) {
-                const auto &mq = ds->mqubits[w];
-                frames_measure_q(*f, [&](uint64_t i) { return mq[i]; }, e - b, seed, epoch++);
-                ++w;
-                continue;
-            }
-            uint64_t w1 = w;
-            while (w1 < W && !ds->is_meas[w1]) ++w1;
-            if (gate_segment_enabled() && w1 - w >= 2 && f->n) {
-                if (!f->seg_bar) QSR_CUDA(cudaMalloc(&f->seg_bar, 256));
-                if (!f->xs) {
-                    QSR_CUDA(cudaMalloc(&f->xs, f->n * f->pitch * 8));
-                    QSR_CUDA(cudaMalloc(&f->zs, f->n * f->pitch * 8));
-                }
-                launch_frame_segment(f->xf, f->zf, f->pitch, f->n, ds->d_gates, ds->d_offsets + w,
-                                     uint32_t(w1 - w), f->num_sms, f->stream, f->seg_bar, f->xs, f->zs);
-            } else {
-                for (uint64_t v = w; v < w1; ++v)
-                    frames_window(*f, ds->d_gates + ds->offsets[v], ds->offsets[v + 1] - ds->offsets[v]);
-            }
-            w = w1;
-        }
         // Fold in the reference outcomes: per_qubit() = last outcome per qubit
         // (measure.hpp:50-64, frames.hpp:183-202).
         std::vector<int8_t> last(c->num_qubits, -1);

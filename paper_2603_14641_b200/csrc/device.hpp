@@ -138,6 +138,9 @@ void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t r
 // Gate fusion support (fuse.hpp): the CM rows un-permuted (logical q <- physical perm[q]) into
 // the spare planes, which then become the current ones.
 void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm);
+// Frames rows (n rows of `pitch` words): dst[q] = src[perm[q]].
+void launch_unpermute_frame_rows(const uint64_t *src, uint64_t *dst, uint64_t pitch, uint64_t n,
+                                 const uint32_t *d_perm, int num_sms, cudaStream_t st);
 // Frames: same rules, no signs.
 void launch_frame_window(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *gates,
                          uint64_t ngates, int num_sms, cudaStream_t st);

@@ -87,8 +87,17 @@ void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &
 struct StreamCounts {
     uint64_t unitary = 0, measures = 0, windows = 0;
 };
+// Optional passenger of the stream: sample()'s Pauli frames ride the same (fused) device windows,
+// measurement windows and row un-permutes, on the tableau's stream (capi.cpp).
+struct FramesSink {
+    virtual ~FramesSink() = default;
+    virtual void unitary(const uint64_t *d_gates, uint64_t cnt, cudaStream_t st) = 0;
+    virtual void unpermute(const uint32_t *d_perm, cudaStream_t st) = 0;
+    virtual void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) = 0;
+};
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
-                           qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts);
+                           qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,
+                           FramesSink *frames = nullptr);
 // Host reference-layout <-> device layout (CM: [n_pad][2kg] words; RM: reference i-major).
 void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout);
 void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z);

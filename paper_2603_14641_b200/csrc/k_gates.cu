@@ -818,6 +818,14 @@ __global__ void k_unpermute_rows(const uint64_t *__restrict__ src, uint64_t *__r
 }
 } // namespace
 
+void launch_unpermute_frame_rows(const uint64_t *src, uint64_t *dst, uint64_t pitch, uint64_t n,
+                                 const uint32_t *d_perm, int num_sms, cudaStream_t st) {
+    if (n == 0) return;
+    k_unpermute_rows<<<unsigned(num_sms * 8), 512, 0, st>>>(src, dst, pitch, n, n, d_perm);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+}
+
 void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm) {
     for (int plane = 0; plane < 2; ++plane) {
         k_unpermute_rows<<<unsigned(t.num_sms * 8), 512, 0, t.stream>>>(plane ? t.z : t.x, plane ? t.z2 : t.x2,

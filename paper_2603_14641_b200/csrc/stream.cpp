@@ -79,7 +79,8 @@ class BucketDir {
 };
 
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
-                           qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts) {
+                           qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,
+                           FramesSink *frames) {
     const uint64_t G = c.gates.size();
     const uint32_t n = c.num_qubits;
     t.ensure_gate_buf(std::max<uint64_t>(G, 1));
@@ -177,15 +178,19 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                     ring.fill += take;
                     i += take;
                 }
-                if (kind == 1) launch_gate_pairs(t, d_gates + dev_off, cnt / kPairRecWords);
-                else launch_gate_window(t, d_gates + dev_off, cnt);
+                if (kind == 1) {
+                    launch_gate_pairs(t, d_gates + dev_off, cnt / kPairRecWords);
+                } else {
+                    launch_gate_window(t, d_gates + dev_off, cnt);
+                    if (frames) frames->unitary(d_gates + dev_off, cnt, t.stream);
+                }
                 ++rt.gate_launches;
                 dev_off += cnt;
                 t_stage += since(ts);
             };
             // Window pairing (pair.hpp): each finished unitary window is held until the next.
-            Pairer pairer(fuse && pairing_enabled() && !gate_segment_enabled() ? n : 0);
-            const bool pairing = fuse && pairing_enabled() && !gate_segment_enabled();
+            const bool pairing = fuse && pairing_enabled() && !gate_segment_enabled() && !frames;
+            Pairer pairer(pairing ? n : 0);
             std::vector<uint64_t> held;
             PairOut po;
             auto unitary_window = [&](std::vector<uint64_t> &w) {
@@ -223,6 +228,7 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                 QSR_CUDA(cudaMemcpyAsync(d_perm, pm.data(), uint64_t(n) * 4, cudaMemcpyHostToDevice, t.stream));
                 QSR_CUDA(cudaStreamSynchronize(t.stream)); // pm is about to go away
                 launch_unpermute_rows(t, d_perm);
+                if (frames) frames->unpermute(d_perm, t.stream);
                 fuser.reset_permutation();
             };
             for (;;) {
@@ -269,6 +275,7 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                         QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
                         measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
                         t_meas += since(tm);
+                        if (frames) frames->measure(mq.data(), cnt, t.stream);
                         QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, cnt * sizeof(qsr_record_entry),
                                                  cudaMemcpyDeviceToDevice, t.stream));
                         rec_off += cnt;
