@@ -310,7 +310,11 @@ qsr_status qsr_circuit_create(uint32_t num_qubits, const qsr_gate *gates, uint64
         if (ngates) REQUIRE_PTR(gates);
         auto c = std::make_unique<qsr_circuit>();
         c->num_qubits = num_qubits;
-        c->gates.assign(gates, gates + ngates);
+        c->gates.resize(ngates);
+        const unsigned T = std::max(1u, std::min<unsigned>(host_threads(), unsigned(ngates >> 22) + 1));
+        parallel_chunks(ngates, T, [&](unsigned, uint64_t b, uint64_t e) {
+            if (e > b) std::memcpy(c->gates.data() + b, gates + b, (e - b) * sizeof(qsr_gate));
+        });
         c->check_valid();
         *out = c.release();
     });

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <chrono>
+#include <memory>
+#include <utility>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -12,6 +14,23 @@
 #include "../../include/qsr.h"
 
 namespace qsr {
+
+// Allocator that default-initialises: a gate vector of 100 M+ entries is always written before
+// it is read, and value-initialising it (a per-element zero fill + single-threaded first touch)
+// cost ~2 s at c5.
+template <typename T>
+struct NoInitAlloc : std::allocator<T> {
+    template <typename U>
+    struct rebind { using other = NoInitAlloc<U>; };
+    NoInitAlloc() = default;
+    template <typename U>
+    NoInitAlloc(const NoInitAlloc<U> &) noexcept {}
+    template <typename U>
+    void construct(U *p) noexcept { ::new (static_cast<void *>(p)) U; }
+    template <typename U, typename... A>
+    void construct(U *p, A &&...a) { ::new (static_cast<void *>(p)) U(std::forward<A>(a)...); }
+};
+using GateVec = std::vector<qsr_gate, NoInitAlloc<qsr_gate>>;
 
 // Host-side phase trace: QSR_TRACE=1 prints "[qsr] phase ms" lines to stderr (wall clock of the
 // calling thread; device work inside a phase is synchronised by the phase itself).
@@ -79,7 +98,7 @@ uint64_t philox_word(uint64_t seed, uint32_t stream, uint32_t ctx, uint64_t inde
 
 struct Circuit {
     uint32_t num_qubits = 0;
-    std::vector<qsr_gate> gates;
+    GateVec gates;
     uint32_t num_clbits = 0; // classical bits named in the source (labels only, circuit.hpp:103-105)
     uint64_t measure_count() const; // cached (keyed by the gate vector's size and storage)
     void check_valid() const; // circuit.hpp:108-115
@@ -94,7 +113,7 @@ Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double measur
 
 struct Schedule {
     int mode = QSR_SINGLE_SHOT;
-    std::vector<qsr_gate> gates;     // flattened, schedule order
+    GateVec gates;                   // flattened, schedule order
     std::vector<uint64_t> offsets;   // nwindows + 1
     std::vector<uint8_t> is_meas;    // nwindows
     uint64_t num_windows() const { return is_meas.size(); }

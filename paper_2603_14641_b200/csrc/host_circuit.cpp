@@ -93,14 +93,34 @@ uint64_t Circuit::measure_count() const {
 }
 
 void Circuit::check_valid() const {
-    for (const auto &g : gates) {
-        if (g.kind > QSR_MEASURE)
-            fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
-        int ar = gate_arity(g.kind);
-        if (g.q0 >= num_qubits || (ar == 2 && g.q1 >= num_qubits))
-            fail(QSR_OUT_OF_RANGE, "gate operand out of range");
-        if (ar == 2 && g.q0 == g.q1)
-            fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
+    // The reference reports the first offending gate (circuit.hpp:108-115): chunks are checked in
+    // parallel, and the earliest failing index wins.
+    const uint64_t G = gates.size();
+    const unsigned T = std::max(1u, std::min<unsigned>(host_threads(), unsigned(G >> 20) + 1));
+    std::vector<uint64_t> first(T, ~uint64_t(0));
+    std::vector<int> why(T, 0);
+    parallel_chunks(G, T, [&](unsigned t, uint64_t b, uint64_t e) {
+        for (uint64_t i = b; i < e; ++i) {
+            const qsr_gate &g = gates[i];
+            int w = 0;
+            if (g.kind > QSR_MEASURE) {
+                w = 1;
+            } else {
+                const int ar = gate_arity(g.kind);
+                if (g.q0 >= num_qubits || (ar == 2 && g.q1 >= num_qubits)) w = 2;
+                else if (ar == 2 && g.q0 == g.q1) w = 3;
+            }
+            if (w) {
+                first[t] = i;
+                why[t] = w;
+                return;
+            }
+        }
+    });
+    for (unsigned t = 0; t < T; ++t) {
+        if (why[t] == 1) fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
+        if (why[t] == 2) fail(QSR_OUT_OF_RANGE, "gate operand out of range");
+        if (why[t] == 3) fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
     }
 }
 
@@ -133,7 +153,7 @@ const uint8_t kUnitary[11] = {QSR_X, QSR_Y, QSR_Z, QSR_H, QSR_S, QSR_SDG, QSR_CX
 const uint8_t kSingle[6] = {QSR_X, QSR_Y, QSR_Z, QSR_H, QSR_S, QSR_SDG};
 
 // One layer of the reference generator from stream position rng.index (circuit.hpp:142-164).
-void sequential_layer(Stream &rng, uint32_t n, std::vector<uint32_t> &order, std::vector<qsr_gate> &out) {
+void sequential_layer(Stream &rng, uint32_t n, std::vector<uint32_t> &order, GateVec &out) {
     {
         for (uint32_t i = 0; i < n; ++i)
             order[i] = i;

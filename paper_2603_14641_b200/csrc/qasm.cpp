@@ -152,7 +152,7 @@ uint32_t qubit_operand(Lexer<Piece> &L, const Regs &r) {
 // One gate or measure statement whose keyword `kw` has been read (qasm.hpp:211-244). Returns
 // false if `kw` is not one.
 template <bool Piece>
-bool gate_statement(Lexer<Piece> &L, const Regs &r, std::string_view kw, std::vector<qsr_gate> &out) {
+bool gate_statement(Lexer<Piece> &L, const Regs &r, std::string_view kw, GateVec &out) {
     if (kw == "measure") {
         if (!r.have_qreg) L.fail("measure before qreg declaration");
         const uint32_t q = qubit_operand(L, r);
@@ -183,6 +183,57 @@ bool gate_statement(Lexer<Piece> &L, const Regs &r, std::string_view kw, std::ve
     }
     L.expect(';');
     out.push_back(g);
+    return true;
+}
+
+// Fast path for the canonical statement shapes emit_qasm writes ("h q[3];", "cx q[0],q[1];",
+// "measure q[5] -> c[5];", no comments or line breaks inside): recognised without the general
+// lexer and with the same checks; anything else (or any error) returns false with nothing
+// consumed, and the general path takes the statement (so error positions stay exact).
+template <bool Piece>
+bool fast_statement(Lexer<Piece> &L, const Regs &r, GateVec &out) {
+    if (!r.have_qreg) return false;
+    const char *p = L.p, *const e = L.e;
+    const char *s = p;
+    while (p < e && *p >= 'a' && *p <= 'z') ++p;
+    if (p >= e || *p != ' ') return false;
+    const std::string_view name(s, size_t(p - s));
+    const int k = unitary_kind(name);
+    const bool meas = k < 0 && name == "measure";
+    if (k < 0 && !meas) return false;
+    ++p;
+    auto index = [&](std::string_view reg, uint64_t bound, uint32_t &out_idx) {
+        if (size_t(e - p) < reg.size() + 3 || std::memcmp(p, reg.data(), reg.size()) != 0) return false;
+        p += reg.size();
+        if (*p != '[') return false;
+        ++p;
+        uint64_t v = 0;
+        int nd = 0;
+        while (p < e && is_digit(*p)) {
+            v = v * 10 + uint64_t(*p++ - '0');
+            if (++nd > 18) return false;
+        }
+        if (nd == 0 || p >= e || *p != ']' || v >= bound) return false;
+        ++p;
+        out_idx = uint32_t(v);
+        return true;
+    };
+    qsr_gate g{uint8_t(meas ? QSR_MEASURE : k), 0, 0};
+    if (!index(r.qreg, r.num_qubits, g.q0)) return false;
+    if (meas) {
+        if (size_t(e - p) >= 4 && p[0] == ' ' && p[1] == '-' && p[2] == '>' && p[3] == ' ') {
+            p += 4;
+            uint32_t cl = 0;
+            if (r.creg.empty() || !index(r.creg, r.num_clbits, cl)) return false;
+        }
+    } else if (gate_arity(uint8_t(k)) == 2) {
+        if (p >= e || *p != ',') return false;
+        ++p;
+        if (!index(r.qreg, r.num_qubits, g.q1) || g.q0 == g.q1) return false;
+    }
+    if (p >= e || *p != ';') return false;
+    out.push_back(g);
+    L.p = p + 1;
     return true;
 }
 
@@ -227,7 +278,7 @@ const char *next_boundary(const char *p, const char *lo, const char *e) {
 }
 
 // Parallel body parse; false = some piece aborted (nothing of `out` is kept then).
-bool parse_body_parallel(const char *b, const char *e, const Regs &r, std::vector<qsr_gate> &out) {
+bool parse_body_parallel(const char *b, const char *e, const Regs &r, GateVec &out) {
     const uint64_t len = uint64_t(e - b);
     const unsigned T = std::max(1u, std::min<unsigned>(host_threads(), unsigned(len >> 22)));
     if (T < 2) return false;
@@ -236,7 +287,7 @@ bool parse_body_parallel(const char *b, const char *e, const Regs &r, std::vecto
     cut[T] = e;
     for (unsigned t = 1; t < T; ++t)
         cut[t] = std::max(cut[t - 1], next_boundary(b + len * t / T, b, e));
-    std::vector<std::vector<qsr_gate>> part(T);
+    std::vector<GateVec> part(T);
     std::atomic<bool> bad{false};
     parallel_chunks(T, T, [&](unsigned, uint64_t t0, uint64_t t1) {
         for (uint64_t t = t0; t < t1 && !bad.load(std::memory_order_relaxed); ++t) {
@@ -245,6 +296,7 @@ bool parse_body_parallel(const char *b, const char *e, const Regs &r, std::vecto
                 auto &v = part[t];
                 v.reserve(size_t(cut[t + 1] - cut[t]) / 14 + 16);
                 while (!L.eof()) {
+                    if (fast_statement(L, r, v)) continue;
                     std::string_view kw = L.ident();
                     if (!gate_statement(L, r, kw, v)) throw Abort{};
                 }
@@ -262,7 +314,7 @@ bool parse_body_parallel(const char *b, const char *e, const Regs &r, std::vecto
         for (uint64_t t = t0; t < t1; ++t) {
             if (!part[t].empty())
                 std::memcpy(out.data() + base + off[t], part[t].data(), part[t].size() * sizeof(qsr_gate));
-            std::vector<qsr_gate>().swap(part[t]);
+            GateVec().swap(part[t]);
         }
     });
     return true;
@@ -365,6 +417,7 @@ Circuit parse_qasm(const char *text, uint64_t len) {
     // Sequential body (also the exact-error path when a piece aborted).
     c.gates.reserve(size_t(L.e - L.p) / 14 + 16);
     while (!L.eof()) {
+        if (fast_statement(L, r, c.gates)) continue;
         std::string_view kw = L.ident();
         if (header_statement(L, r, kw)) {
             c.num_qubits = r.num_qubits;
