@@ -81,8 +81,6 @@ __device__ __forceinline__ V2 rule2(uint32_t kind, V2 &x0, V2 &z0, V2 &x1, V2 &z
     return sign;
 }
 
-__device__ __forceinline__ uint64_t bitmask(uint32_t c, int b) { return 0ull - uint64_t((c >> b) & 1u); }
-
 // One of the 24 single-qubit Cliffords (kCliff1 encoding: bits 0-3 matrix m00 m01 m10 m11, bits
 // 4-6 sign flips of the images of X, Z, Y) on a word pair; returns the sign-flip words. Each
 // element is a compile-time instance (the masks fold away: 2-6 logic ops per word instead of
