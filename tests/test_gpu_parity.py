@@ -298,7 +298,8 @@ def test_mixed_bell_and_random(q, oracle):
 
 @pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_GATE_ENGINE": "segment"},
                                  {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"}, {"QSR_APPLY": "rows"},
-                                 {"QSR_PIVOTS": "fused"}, {"QSR_PAIR": "1", "QSR_STREAM": "0"}])
+                                 {"QSR_PIVOTS": "fused"}, {"QSR_PAIR": "1", "QSR_STREAM": "0"},
+                                 {"QSR_PAIR": "1"}, {"QSR_GRAPHS": "0"}])
 def test_alternate_collapse_paths_match(q, env):
     """Every alternate path must agree with the default and the oracle: QSR_MEASURE_BATCH=0 (one
     collapse per pass), QSR_GATE_ENGINE=segment (temporally blocked gates), QSR_FUSE=0 (no gate
@@ -321,6 +322,18 @@ def test_alternate_collapse_paths_match(q, env):
         "    gx, gz, gs = r.tableau.planes()\n"
         "    assert np.array_equal(gx, x) and np.array_equal(gz, z) and np.array_equal(gs, s)\n"
         "    assert np.array_equal(r.record_array, rec)\n"
+        "    e = q.Engine(c)\n"
+        "    for _ in range(2):\n"
+        "        e.run(seed)\n"
+        "        assert np.array_equal(e.record(), rec)\n"
+        "        gx, gz, gs = e.tableau_planes(n)\n"
+        "        assert np.array_equal(gx, x) and np.array_equal(gz, z) and np.array_equal(gs, s)\n"
+        "    se = q.ShardedEngine(c, min(3, (n + 63) // 64))\n"
+        "    se.run(seed)\n"
+        "    assert np.array_equal(se.record(), rec)\n"
+        "    meas, words, _ = o.sample(n, c.gate_array, 200, seed)\n"
+        "    smp = q.sample(c, 200, seed)\n"
+        "    assert smp.measured == [int(v) for v in meas] and np.array_equal(smp.words, words)\n"
         "print('ok')\n")
     import os
     env = dict(os.environ, **env)
