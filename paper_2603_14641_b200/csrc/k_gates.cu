@@ -293,7 +293,9 @@ void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool sig
     }();
     const uint64_t max_chunks = std::max<uint64_t>(1, nitems / (kWarps * per_warp));
     uint64_t c_min = std::max<uint64_t>(1, (4 * slots + tiles - 1) / tiles);
-    if (c_min > max_chunks) c_min = max_chunks;
+    // Small windows cannot reach ~4 waves: search the upper half of the allowed range, where a
+    // grid just under a whole wave beats one that spills a few CTAs into a second wave.
+    if (c_min > max_chunks) c_min = std::max<uint64_t>(1, max_chunks / 2);
     uint64_t chunks = c_min;
     double best = 1e30;
     for (uint64_t c = c_min; c <= std::min<uint64_t>(max_chunks, 4 * c_min); ++c) {
