@@ -246,3 +246,28 @@ def test_num_threads_roundtrip(q):
         assert q.parse_qasm(q.emit_qasm(c)) == c
     finally:
         q.set_num_threads(0)
+
+
+def test_text_output_convention(q):
+    """qsr.h text outputs: NULL buffer -> size query; a short buffer is rejected with the size set."""
+    import ctypes as C
+    from paper_2603_14641_b200 import _lib
+    c = q.generate_random(20, 5, 2, 0.5)
+    n = C.c_uint64()
+    _lib.check(_lib.lib.qsr_emit_qasm(c._h, None, 0, C.byref(n)))
+    need = n.value
+    assert need == len(q.emit_qasm(c).encode())
+    small = C.create_string_buffer(need - 1)
+    st = _lib.lib.qsr_emit_qasm(c._h, small, need - 1, C.byref(n))
+    assert st == _lib.INVALID_ARGUMENT and n.value == need
+    assert b"too small" in _lib.lib.qsr_last_error()
+
+
+def test_qasm_error_struct_and_status(q):
+    import ctypes as C
+    from paper_2603_14641_b200 import _lib
+    h, err = C.c_void_p(), _lib.QasmError_t()
+    text = b"OPENQASM 2.0;\nqreg q[2];\n  cx q[0],q[0];\n"
+    st = _lib.lib.qsr_parse_qasm(text, len(text), C.byref(h), C.byref(err))
+    assert st == _lib.PARSE_ERROR and (err.line, err.column) == (3, 15)
+    assert _lib.lib.qsr_last_error().decode() == "qasm:3:15: two-qubit gate with identical operands"
