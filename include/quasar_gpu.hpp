@@ -10,13 +10,14 @@
 //
 // Signatures, results (bit-exact) and exception types are the reference's: the C ABI status
 // is rethrown as std::invalid_argument / std::out_of_range / std::logic_error, parse errors as
-// quasar::QasmError with the reference's line / column. Tableau-valued calls take the word type
-// uint64_t (the reference default); sample<W> takes every W of the reference. Host
-// Tableau<uint64_t> arguments are uploaded, processed on the GPU and downloaded in the
-// reference's own storage layout.
+// quasar::QasmError with the reference's line / column. Every word type W of the reference is
+// accepted: the engine computes on 64-bit words and Tableau<W> / ShotRecord<W> are exact
+// repackings of the same bits (ColumnMajor tableaux). Host tableaux are uploaded, processed on
+// the GPU and downloaded in the reference's own storage layout.
 #ifndef QUASAR_GPU_HPP_
 #define QUASAR_GPU_HPP_
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -105,6 +106,54 @@ inline void download(qsr_tableau *h, Tableau<uint64_t> &t) {
     check(qsr_tableau_download(h, t.x_plane().data(), t.z_plane().data(), t.signs().data()));
 }
 
+// Tableau<W> <-> Tableau<uint64_t>, ColumnMajor (tableau.hpp:51-61): the generator bits of every
+// qubit row are the same bit string in either word size, so W-words are the 64-bit words' W-bit
+// pieces (little-endian order); rows and words past n stay zero padding in both.
+template <Word W>
+Tableau<W> from64(const Tableau<uint64_t> &a) {
+    if (a.layout() != Layout::ColumnMajor) throw std::logic_error("quasar::gpu: ColumnMajor expected");
+    const size_t n = a.num_qubits(), k64 = a.num_words();
+    Tableau<W> b(n);
+    const size_t kw = b.num_words();
+    constexpr size_t bits = 8 * sizeof(W), per = 64 / bits;
+    auto piece = [&](const std::vector<uint64_t> &v, size_t base, size_t jw) {
+        return static_cast<W>(v[base + jw / per] >> (bits * (jw % per)));
+    };
+    for (size_t q = 0; q < n; ++q)
+        for (size_t h = 0; h < 2; ++h)
+            for (size_t jw = 0; jw < kw; ++jw) {
+                b.x_plane()[q * 2 * kw + h * kw + jw] = piece(a.x_plane(), q * 2 * k64 + h * k64, jw);
+                b.z_plane()[q * 2 * kw + h * kw + jw] = piece(a.z_plane(), q * 2 * k64 + h * k64, jw);
+            }
+    for (size_t h = 0; h < 2; ++h)
+        for (size_t jw = 0; jw < kw; ++jw) b.signs()[h * kw + jw] = piece(a.signs(), h * k64, jw);
+    return b;
+}
+
+template <Word W>
+Tableau<uint64_t> to64(const Tableau<W> &b) {
+    if (b.layout() != Layout::ColumnMajor) throw std::invalid_argument("tableau must be ColumnMajor");
+    const size_t n = b.num_qubits(), kw = b.num_words();
+    Tableau<uint64_t> a(n);
+    const size_t k64 = a.num_words();
+    constexpr size_t bits = 8 * sizeof(W), per = 64 / bits;
+    auto put = [&](std::vector<uint64_t> &v, size_t base, size_t jw, W w) {
+        v[base + jw / per] |= uint64_t(w) << (bits * (jw % per));
+    };
+    std::fill(a.x_plane().begin(), a.x_plane().end(), 0);
+    std::fill(a.z_plane().begin(), a.z_plane().end(), 0);
+    std::fill(a.signs().begin(), a.signs().end(), 0);
+    for (size_t q = 0; q < b.padded_qubits() && q < a.padded_qubits(); ++q)
+        for (size_t h = 0; h < 2; ++h)
+            for (size_t jw = 0; jw < kw; ++jw) {
+                put(a.x_plane(), q * 2 * k64 + h * k64, jw, b.x_plane()[q * 2 * kw + h * kw + jw]);
+                put(a.z_plane(), q * 2 * k64 + h * k64, jw, b.z_plane()[q * 2 * kw + h * kw + jw]);
+            }
+    for (size_t h = 0; h < 2; ++h)
+        for (size_t jw = 0; jw < kw; ++jw) put(a.signs(), h * k64, jw, b.signs()[h * kw + jw]);
+    return a;
+}
+
 inline RunReport report(const qsr_run_report &r) {
     RunReport o;
     o.timers.to_seconds = r.timers.to_seconds;
@@ -137,19 +186,29 @@ inline SingleShotResult<uint64_t> run(const Circuit &c, const Schedule *s, uint6
 }
 } // namespace detail
 
-// run_single_shot<uint64_t>(circuit, schedule, seed)   (simulator.hpp:46-70)
+// run_single_shot<W>(circuit, schedule, seed)   (simulator.hpp:46-70), every W: the engine runs
+// on 64-bit words; other word types get the same tableau bits repacked (records are word-size
+// independent, test_measure.cpp:315-335).
 template <Word W>
 SingleShotResult<W> run_single_shot(const Circuit &circuit, const Schedule &schedule,
                                     uint64_t seed) {
-    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
-    return detail::run(circuit, &schedule, seed);
+    if constexpr (std::is_same_v<W, uint64_t>) {
+        return detail::run(circuit, &schedule, seed);
+    } else {
+        auto r = detail::run(circuit, &schedule, seed);
+        return {detail::from64<W>(r.tableau), std::move(r.record), r.report};
+    }
 }
 
-// run_single_shot<uint64_t>(circuit, seed)   (simulator.hpp:72-76)
+// run_single_shot<W>(circuit, seed)   (simulator.hpp:72-76)
 template <Word W>
 SingleShotResult<W> run_single_shot(const Circuit &circuit, uint64_t seed) {
-    static_assert(std::is_same_v<W, uint64_t>, "quasar::gpu supports W = uint64_t");
-    return detail::run(circuit, nullptr, seed);
+    if constexpr (std::is_same_v<W, uint64_t>) {
+        return detail::run(circuit, nullptr, seed);
+    } else {
+        auto r = detail::run(circuit, nullptr, seed);
+        return {detail::from64<W>(r.tableau), std::move(r.record), r.report};
+    }
 }
 
 // schedule_windows(circuit, mode)   (schedule.hpp:51-137)
@@ -191,6 +250,14 @@ inline Circuit generate_random(uint32_t n, uint32_t depth, uint64_t seed, double
 }
 
 // apply_window(tableau, window)   (gates.hpp:147-197)
+inline void apply_window(Tableau<uint64_t> &t, const Window &window);
+template <Word W, typename = std::enable_if_t<!std::is_same_v<W, uint64_t>>>
+void apply_window(Tableau<W> &t, const Window &window) {
+    if (window.is_measurement) throw std::invalid_argument("apply_window: window contains measurements");
+    auto t64 = detail::to64(t);
+    apply_window(t64, window);
+    t = detail::from64<W>(t64);
+}
 inline void apply_window(Tableau<uint64_t> &t, const Window &window) {
     if (window.is_measurement)
         throw std::invalid_argument("apply_window: window contains measurements");
@@ -206,7 +273,19 @@ inline void apply_window(Tableau<uint64_t> &t, const Window &window) {
 // the number of probabilistic collapses, as in the reference.
 inline void measure_window(Tableau<uint64_t> &t, const Window &window, RandomStream &rng,
                            MeasurementRecord &record, MeasureScratch<uint64_t> &,
-                           PhaseTimers *timers = nullptr) {
+                           PhaseTimers *timers = nullptr);
+template <Word W, typename = std::enable_if_t<!std::is_same_v<W, uint64_t>>>
+void measure_window(Tableau<W> &t, const Window &window, RandomStream &rng, MeasurementRecord &record,
+                    MeasureScratch<W> &, PhaseTimers *timers = nullptr) {
+    if (!window.is_measurement) throw std::invalid_argument("measure_window: not a measurement window");
+    auto t64 = detail::to64(t);
+    MeasureScratch<uint64_t> scratch;
+    measure_window(t64, window, rng, record, scratch, timers);
+    t = detail::from64<W>(t64);
+}
+inline void measure_window(Tableau<uint64_t> &t, const Window &window, RandomStream &rng,
+                           MeasurementRecord &record, MeasureScratch<uint64_t> &,
+                           PhaseTimers *timers) {
     if (t.layout() != Layout::ColumnMajor)
         throw std::invalid_argument("measure_window: tableau must be ColumnMajor");
     if (!window.is_measurement)
@@ -295,14 +374,20 @@ inline std::string emit_qasm(const Circuit &circuit) {
     return out;
 }
 
-// Tableau::check_group_validity()   (tableau.hpp:184-213) on the device.
-inline std::string check_group_validity(const Tableau<uint64_t> &t) {
+// Tableau::check_group_validity()   (tableau.hpp:184-213) on the device, every W.
+template <Word W>
+std::string check_group_validity(const Tableau<W> &tw) {
+    if constexpr (!std::is_same_v<W, uint64_t>) {
+        return check_group_validity(detail::to64(tw));
+    } else {
+    const Tableau<uint64_t> &t = tw;
     auto h = detail::upload(t);
     uint64_t len = 0;
     check(qsr_tableau_check_validity(h.get(), nullptr, 0, &len));
     std::string out(len, '\0');
     check(qsr_tableau_check_validity(h.get(), out.data(), len, &len));
     return out;
+    }
 }
 
 } // namespace quasar::gpu

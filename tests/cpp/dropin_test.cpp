@@ -119,6 +119,33 @@ int main() {
             CHECK(rc.probabilistic_count == rg.probabilistic_count);
         }
     }
+    // run_single_shot / apply_window / measure_window / check_group_validity for the other W
+    for (uint64_t seed = 0; seed < 6; ++seed) {
+        const uint32_t n = 3 + uint32_t(seed * 23);
+        Circuit c = generate_random(n, 8 + uint32_t(seed), 700 + seed, 0.5);
+        auto a8 = run_single_shot<uint8_t>(c, seed);
+        auto b8 = gpu::run_single_shot<uint8_t>(c, seed);
+        CHECK(a8.tableau == b8.tableau && same_record(a8.record, b8.record));
+        auto a32 = run_single_shot<uint32_t>(c, seed);
+        auto b32 = gpu::run_single_shot<uint32_t>(c, seed);
+        CHECK(a32.tableau == b32.tableau && same_record(a32.record, b32.record));
+        CHECK(gpu::check_group_validity(b32.tableau) == "valid");
+        Schedule s = schedule_windows(c, ScheduleMode::single_shot);
+        auto ta = Tableau<uint16_t>::zero_state(n), tb = Tableau<uint16_t>::zero_state(n);
+        RandomStream ra(seed, kStreamMeasure), rb(seed, kStreamMeasure);
+        MeasurementRecord ma, mb;
+        MeasureScratch<uint16_t> sa, sb;
+        for (const Window &w : s.windows) {
+            if (w.is_measurement) {
+                measure_window(ta, w, ra, ma, sa);
+                gpu::measure_window(tb, w, rb, mb, sb);
+            } else {
+                apply_window(ta, w);
+                gpu::apply_window(tb, w);
+            }
+        }
+        CHECK(ta == tb && same_record(ma, mb) && ra.next_word() == rb.next_word());
+    }
     // sample<W> for the reference's other word types
     for (uint64_t seed = 0; seed < 3; ++seed) {
         Circuit c = generate_random(uint32_t(6 + seed * 7), 12, 300 + seed, 0.7);
