@@ -82,3 +82,18 @@ def test_sample_empty_and_unmeasured(q, oracle):
 
 def test_geometry_helper_consistent():
     assert geometry(64) == (1, 64) and geometry(65) == (2, 128)
+
+
+def test_shot_word_keying_prefix(q):
+    """test_frames.cpp:188-196: a 64-shot run is a prefix of the 128-shot run (the Z frames are
+    keyed by (seed, qubit, shot-word), not by the shot count); also across word sizes."""
+    c = q.generate_random(6, 10, 91, 1.0)
+    small = q.sample(c, 64, 1234)
+    big = q.sample(c, 128, 1234)
+    assert small.measured == big.measured
+    for r in range(len(small.measured)):
+        for shot in range(64):
+            assert small.bit(r, shot) == big.bit(r, shot)
+    # deterministic in (circuit, shots, seed)
+    again = q.sample(c, 128, 1234)
+    assert np.array_equal(again.words, big.words)
