@@ -3,6 +3,8 @@
 #include <nccl.h>
 
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "device.hpp"
@@ -128,6 +130,30 @@ void nccl_check(ncclResult_t r, const char *what) {
     fail(QSR_NCCL_ERROR, std::string(what) + ": " + m);
 }
 
+// Communicators are cached per (unique id, world, rank, device): a ncclUniqueId's bootstrap
+// root serves exactly one ncclCommInitRank round, so an engine rebuilt with the same id (bench.py
+// recreates the sharded engine every e2e step) must reuse the communicator instead of
+// re-initialising — a second init on a spent id would wait for the root forever. Engines sharing
+// a communicator run one after another (calls are synchronous), never concurrently.
+std::mutex g_comm_mu;
+std::map<std::string, ncclComm_t> g_comms;
+
+ncclComm_t comm_for(int w, int rank, const void *uid) {
+    int dev = 0;
+    QSR_CUDA(cudaGetDevice(&dev));
+    std::string key(static_cast<const char *>(uid), sizeof(ncclUniqueId));
+    key += ":" + std::to_string(w) + ":" + std::to_string(rank) + ":" + std::to_string(dev);
+    std::lock_guard<std::mutex> g(g_comm_mu);
+    auto it = g_comms.find(key);
+    if (it != g_comms.end()) return it->second;
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    ncclComm_t c = nullptr;
+    nccl_check(nccl().CommInitRank(&c, w, id, rank), "ncclCommInitRank");
+    g_comms.emplace(key, c);
+    return c;
+}
+
 class NcclExchange final : public Exchange {
   public:
     NcclExchange(int w, int rank, cudaStream_t st, const void *uid) {
@@ -135,13 +161,9 @@ class NcclExchange final : public Exchange {
         world = w;
         ranks = {rank};
         streams = {st};
-        ncclUniqueId id;
-        std::memcpy(&id, uid, sizeof(id));
-        nccl_check(nccl().CommInitRank(&comm, w, id, rank), "ncclCommInitRank");
+        comm = comm_for(w, rank, uid);
     }
-    ~NcclExchange() override {
-        if (comm && nccl().CommDestroy) nccl().CommDestroy(comm);
-    }
+    ~NcclExchange() override = default; // the communicator stays cached (see comm_for)
     void broadcast(const std::vector<void *> &buf, size_t bytes, int root) override {
         nccl_check(nccl().Broadcast(buf[0], buf[0], bytes, ncclUint8, root, comm, streams[0]),
                    "ncclBroadcast");

@@ -111,6 +111,32 @@ def test_sharded_nccl_transport_single_rank(q, oracle):
     np.testing.assert_array_equal(gs, s)
 
 
+def test_sharded_nccl_engine_rebuilt_with_same_id(q):
+    """bench.py rebuilds the NCCL-sharded engine with one ncclUniqueId (timed steps, then every
+    e2e step): the communicator is reused, never re-initialised on the spent id (which would
+    wait for the bootstrap root forever). Run in a subprocess under a timeout."""
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np\n"
+        "sys.path.insert(0, '.')\n"
+        "from paper_2603_14641_b200 import quasar as q\n"
+        "c = q.generate_random(200, 20, 3, 0.5)\n"
+        "uid = q.nccl_unique_id()\n"
+        "recs = []\n"
+        "for _ in range(3):\n"
+        "    e = q.ShardedEngine(c, 1, exchange='nccl', rank=0, nccl_id=uid)\n"
+        "    e.run(5)\n"
+        "    recs.append(e.record())\n"
+        "    del e\n"
+        "assert all(np.array_equal(r, recs[0]) for r in recs)\n"
+        "print('ok')\n")
+    root = __import__("pathlib").Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert "ok" in out.stdout
+
+
 @pytest.mark.parametrize("shots", [64, 130, 1000, 4100])
 def test_sample_sharded_by_shot(q, oracle, shots):
     """Sampling sharded by shot-word (one rank per GPU in production): the ranks' record
