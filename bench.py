@@ -270,7 +270,8 @@ def main():
     # download into pinned memory; N > 1 -> ShardedEngine create (schedule + upload per rank),
     # run, record download and this rank's tableau columns.
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
-    plane = n_pad * 2 * k
+    # Host buffers: the full tableau at N = 1; each rank's own columns (1/N of it) at N > 1.
+    plane = n_pad * 2 * k if world == 1 else n_pad * 2 * kg_local
     px, pz = C.c_void_p(), C.c_void_p()
     _lib.check(_lib.lib.qsr_host_alloc(plane * 8, C.byref(px)))
     _lib.check(_lib.lib.qsr_host_alloc(plane * 8, C.byref(pz)))
@@ -284,8 +285,12 @@ def main():
             e = make_engine()
             e.run(run_seed)
             _lib.check(_lib.lib.qsr_sharded_record(e._h, _lib.ptr(rec)))
-            _lib.check(_lib.lib.qsr_sharded_tableau(e._h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
-                                                    _lib.ptr(ps, C.c_uint64)))
+            if world > 1:  # this rank's columns, compact
+                _lib.check(_lib.lib.qsr_sharded_tableau_local(e._h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
+                                                              _lib.ptr(ps, C.c_uint64)))
+            else:  # local shards of one process: the full reference layout
+                _lib.check(_lib.lib.qsr_sharded_tableau(e._h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),
+                                                        _lib.ptr(ps, C.c_uint64)))
             del e
         else:
             rep = _lib.Report_t()
@@ -303,7 +308,7 @@ def main():
     e2e_total = qd.max_over_ranks(dist, float(np.sum(e2e_s))) if e2e_steps else float("nan")
     e2e_value = G * e2e_steps / e2e_total if e2e_steps else None
     h2d = world * (8 * G + 4 * nm)
-    d2h = world * 8 * nm + 2 * 8 * plane + 8 * 2 * k
+    d2h = world * 8 * nm + 2 * 8 * (n_pad * 2 * k) + 8 * 2 * k  # all ranks together: the tableau once
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

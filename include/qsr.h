@@ -309,6 +309,10 @@ qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record);
 /* Writes the generator-word columns of this process's shards into full-size reference-layout
  * CM buffers (x, z: n_pad*2k words; s: 2k words); other columns are left untouched. */
 qsr_status qsr_sharded_tableau(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s);
+/* This process's shards only, compact: per local shard (in rank order) a block of n_pad rows x
+ * 2kg words (its destabilizer words, then its stabilizer words) for x and z, and 2kg sign words
+ * — 1/world of the tableau per process, no full-size host buffers. */
+qsr_status qsr_sharded_tableau_local(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s);
 void qsr_sharded_destroy(qsr_sharded *e);
 
 #ifdef __cplusplus

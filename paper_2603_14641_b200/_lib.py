@@ -174,6 +174,7 @@ SIGNATURES = {
     "qsr_sharded_stats": (i32, [P, pd, pu64, pd, pd, pu64]),
     "qsr_sharded_record": (i32, [P, P]),
     "qsr_sharded_tableau": (i32, [P, pu64, pu64, pu64]),
+    "qsr_sharded_tableau_local": (i32, [P, pu64, pu64, pu64]),
     "qsr_sharded_destroy": (None, [P]),
 }
 

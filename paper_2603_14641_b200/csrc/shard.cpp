@@ -369,6 +369,28 @@ qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record) {
     });
 }
 
+qsr_status qsr_sharded_tableau_local(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        QSR_CUDA(cudaSetDevice(e->device));
+        const uint64_t n_pad = 64 * e->k;
+        uint64_t xo = 0, so = 0;
+        for (const Shard &sd : e->sh) {
+            DeviceTableau &t = *sd.t;
+            if (t.layout != QSR_COLUMN_MAJOR) fail(QSR_INTERNAL, "sharded tableau not ColumnMajor");
+            const uint64_t w = 2 * t.kg; // destabilizer words then stabilizer words of this shard
+            if (x) QSR_CUDA(cudaMemcpy2DAsync(x + xo, w * 8, t.x, t.cm_pitch * 8, w * 8, n_pad,
+                                              cudaMemcpyDeviceToHost, t.stream));
+            if (z) QSR_CUDA(cudaMemcpy2DAsync(z + xo, w * 8, t.z, t.cm_pitch * 8, w * 8, n_pad,
+                                              cudaMemcpyDeviceToHost, t.stream));
+            if (s) QSR_CUDA(cudaMemcpyAsync(s + so, t.s, w * 8, cudaMemcpyDeviceToHost, t.stream));
+            xo += n_pad * w;
+            so += w;
+            t.sync();
+        }
+    });
+}
+
 qsr_status qsr_sharded_tableau(const qsr_sharded *e, uint64_t *x, uint64_t *z, uint64_t *s) {
     return guard([&] {
         REQUIRE_PTR(e);

@@ -111,6 +111,36 @@ def test_sharded_nccl_transport_single_rank(q, oracle):
     np.testing.assert_array_equal(gs, s)
 
 
+def test_sharded_tableau_local_layout(q, oracle):
+    """qsr_sharded_tableau_local: per local shard, n_pad rows x 2kg words (destabilizer words
+    then stabilizer words) — the same words as the shard's columns of the full CM layout."""
+    import ctypes as C
+    from paper_2603_14641_b200 import _lib
+    n, world = 300, 3
+    c = q.generate_random(n, 20, 4, 0.5)
+    x, z, s, _, _ = oracle.run_single_shot(n, c.gate_array, 6)
+    e = q.ShardedEngine(c, world)
+    e.run(6)
+    k = (n + 63) // 64
+    n_pad = 64 * k
+    lx = np.zeros(n_pad * 2 * k, dtype=np.uint64)
+    lz = np.zeros_like(lx)
+    ls = np.zeros(2 * k, dtype=np.uint64)
+    _lib.check(_lib.lib.qsr_sharded_tableau_local(e._h, _lib.ptr(lx, C.c_uint64), _lib.ptr(lz, C.c_uint64),
+                                                  _lib.ptr(ls, C.c_uint64)))
+    X, Z = x.reshape(n_pad, 2 * k), z.reshape(n_pad, 2 * k)
+    xo = so = 0
+    for r in range(world):
+        j0, kg = q.shard_range(n, world, r)
+        cols = list(range(j0, j0 + kg)) + list(range(k + j0, k + j0 + kg))
+        blk = n_pad * 2 * kg
+        np.testing.assert_array_equal(lx[xo:xo + blk].reshape(n_pad, 2 * kg), X[:, cols])
+        np.testing.assert_array_equal(lz[xo:xo + blk].reshape(n_pad, 2 * kg), Z[:, cols])
+        np.testing.assert_array_equal(ls[so:so + 2 * kg], s[cols])
+        xo += blk
+        so += 2 * kg
+
+
 def test_sharded_nccl_engine_rebuilt_with_same_id(q):
     """bench.py rebuilds the NCCL-sharded engine with one ncclUniqueId (timed steps, then every
     e2e step): the communicator is reused, never re-initialised on the spent id (which would
