@@ -57,6 +57,7 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
     ds.wkind.clear();
     ds.mqubits.clear();
     ds.wwords.clear();
+    constexpr uint32_t kDeferredWords = ~0u; // gate-window words, computed after fusion in parallel
     auto gate_words = [](const uint64_t *g, size_t cnt) {
         uint32_t words = 0;
         for (size_t i = 0; i < cnt; ++i)
@@ -78,13 +79,13 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
     size_t held = SIZE_MAX; // start of the held window in `out` (it runs to out.size())
     auto flush_held = [&] {
         if (held == SIZE_MAX) return;
-        push_window(0, gate_words(out.data() + held, out.size() - held));
+        push_window(0, kDeferredWords);
         held = SIZE_MAX;
     };
     auto close_unitary = [&](size_t s0) {
         if (out.size() == s0) return;
         if (!pairing) {
-            push_window(0, gate_words(out.data() + s0, out.size() - s0));
+            push_window(0, kDeferredWords);
             return;
         }
         if (held == SIZE_MAX) {
@@ -94,7 +95,7 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         if (!pair_windows_of(s0 - held, out.size() - s0)) { // the held one goes alone, hold this one
             const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
             out.resize(s0);
-            push_window(0, gate_words(out.data() + held, s0 - held));
+            push_window(0, kDeferredWords);
             out.insert(out.end(), B.begin(), B.end());
             held = s0;
             return;
@@ -111,11 +112,11 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         }
         if (!po.rest_a.empty()) {
             out.insert(out.end(), po.rest_a.begin(), po.rest_a.end());
-            push_window(0, gate_words(po.rest_a.data(), po.rest_a.size()));
+            push_window(0, kDeferredWords);
         }
         if (!po.rest_b.empty()) {
             out.insert(out.end(), po.rest_b.begin(), po.rest_b.end());
-            push_window(0, gate_words(po.rest_b.data(), po.rest_b.size()));
+            push_window(0, kDeferredWords);
         }
     };
     for (size_t w = 0; w + 1 < offsets.size(); ++w) {
@@ -159,6 +160,14 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vect
         const std::vector<uint32_t> pm = f.permutation();
         perms.insert(perms.end(), pm.begin(), pm.end());
     }
+    // Bytes accounting of the gate windows, off the sequential fusion pass.
+    const uint64_t W = ds.wwords.size();
+    parallel_chunks(W, std::max(1u, std::min<unsigned>(host_threads(), unsigned(W / 8) + 1)),
+                    [&](unsigned, uint64_t b, uint64_t e) {
+                        for (uint64_t w = b; w < e; ++w)
+                            if (ds.wwords[w] == kDeferredWords)
+                                ds.wwords[w] = gate_words(out.data() + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+                    });
 }
 
 // Packed gates of a planned / validated schedule -> device (optionally through the gate fusion).
