@@ -122,7 +122,7 @@ struct Schedule {
 // Window plan of the O(G) scheduler: key = 2*round + is_measure per gate, the window
 // boundaries, and per-thread stable scatter offsets (see host_circuit.cpp).
 struct WindowPlan {
-    std::vector<uint32_t> key;
+    std::vector<uint32_t, NoInitAlloc<uint32_t>> key;
     uint64_t nkeys = 0;
     unsigned threads = 1;
     std::vector<uint64_t> chunk_offsets; // [threads][nkeys]

@@ -488,7 +488,11 @@ WindowPlan plan_windows(const Circuit &c) {
     const uint64_t G = c.gates.size();
     const uint32_t n = c.num_qubits;
     WindowPlan p;
-    p.key.resize(G);
+    p.key.resize(G); // no zero fill (NoInitAlloc); first touch in parallel, off the serial scan
+    parallel_chunks(G, std::max(1u, std::min<unsigned>(host_threads(), unsigned(G >> 22) + 1)),
+                    [&](unsigned, uint64_t b, uint64_t e) {
+                        if (e > b) std::memset(p.key.data() + b, 0, (e - b) * sizeof(uint32_t));
+                    });
     // wire state = round << 1 | (last gate on the wire was a MEASURE)
     std::vector<uint32_t> wire(n, 0);
     uint32_t max_round = 0, dup = 0;
