@@ -3,6 +3,7 @@
 #include "fuse.hpp"
 #include "pair.hpp"
 
+#include <cstring>
 #include <algorithm>
 #include <thread>
 
@@ -47,7 +48,7 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
 // Fuser, pending single-qubit operations are flushed in a window of their own before every
 // measurement window and at the end, and the rows return to logical order before every
 // measurement window (perm_at). Windows that end up empty are dropped.
-void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, std::vector<uint64_t> &out,
+void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &out,
                std::vector<uint32_t> &perms) {
     Fuser f(n);
     const std::vector<uint64_t> offsets = ds.offsets;
@@ -176,11 +177,18 @@ void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint6
     QSR_CUDA(cudaSetDevice(device));
     const uint64_t *dev_gates = packed;
     uint64_t DG = G;
-    std::vector<uint64_t> fused;
+    WordVec fused;
     if (fuse && fusion_enabled()) {
         TraceScope tr("  fuse");
         std::vector<uint32_t> perms;
-        fused.reserve(G);
+        // First-touch the output pages on all host threads (the fusion pass itself is sequential
+        // and would otherwise take every page fault of a G-word buffer on one core).
+        fused.resize(G);
+        parallel_chunks(G, std::max(1u, std::min<unsigned>(host_threads(), unsigned(G >> 16) + 1)),
+                        [&](unsigned, uint64_t b, uint64_t e) {
+                            if (e > b) memset(fused.data() + b, 0, (e - b) * 8);
+                        });
+        fused.resize(0);
         fuse_into(ds, n, packed, fused, perms);
         dev_gates = fused.data();
         DG = fused.size();

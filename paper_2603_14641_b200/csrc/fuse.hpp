@@ -21,6 +21,8 @@
 #include <cstdint>
 #include <vector>
 
+#include "host.hpp"
+
 namespace qsr {
 
 // Host copies of the 24-element group (same encoding as common.cuh kCliff1).
@@ -37,9 +39,9 @@ class Fuser {
   public:
     explicit Fuser(uint32_t n);
     // One unitary window of packed logical gates -> packed physical device gates (appended).
-    void unitary(const uint64_t *in, uint64_t cnt, std::vector<uint64_t> &out);
+    void unitary(const uint64_t *in, uint64_t cnt, WordVec &out);
     // All pending single-qubit operations as K_C1 gates (appended; one window's worth).
-    void flush(std::vector<uint64_t> &out);
+    void flush(WordVec &out);
     bool pending() const { return !pend_list_.empty(); }
     uint32_t phys(uint32_t q) const { return st_[q].pi; }
     std::vector<uint32_t> permutation() const; // logical -> physical

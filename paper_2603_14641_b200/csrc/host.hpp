@@ -31,6 +31,7 @@ struct NoInitAlloc : std::allocator<T> {
     void construct(U *p, A &&...a) { ::new (static_cast<void *>(p)) U(std::forward<A>(a)...); }
 };
 using GateVec = std::vector<qsr_gate, NoInitAlloc<qsr_gate>>;
+using WordVec = std::vector<uint64_t, NoInitAlloc<uint64_t>>; // packed device gate words
 
 // Host-side phase trace: QSR_TRACE=1 prints "[qsr] phase ms" lines to stderr (wall clock of the
 // calling thread; device work inside a phase is synchronised by the phase itself).

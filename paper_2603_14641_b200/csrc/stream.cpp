@@ -129,7 +129,7 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             QSR_CUDA(cudaSetDevice(t.device));
             const bool fuse = fusion_enabled();
             Fuser fuser(fuse ? n : 0);
-            std::vector<uint64_t> dev; // device gates of the window being emitted
+            WordVec dev; // device gates of the window being emitted
             std::vector<uint8_t> flags;
             std::vector<uint32_t> mq;
             uint64_t next_key = 2, dev_off = 0, rec_off = 0;
@@ -191,9 +191,9 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             // Window pairing (pair.hpp): each finished unitary window is held until the next.
             const bool pairing = fuse && pairing_enabled() && !gate_segment_enabled() && !frames;
             Pairer pairer(pairing ? n : 0);
-            std::vector<uint64_t> held;
+            WordVec held;
             PairOut po;
-            auto unitary_window = [&](std::vector<uint64_t> &w) {
+            auto unitary_window = [&](WordVec &w) {
                 if (w.empty()) return;
                 if (!pairing) {
                     launch_staged(w.data(), w.size());
