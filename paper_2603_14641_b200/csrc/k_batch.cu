@@ -209,7 +209,19 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
             break;
         }
         const uint32_t c = s_min;
-        if (tid == 0) {
+        // A pivot from the window: its owner holds the batch-start column bits and the
+        // memberships so far in registers (no dependent global load on the sequential chain).
+#pragma unroll
+        for (int u = 0; u < kSelRows; ++u) {
+            if (row[u] == c) {
+                uint32_t vb = cb[u];
+                for (uint32_t U = M[u]; U; U &= U - 1) vb ^= s_vb[__ffs(U) - 1];
+                s_vb[m] = vb;
+                s_c[m] = c;
+                s_mc[m] = M[u];
+            }
+        }
+        if (tid == 0 && c >= s_next) { // found by the fallback scan after the window
             const uint32_t cbc = colbits[ng + c];
             const uint32_t Mc = membership(cbc, s_vbcol, 0, m);
             uint32_t vb = cbc;
@@ -344,26 +356,34 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
         s_coin[lane] = draw_coin(seed, idx0 + lane, coin_table);
     }
     __syncwarp();
-    if (lane == 0) {
-        bool odd = false;
-        for (uint32_t m = 0; m < len; ++m) {
-            int E = s_e[m];
-            uint32_t sign = s_ss[m];
-            for (uint32_t U = s_mc[m]; U; U &= U - 1) {
-                const uint32_t j = __ffs(U) - 1;
-                E += int(s_beta[j]);
-                sign ^= s_vsign[j];
-            }
-            odd |= (E & 1) != 0;
-            s_vsign[m] = sign ^ ((uint32_t(E) >> 1) & 1u);
-            // Replaced pair: D_c <- sign of V_m, S_c <- coin (same 64-bit words possible: serial).
-            const uint64_t c = s_c[m], rs = ng + c;
-            s[c >> 6] = (s[c >> 6] & ~(1ull << (c & 63))) | (uint64_t(s_vsign[m]) << (c & 63));
-            s[rs >> 6] = (s[rs >> 6] & ~(1ull << (rs & 63))) | (uint64_t(s_coin[m]) << (rs & 63));
-        }
-        if (odd) atomicExch(err, 1);
-        *coin_index = idx0 + len;
+    // Lane m: E_m + sum_{j in Mc_m} beta(V_j) needs no chain (beta(V_j) is known for every j);
+    // the signs are a unit-triangular GF(2) system, solved one ballot per collapse.
+    uint32_t mc = 0, base = 0;
+    bool odd = false;
+    if (lane < len) {
+        mc = s_mc[lane];
+        int E = s_e[lane];
+        for (uint32_t U = mc; U; U &= U - 1) E += int(s_beta[__ffs(U) - 1]);
+        odd = (E & 1) != 0;
+        base = s_ss[lane] ^ ((uint32_t(E) >> 1) & 1u);
     }
+    uint32_t vs = 0; // bit j = sign of V_j
+    for (uint32_t m = 0; m < len; ++m) {
+        const uint32_t bit = __shfl_sync(0xffffffffu, base ^ parity32(mc & vs), m);
+        vs |= bit << m;
+    }
+    if (lane < len) {
+        s_vsign[lane] = (vs >> lane) & 1u;
+        // Replaced pair: D_c <- sign of V_m, S_c <- coin. The c_m are distinct, so every lane owns
+        // its two bits; lanes sharing a 64-bit word combine through bitwise atomics.
+        const uint64_t c = s_c[lane], rs = ng + c;
+        const unsigned long long bc = 1ull << (c & 63), br = 1ull << (rs & 63);
+        auto *sw = reinterpret_cast<unsigned long long *>(s);
+        if ((vs >> lane) & 1u) atomicOr(sw + (c >> 6), bc); else atomicAnd(sw + (c >> 6), ~bc);
+        if (s_coin[lane]) atomicOr(sw + (rs >> 6), br); else atomicAnd(sw + (rs >> 6), ~br);
+    }
+    if (__any_sync(0xffffffffu, odd) && lane == 0) atomicExch(err, 1);
+    if (lane == 0) *coin_index = idx0 + len;
     __syncwarp();
     if (lane < len) {
         out[fidx[lane]] = qsr_record_entry{fq[lane], uint8_t(s_coin[lane]), 0};
