@@ -45,6 +45,10 @@ enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_M
 static_assert(5 * kB == kVinfoWords, "vinfo layout");
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
 
 // Membership vector of a row given its batch-start column bits `cb` (bit m = X at q_m),
 // the per-collapse VB columns and the first collapse it can take part in.
@@ -284,21 +288,44 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
     const uint64_t i = uint64_t(blockIdx.x) * kRowThreads + tid;
     const bool act = i < pitch;
     // All pivot rows' batch-start words first (independent loads, all in flight at once).
+    // (cp.async: one DRAM round trip for all of them, no registers held per load.)
     for (uint32_t m = 0; m < len; ++m) {
         const uint64_t rs = ng + s_c[m];
-        sv[m][0][tid] = act ? __ldcg(x + rs * pitch + i) : 0ull;
-        sv[m][1][tid] = act ? __ldcg(z + rs * pitch + i) : 0ull;
+        if (act) {
+            cp_async8(&sv[m][0][tid], x + rs * pitch + i);
+            cp_async8(&sv[m][1][tid], z + rs * pitch + i);
+        } else {
+            sv[m][0][tid] = 0ull;
+            sv[m][1][tid] = 0ull;
+        }
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::); // each thread reads back only its own words
     for (uint32_t m = 0; m < len; ++m) {
         u64 cx = sv[m][0][tid], cz = sv[m][1][tid];
         int e = __popcll(cx & cz);
         u64 acc = 0;
-        for (uint32_t U = s_mc[m]; U; U &= U - 1) {
-            const uint32_t j = __ffs(U) - 1;
-            const u64 vx = sv[j][0][tid], vz = sv[j][1][tid];
-            acc ^= vz & cx;
-            cx ^= vx;
-            cz ^= vz;
+        uint32_t U = s_mc[m];
+        if (U) { // the next member's words are read while this one is applied
+            uint32_t j = __ffs(U) - 1;
+            U &= U - 1;
+            u64 vx = sv[j][0][tid], vz = sv[j][1][tid];
+            for (;;) {
+                const bool more = U != 0;
+                u64 nx = 0, nzv = 0;
+                if (more) {
+                    j = __ffs(U) - 1;
+                    U &= U - 1;
+                    nx = sv[j][0][tid];
+                    nzv = sv[j][1][tid];
+                }
+                acc ^= vz & cx;
+                cx ^= vx;
+                cz ^= vz;
+                if (!more) break;
+                vx = nx;
+                vz = nzv;
+            }
         }
         const int bend = __popcll(cx & cz);
         e += 2 * (__popcll(acc) & 1) - bend;
