@@ -126,7 +126,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
     __shared__ uint32_t s_scan[kSelThreads / 32];
-    __shared__ uint32_t s_nwin, s_next, s_min, s_len, s_stop;
+    __shared__ uint32_t s_nwin, s_next, s_minb[2], s_len, s_stop;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nzw = (n_gen + 31) / 32;
     if (tid < kB) s_vbcol[tid] = 0;
@@ -137,7 +137,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         if (tid == 0) { bctl[BL_LEN] = 0; bctl[BL_DET] = 0; bctl[BL_SKIP] = 1; }
         return;
     }
-    if (tid == 0) { s_nwin = 0; s_next = uint32_t(n_gen); s_len = b; s_stop = 0; }
+    if (tid == 0) { s_nwin = 0; s_next = uint32_t(n_gen); s_len = b; s_stop = 0; s_minb[0] = s_minb[1] = 0xFFFFFFFFu; }
     __syncthreads();
     // Window: the first kWin active stabilizers in ascending order.
     for (uint64_t base = 0; base < nzw; base += kSelThreads) {
@@ -165,30 +165,33 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         if (s_nwin >= uint32_t(kWin)) break;
     }
     const uint32_t nwin = s_nwin;
-    uint32_t row[kSelRows], cb[kSelRows], M[kSelRows];
+    // cur[u]: the candidate's current X bits at the batch's qubits (batch-start bits XOR the vb
+    // of every V it absorbed), so its bit at q_m is one shift and absorbing V_m one XOR.
+    uint32_t row[kSelRows], cur[kSelRows], M[kSelRows];
 #pragma unroll
     for (int u = 0; u < kSelRows; ++u) {
         const uint32_t e = tid + u * kSelThreads;
         row[u] = e < nwin ? s_rows[e] : 0xFFFFFFFFu;
-        cb[u] = e < nwin ? colbits[ng + row[u]] : 0u;
+        cur[u] = e < nwin ? colbits[ng + row[u]] : 0u;
         M[u] = 0;
     }
+    // Two barriers per collapse; s_minb is double-buffered (step m resets the other slot).
     for (uint32_t m = 0; m < b; ++m) {
-        if (tid == 0) s_min = 0xFFFFFFFFu;
-        __syncthreads();
-        const uint32_t vc = s_vbcol[m];
+        const uint32_t pm = m & 1u;
         uint32_t best = 0xFFFFFFFFu, bits = 0;
 #pragma unroll
         for (int u = 0; u < kSelRows; ++u) {
-            const uint32_t bit = ((cb[u] >> m) ^ parity32(M[u] & vc)) & 1u;
+            const uint32_t bit = (cur[u] >> m) & 1u;
             bits |= bit << u;
-            if (bit) best = min(best, row[u]); // used pivots hold no X bit any more (cb masked)
+            if (bit) best = min(best, row[u]); // used pivots are inert (cur = 0)
         }
         best = __reduce_min_sync(0xffffffffu, best);
-        if (lane == 0 && best != 0xFFFFFFFFu) atomicMin(&s_min, best);
+        if (lane == 0 && best != 0xFFFFFFFFu) atomicMin(&s_minb[pm], best);
         __syncthreads();
-        if (s_min == 0xFFFFFFFFu) {
+        if (tid == 0) s_minb[pm ^ 1u] = 0xFFFFFFFFu;
+        if (s_minb[pm] == 0xFFFFFFFFu) {
             // Fallback: stabilizers after the window, memberships from the column bits.
+            const uint32_t vc = s_vbcol[m];
             for (uint64_t g0r = s_next; g0r < n_gen; g0r += kSelThreads) {
                 const uint64_t g = g0r + tid;
                 uint32_t cand = 0xFFFFFFFFu;
@@ -202,25 +205,22 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
                     }
                 }
                 cand = __reduce_min_sync(0xffffffffu, cand);
-                if (lane == 0 && cand != 0xFFFFFFFFu) atomicMin(&s_min, cand);
+                if (lane == 0 && cand != 0xFFFFFFFFu) atomicMin(&s_minb[pm], cand);
                 __syncthreads();
-                if (s_min != 0xFFFFFFFFu) break;
+                if (s_minb[pm] != 0xFFFFFFFFu) break;
                 __syncthreads();
             }
         }
-        if (s_min == 0xFFFFFFFFu) { // no stabilizer anticommutes with Z_{q_m}: batch ends here
+        const uint32_t c = s_minb[pm];
+        if (c == 0xFFFFFFFFu) { // no stabilizer anticommutes with Z_{q_m}: batch ends here
             if (tid == 0) { s_len = m; s_stop = 1; }
             break;
         }
-        const uint32_t c = s_min;
-        // A pivot from the window: its owner holds the batch-start column bits and the
-        // memberships so far in registers (no dependent global load on the sequential chain).
+        // A pivot from the window: its owner holds cur and the memberships in registers.
 #pragma unroll
         for (int u = 0; u < kSelRows; ++u) {
             if (row[u] == c) {
-                uint32_t vb = cb[u];
-                for (uint32_t U = M[u]; U; U &= U - 1) vb ^= s_vb[__ffs(U) - 1];
-                s_vb[m] = vb;
+                s_vb[m] = cur[u];
                 s_c[m] = c;
                 s_mc[m] = M[u];
             }
@@ -235,13 +235,13 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
             s_mc[m] = Mc;
         }
         __syncthreads();
-        if (tid < kB) s_vbcol[tid] |= ((s_vb[m] >> tid) & 1u) << m;
+        const uint32_t vb = s_vb[m];
+        if (tid < kB) s_vbcol[tid] |= ((vb >> tid) & 1u) << m; // read by the fallback only
 #pragma unroll
         for (int u = 0; u < kSelRows; ++u) {
-            if (row[u] == c) { cb[u] = 0; M[u] = 0; row[u] = 0xFFFFFFFFu; } // now +/-Z_q: inert
-            else if ((bits >> u) & 1u) M[u] |= 1u << m;
+            if (row[u] == c) { cur[u] = 0; M[u] = 0; row[u] = 0xFFFFFFFFu; } // now +/-Z_q: inert
+            else if ((bits >> u) & 1u) { M[u] |= 1u << m; cur[u] ^= vb; }
         }
-        __syncthreads();
     }
     __syncthreads();
     const uint32_t len = s_len;
