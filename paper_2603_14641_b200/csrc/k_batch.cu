@@ -747,12 +747,14 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
     if (blockIdx.x >= row_blocks) {
-        const uint32_t j = blockIdx.x - row_blocks;
+        // Pair-parity row j over one word chunk (chunks x 256 threads stride the words); the
+        // chunks' partial rows are XOR-combined by k_batch_signs (no zeroing, no atomics).
+        const uint32_t e = blockIdx.x - row_blocks, j = e / kPmatChunks, ch = e % kPmatChunks;
         if (tid == 0) s_p = 0;
         __syncthreads();
         uint32_t mask = 0;
         if (j < len) {
-            for (uint64_t i = tid; i < k; i += blockDim.x) {
+            for (uint64_t i = uint64_t(ch) * blockDim.x + tid; i < k; i += uint64_t(kPmatChunks) * blockDim.x) {
                 const u64 vz = Vz[uint64_t(j) * vstride + i];
                 for (uint32_t jp = 0; jp < j; ++jp)
                     mask ^= (uint32_t(__popcll(vz & Vx[uint64_t(jp) * vstride + i])) & 1u) << jp;
@@ -761,7 +763,7 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
         mask = __reduce_xor_sync(0xffffffffu, mask);
         if ((tid & 31) == 0 && mask) atomicXor(&s_p, mask);
         __syncthreads();
-        if (tid == 0) pmat[j] = s_p;
+        if (tid == 0) pmat[j * kPmatChunks + ch] = s_p;
         return;
     }
     if (tid < kB) {
@@ -921,7 +923,12 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
         }
         s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
     }
-    if (tid < kB) s_p[tid] = tid < len ? pmat[tid] : 0u;
+    if (tid < kB) {
+        uint32_t p = 0;
+        if (tid < len)
+            for (uint32_t ch = 0; ch < kPmatChunks; ++ch) p ^= pmat[tid * kPmatChunks + ch];
+        s_p[tid] = p;
+    }
     __syncthreads();
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
     uint32_t f = 0;
@@ -1038,7 +1045,7 @@ void batch_apply(DeviceTableau &t) {
         ms.partial = static_cast<uint8_t *>(cache_acquire(t.device, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
-    k_batch_member<<<row_blocks + kB, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
+    k_batch_member<<<row_blocks + kB * kPmatChunks, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
                                                           ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl,
                                                           ms.gconst, row_blocks);
     QSR_CUDA(cudaGetLastError());
