@@ -796,20 +796,26 @@ __global__ void __launch_bounds__(kAThreads, 1)
 k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
                uint64_t nrows, const uint32_t *__restrict__ member,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
-               const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial) {
+               const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial, uint64_t stride) {
     extern __shared__ __align__(16) u64 tab[]; // [g][S][plane][kSlice]
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ngroups = (len + 3) / 4;
     const uint64_t nslices = (pitch + kSlice - 1) / kSlice;
-    const uint64_t total = nslices * nrows;
+    // Work items are (slice, row group of kARows rows). Within a slice, item u covers the rows of
+    // group (u * stride) mod nfull (a bijection, stride coprime with nfull; the tail group maps to
+    // itself): rows that absorb nothing (the growing block of collapsed stabilizers of a
+    // measure-all window) are spread over all CTAs instead of idling the few that own them.
+    const uint64_t ngr = (nrows + kARows - 1) / kARows, nfull = nrows / kARows;
+    const uint64_t total = nslices * ngr;
     const uint64_t item0 = total * blockIdx.x / gridDim.x, item1 = total * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t step = nfull ? (uint64_t(kAWarps) * stride) % nfull : 0;
     uint64_t it = item0;
     while (it < item1) {
-        const uint64_t sl = it / nrows;
-        const uint64_t r_begin = it - sl * nrows;
-        const uint64_t r_end = min(nrows, r_begin + (item1 - it));
+        const uint64_t sl = it / ngr;
+        const uint64_t g_begin = it - sl * ngr;
+        const uint64_t g_end = min(ngr, g_begin + (item1 - it));
         const uint64_t w0 = sl * kSlice;
         // Build the combination table of this slice.
         __syncthreads(); // previous slice's readers are done
@@ -837,24 +843,30 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         __syncthreads();
         const uint64_t i = w0 + 2 * lane;
         const bool act = i < pitch;
+        // Group u -> first row; pos tracks (u * stride) mod nfull incrementally.
+        uint64_t u = g_begin + warp;
+        uint64_t pos = nfull ? (u % nfull) * (stride % nfull) % nfull : 0;
+        auto first_row = [&](uint64_t uu, uint64_t pp) { return (uu < nfull ? pp : uu) * kARows; };
         // Memberships of the next row group are loaded one iteration ahead (their L2 round
         // trip overlaps this group's loads and table lookups).
         uint32_t Mn[kARows];
         {
-            const uint64_t b0 = r_begin + uint64_t(warp) * kARows;
+            const uint64_t b0 = first_row(u, pos);
 #pragma unroll
-            for (int q = 0; q < kARows; ++q) Mn[q] = b0 + q < r_end ? member[b0 + q] : 0u;
+            for (int q = 0; q < kARows; ++q) Mn[q] = u < g_end && b0 + q < nrows ? member[b0 + q] : 0u;
         }
-        for (uint64_t base = r_begin + uint64_t(warp) * kARows; base < r_end;
-             base += uint64_t(kAWarps) * kARows) {
+        for (; u < g_end; u += kAWarps) {
+            const uint64_t base = first_row(u, pos);
+            pos += step;
+            if (pos >= nfull) pos -= nfull;
+            const uint64_t un = u + kAWarps, nb = first_row(un, pos);
             uint32_t M[kARows];
             uint32_t U = 0;
-            const uint64_t nb = base + uint64_t(kAWarps) * kARows;
 #pragma unroll
             for (int q = 0; q < kARows; ++q) {
                 M[q] = Mn[q];
                 U |= M[q];
-                Mn[q] = nb + q < r_end ? member[nb + q] : 0u;
+                Mn[q] = un < g_end && nb + q < nrows ? member[nb + q] : 0u;
             }
             if (U == 0) continue;
             ulonglong2 x0[kARows], z0[kARows], dx[kARows], dz[kARows];
@@ -901,7 +913,7 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
             if (lane < kARows && M[lane] != 0u) // M[] is warp-uniform; lane q writes row q
                 partial[sl * nrows + base + lane] = uint8_t((packed >> (8 * lane)) & 3u);
         }
-        it += r_end - r_begin;
+        it += g_end - g_begin;
     }
 }
 
@@ -1015,6 +1027,15 @@ bool table_absorb() {
     return on;
 }
 
+// A stride coprime with the number of full row groups, near its golden section (k_batch_absorb).
+uint64_t absorb_stride(uint64_t nfull) {
+    if (nfull < 2) return 1;
+    uint64_t st = std::max<uint64_t>(1, uint64_t(double(nfull) * 0.6180339887));
+    auto gcd = [](uint64_t a, uint64_t b) { while (b) { const uint64_t t = a % b; a = b; b = t; } return a; };
+    while (gcd(st, nfull) != 1) ++st;
+    return st;
+}
+
 void batch_apply(DeviceTableau &t) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
@@ -1050,7 +1071,8 @@ void batch_apply(DeviceTableau &t) {
                                                           ms.gconst, row_blocks);
     QSR_CUDA(cudaGetLastError());
     k_batch_absorb<<<unsigned(t.num_sms), kAThreads, kAbsorbSmem, t.stream>>>(
-        t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial);
+        t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
+        absorb_stride(nrows / kARows));
     QSR_CUDA(cudaGetLastError());
     k_batch_signs<<<row_blocks, 256, 0, t.stream>>>(t.s, nrows, nslices, ms.colbits, ms.partial, ms.vinfo,
                                                     ms.bctl, ms.gconst, ms.err);
