@@ -803,14 +803,16 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t ngroups = (len + 3) / 4;
     const uint64_t nslices = (pitch + kSlice - 1) / kSlice;
-    // Work items are (slice, row group of kARows rows). Within a slice, item u covers the rows of
-    // group (u * stride) mod nfull (a bijection, stride coprime with nfull; the tail group maps to
-    // itself): rows that absorb nothing (the growing block of collapsed stabilizers of a
-    // measure-all window) are spread over all CTAs instead of idling the few that own them.
-    const uint64_t ngr = (nrows + kARows - 1) / kARows, nfull = nrows / kARows;
+    // Work items are (slice, row group of kARows rows). Within a slice, blocks of kAWarps
+    // consecutive groups (one per warp: 64 contiguous rows per CTA step, page-friendly) are
+    // visited in the order b -> (b * stride) mod nblk (a bijection, stride coprime with nblk; the
+    // tail groups map to themselves): rows that absorb nothing (the growing block of collapsed
+    // stabilizers of a measure-all window) spread over all CTAs instead of idling a few.
+    const uint64_t ngr = (nrows + kARows - 1) / kARows;
+    const uint64_t nblk = nrows / (uint64_t(kARows) * kAWarps), nmapped = nblk * kAWarps;
     const uint64_t total = nslices * ngr;
     const uint64_t item0 = total * blockIdx.x / gridDim.x, item1 = total * (blockIdx.x + 1) / gridDim.x;
-    const uint64_t step = nfull ? (uint64_t(kAWarps) * stride) % nfull : 0;
+    const uint64_t step = nblk ? stride % nblk : 0;
     uint64_t it = item0;
     while (it < item1) {
         const uint64_t sl = it / ngr;
@@ -843,10 +845,14 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         __syncthreads();
         const uint64_t i = w0 + 2 * lane;
         const bool act = i < pitch;
-        // Group u -> first row; pos tracks (u * stride) mod nfull incrementally.
+        // Group u -> first row; pos tracks ((u / kAWarps) * stride) mod nblk incrementally
+        // (u advances by kAWarps, so its block by one and its place in the block stays wq).
         uint64_t u = g_begin + warp;
-        uint64_t pos = nfull ? (u % nfull) * (stride % nfull) % nfull : 0;
-        auto first_row = [&](uint64_t uu, uint64_t pp) { return (uu < nfull ? pp : uu) * kARows; };
+        const uint64_t wq = u % kAWarps;
+        uint64_t pos = nblk ? ((u / kAWarps) % nblk) * step % nblk : 0;
+        auto first_row = [&](uint64_t uu, uint64_t pp) {
+            return (uu < nmapped ? pp * kAWarps + wq : uu) * kARows;
+        };
         // Memberships of the next row group are loaded one iteration ahead (their L2 round
         // trip overlaps this group's loads and table lookups).
         uint32_t Mn[kARows];
@@ -858,7 +864,7 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
         for (; u < g_end; u += kAWarps) {
             const uint64_t base = first_row(u, pos);
             pos += step;
-            if (pos >= nfull) pos -= nfull;
+            if (pos >= nblk) pos -= nblk;
             const uint64_t un = u + kAWarps, nb = first_row(un, pos);
             uint32_t M[kARows];
             uint32_t U = 0;
@@ -1027,7 +1033,7 @@ bool table_absorb() {
     return on;
 }
 
-// A stride coprime with the number of full row groups, near its golden section (k_batch_absorb).
+// A stride coprime with the number of full row blocks, near its golden section (k_batch_absorb).
 uint64_t absorb_stride(uint64_t nfull) {
     if (nfull < 2) return 1;
     uint64_t st = std::max<uint64_t>(1, uint64_t(double(nfull) * 0.6180339887));
@@ -1072,7 +1078,7 @@ void batch_apply(DeviceTableau &t) {
     QSR_CUDA(cudaGetLastError());
     k_batch_absorb<<<unsigned(t.num_sms), kAThreads, kAbsorbSmem, t.stream>>>(
         t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
-        absorb_stride(nrows / kARows));
+        absorb_stride(nrows / (uint64_t(kARows) * kAWarps)));
     QSR_CUDA(cudaGetLastError());
     k_batch_signs<<<row_blocks, 256, 0, t.stream>>>(t.s, nrows, nslices, ms.colbits, ms.partial, ms.vinfo,
                                                     ms.bctl, ms.gconst, ms.err);
