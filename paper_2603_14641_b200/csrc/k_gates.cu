@@ -205,6 +205,9 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
               const uint64_t *__restrict__ gates, uint32_t ngates, uint32_t chunk,
               uint64_t *__restrict__ partials, uint32_t *__restrict__ counters,
               uint64_t *__restrict__ s) {
+    // Programmatic dependent launch (launch_window_kernel): wait for the previous window to
+    // complete, then let the next one's CTAs take the SM slots this grid's tail frees.
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t j = uint64_t(blockIdx.x) * kTileWords + lane * 2;
     const bool active = j < pitch; // pitch % 16 == 0, so j+1 < pitch too
@@ -319,6 +322,16 @@ void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool sig
     *chunks_out = chunks;
 }
 
+// Gate windows launch with programmatic stream serialization (PDL): back-to-back windows overlap
+// the next launch with the previous grid's tail. QSR_PDL=0 restores plain launches.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("QSR_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <bool kSigns, int U, int B>
 void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *gates,
                     uint64_t ngates, int num_sms, cudaStream_t st, uint64_t **partials,
@@ -333,9 +346,24 @@ void launch_variant(uint64_t *x, uint64_t *z, uint64_t pitch, const uint64_t *ga
     uint64_t tiles, chunk, chunks;
     pick_chunks(pitch, ngates, num_sms, bps, kSigns, partials, partial_chunks, &tiles, &chunk, &chunks);
     dim3 grid{unsigned(tiles), unsigned(chunks)};
-    k_gate_window<kSigns, U, B><<<grid, kThreads, 0, st>>>(
-        x, z, pitch, gates, uint32_t(ngates), uint32_t(chunk), kSigns ? *partials : nullptr,
-        counters, s);
+    uint64_t *part = kSigns ? *partials : nullptr;
+    if (pdl_enabled()) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        QSR_CUDA(cudaLaunchKernelEx(&cfg, k_gate_window<kSigns, U, B>, x, z, pitch, gates,
+                                    uint32_t(ngates), uint32_t(chunk), part, counters, s));
+    } else {
+        k_gate_window<kSigns, U, B><<<grid, kThreads, 0, st>>>(x, z, pitch, gates, uint32_t(ngates),
+                                                               uint32_t(chunk), part, counters, s);
+    }
     QSR_CUDA(cudaGetLastError());
     count_launch();
 }
