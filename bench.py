@@ -83,6 +83,16 @@ class Clocks:
 
     def __exit__(self, *a):
         if self.proc:
+            # A timed region shorter than nvidia-smi's start-up + one period (c2: ~70 ms) has no
+            # sample yet: keep the sampler until its first row lands (at most ~3 s).
+            t0 = time.perf_counter()
+            while time.perf_counter() - t0 < 3.0 and self.proc.poll() is None:
+                try:
+                    if any(len(l.split(",")) >= 6 for l in self.path.read_text().splitlines()):
+                        break
+                except OSError:
+                    pass
+                time.sleep(0.02)
             self.proc.terminate()
             self.proc.wait()
 
