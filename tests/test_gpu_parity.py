@@ -299,13 +299,14 @@ def test_mixed_bell_and_random(q, oracle):
 @pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_GATE_ENGINE": "segment"},
                                  {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"}, {"QSR_APPLY": "rows"},
                                  {"QSR_PIVOTS": "fused"}, {"QSR_PAIR": "1", "QSR_STREAM": "0"},
-                                 {"QSR_PAIR": "1"}, {"QSR_GRAPHS": "0"}])
+                                 {"QSR_PAIR": "1"}, {"QSR_GRAPHS": "0"}, {"QSR_PDL": "0"}])
 def test_alternate_collapse_paths_match(q, env):
     """Every alternate path must agree with the default and the oracle: QSR_MEASURE_BATCH=0 (one
     collapse per pass), QSR_GATE_ENGINE=segment (temporally blocked gates), QSR_FUSE=0 (no gate
     fusion), QSR_STREAM=0 (schedule first, then run), QSR_APPLY=rows (row-major absorb, one V at
     a time), QSR_PIVOTS=fused (single-CTA pivot kernel), QSR_PAIR=1 (consecutive windows as
-    component records, k_gate_pairs)."""
+    component records, k_gate_pairs), QSR_GRAPHS=0 (no graph replay), QSR_PDL=0 (plain gate-window
+    launches instead of programmatic dependent launches)."""
     import subprocess
     import sys
     code = (
