@@ -29,6 +29,7 @@
 // rows are staged through shared memory (cp.async, double-buffered 64-word slices) and each
 // staged word is reused by the 4 rows a warp carries.
 #include <string>
+#include <utility>
 
 #include "common.cuh"
 #include "device.hpp"
@@ -45,6 +46,9 @@ enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_M
 static_assert(5 * kB == kVinfoWords, "vinfo layout");
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
+// Kernels of the batch chain launch with programmatic stream serialization (launch_chain): each
+// waits here for its predecessor before touching memory; the launch itself overlaps its tail.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
     const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
@@ -123,6 +127,7 @@ __global__ void __launch_bounds__(kSelThreads)
 k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
                uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
                uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect) {
+    pdl_wait();
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
     __shared__ uint32_t s_scan[kSelThreads / 32];
@@ -273,6 +278,7 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
              uint64_t g0, const uint32_t *__restrict__ fq, uint64_t *__restrict__ Vx,
              uint64_t *__restrict__ Vz, uint64_t vstride, const uint32_t *__restrict__ vinfo,
              const uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
+    pdl_wait();
     __shared__ u64 sv[kB][2][kRowThreads];
     __shared__ uint32_t s_c[kB], s_mc[kB], s_q[kB];
     __shared__ int8_t s_e[kB][kRowThreads], s_bend[kB][kRowThreads]; // per word: |e| <= 66, bend <= 64
@@ -368,6 +374,7 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
                const int *__restrict__ pcount, uint64_t seed,
                uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
                int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
+    pdl_wait();
     __shared__ uint32_t s_c[kB], s_mc[kB], s_ss[kB], s_coin[kB], s_vsign[kB], s_beta[kB];
     __shared__ int s_e[kB];
     const uint32_t lane = threadIdx.x;
@@ -742,6 +749,7 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
                uint32_t *__restrict__ pmat, uint32_t row_blocks) {
+    pdl_wait();
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
     __shared__ uint32_t s_p;
     const uint32_t len = bctl[BL_LEN];
@@ -797,6 +805,7 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                uint64_t nrows, const uint32_t *__restrict__ member,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial, uint64_t stride) {
+    pdl_wait();
     extern __shared__ __align__(16) u64 tab[]; // [g][S][plane][kSlice]
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
@@ -928,6 +937,7 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
               const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
               const uint32_t *__restrict__ pmat, int *__restrict__ err) {
+    pdl_wait();
     __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB];
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
@@ -971,10 +981,42 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
 
 } // namespace
 
+// QSR_PDL=0 restores plain launches for the batch chain (as for the gate windows).
+static bool chain_pdl() {
+    static const bool on = [] {
+        const char *e = getenv("QSR_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... P, typename... A>
+static void launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A &&...args) {
+    if (chain_pdl()) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = grid;
+        cfg.blockDim = block;
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        QSR_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...));
+    } else {
+        k<<<grid, block, smem, st>>>(std::forward<A>(args)...);
+    }
+    QSR_CUDA(cudaGetLastError());
+}
+
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     QSR_CUDA(cudaMemsetAsync(ms.bctl, 0, 16, t.stream));
+    // The pivot kernels' phase sums (zeroed here, ahead of the chain, so k_pivot_select follows
+    // k_colbits kernel-to-kernel).
+    QSR_CUDA(cudaMemsetAsync(ms.pcount, 0, 2 * kB * sizeof(int), t.stream));
     k_colbits<<<unsigned((nrows + 255) / 256), 256, 0, t.stream>>>(t.x, t.rm_pitch, nrows, t.ng, d_fq,
                                                                     b, ms.colbits, ms.bctl + BL_STAB_OR,
                                                                     ms.nz);
@@ -1003,16 +1045,14 @@ void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx
                   uint64_t seed, uint32_t *d_pos, uint32_t expect) {
     MeasureScratch &ms = t.ms;
     if (split_pivots()) {
-        QSR_CUDA(cudaMemsetAsync(ms.pcount, 0, 2 * kB * sizeof(int), t.stream));
-        k_pivot_select<<<1, kSelThreads, 0, t.stream>>>(ms.colbits, ms.nz, t.n_gen, t.ng, t.g0, b,
-                                                        ms.vinfo, ms.bctl, d_pos, expect);
-        QSR_CUDA(cudaGetLastError());
-        k_pivot_rows<<<unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads), kRowThreads, 0, t.stream>>>(
-            t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz, ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
-        QSR_CUDA(cudaGetLastError());
-        k_pivot_finish<<<1, 32, 0, t.stream>>>(t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo, ms.bctl, ms.pcount,
-                                               seed, ms.coin_index, ms.out, ms.err, ms.coin_table);
-        QSR_CUDA(cudaGetLastError());
+        // (ms.pcount was zeroed by batch_colbits, which always precedes on this tableau.)
+        launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
+                     t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect);
+        launch_chain(k_pivot_rows, dim3(unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads)),
+                     dim3(kRowThreads), 0, t.stream, t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz,
+                     ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
+        launch_chain(k_pivot_finish, dim3(1), dim3(32), 0, t.stream, t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo,
+                     ms.bctl, ms.pcount, seed, ms.coin_index, ms.out, ms.err, ms.coin_table);
         count_launch(3);
         return;
     }
@@ -1072,17 +1112,13 @@ void batch_apply(DeviceTableau &t) {
         ms.partial = static_cast<uint8_t *>(cache_acquire(t.device, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
-    k_batch_member<<<row_blocks + kB * kPmatChunks, 256, 0, t.stream>>>(ms.colbits, nrows, t.ng, t.g0, ms.Vx,
-                                                          ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl,
-                                                          ms.gconst, row_blocks);
-    QSR_CUDA(cudaGetLastError());
-    k_batch_absorb<<<unsigned(t.num_sms), kAThreads, kAbsorbSmem, t.stream>>>(
-        t.x, t.z, t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
-        absorb_stride(nrows / (uint64_t(kARows) * kAWarps)));
-    QSR_CUDA(cudaGetLastError());
-    k_batch_signs<<<row_blocks, 256, 0, t.stream>>>(t.s, nrows, nslices, ms.colbits, ms.partial, ms.vinfo,
-                                                    ms.bctl, ms.gconst, ms.err);
-    QSR_CUDA(cudaGetLastError());
+    launch_chain(k_batch_member, dim3(row_blocks + kB * kPmatChunks), dim3(256), 0, t.stream, ms.colbits,
+                 nrows, t.ng, t.g0, ms.Vx, ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl, ms.gconst, row_blocks);
+    launch_chain(k_batch_absorb, dim3(unsigned(t.num_sms)), dim3(kAThreads), kAbsorbSmem, t.stream, t.x, t.z,
+                 t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
+                 absorb_stride(nrows / (uint64_t(kARows) * kAWarps)));
+    launch_chain(k_batch_signs, dim3(row_blocks), dim3(256), 0, t.stream, t.s, nrows, nslices, ms.colbits,
+                 ms.partial, ms.vinfo, ms.bctl, ms.gconst, ms.err);
     count_launch(3);
 }
 
