@@ -97,3 +97,14 @@ def test_shot_word_keying_prefix(q):
     # deterministic in (circuit, shots, seed)
     again = q.sample(c, 128, 1234)
     assert np.array_equal(again.words, big.words)
+
+
+@pytest.mark.parametrize("n", [600, 1000])
+def test_measure_all_window_block_order(q, oracle, n):
+    """Measure-all windows (c3's shape) at sizes where the absorb pass visits 64-row blocks in a
+    strided order (n = 600: 18 blocks, stride 11; n = 1000: 31 blocks) and collapsed stabilizers
+    pile up at the low stabilizer rows batch after batch."""
+    for seed in range(2):
+        c = q.generate_random(n, 15, 300 + seed, 1.0)
+        r = run_both(q, oracle, n, c.gate_array, seed)
+        assert r.report.probabilistic_count > n // 2
