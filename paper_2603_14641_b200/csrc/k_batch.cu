@@ -87,6 +87,7 @@ __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64
                           uint64_t ng, const uint32_t *__restrict__ fq, uint32_t b,
                           uint32_t *__restrict__ colbits, uint32_t *__restrict__ stab_or,
                           uint32_t *__restrict__ nz) {
+    pdl_wait();
     __shared__ uint32_t sq[kB];
     if (threadIdx.x < b) sq[threadIdx.x] = fq[threadIdx.x];
     __syncthreads();
@@ -266,6 +267,14 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
 
 
 __global__ void k_set_u32(uint32_t *p, uint32_t v) { *p = v; }
+
+// Batch start: control words and the pivot kernels' phase sums (one launch instead of two
+// memsets, so the whole batch chain is kernel-to-kernel).
+__global__ void k_batch_reset(uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
+    pdl_wait();
+    if (threadIdx.x < 4) bctl[threadIdx.x] = 0u;
+    if (threadIdx.x < 2 * kB) pcount[threadIdx.x] = 0;
+}
 
 // B2. Pivot rows, word-parallel: thread = word i of every V_m (m in order, V_j of the same
 // word kept in shared memory), with the telescoped phase pieces of each V_m reduced into
@@ -1013,15 +1022,12 @@ static void launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cu
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
-    QSR_CUDA(cudaMemsetAsync(ms.bctl, 0, 16, t.stream));
-    // The pivot kernels' phase sums (zeroed here, ahead of the chain, so k_pivot_select follows
-    // k_colbits kernel-to-kernel).
-    QSR_CUDA(cudaMemsetAsync(ms.pcount, 0, 2 * kB * sizeof(int), t.stream));
-    k_colbits<<<unsigned((nrows + 255) / 256), 256, 0, t.stream>>>(t.x, t.rm_pitch, nrows, t.ng, d_fq,
-                                                                    b, ms.colbits, ms.bctl + BL_STAB_OR,
-                                                                    ms.nz);
-    QSR_CUDA(cudaGetLastError());
-    count_launch();
+    // Control words and the pivot kernels' phase sums, zeroed ahead of the chain.
+    launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount);
+    launch_chain(k_colbits, dim3(unsigned((nrows + 255) / 256)), dim3(256), 0, t.stream,
+                 static_cast<const uint64_t *>(t.x), t.rm_pitch, nrows, t.ng, d_fq, b, ms.colbits,
+                 ms.bctl + BL_STAB_OR, ms.nz);
+    count_launch(2);
 }
 
 // QSR_PIVOTS=fused selects the single-CTA pivot kernel (A/B and differential tests).
