@@ -1,13 +1,13 @@
 """Full-size parity on the BASELINE configs that the CPU oracle finishes in minutes
-(SURVEY.md §8(c) parity plan). Slow (the reference CPU path runs at full size on the host):
-enabled with QSR_FULLSIZE=1; the evidence of each run is kept under profiles/.
+(SURVEY.md §8(c) parity plan). Slow (the reference CPU path runs at full size on the host's
+cores, ~1-2 min per config); part of the default `-m gpu` suite.
 
   c2: generate_random(20000, 1000, 42, 0.0), run seed 7      — final tableau bit-identical
   c4: generate_random(10000, 500, 42, 1.0), sample(100000, 7) — every shot word identical
   c5 prefix: the first 6 layers of the c5 circuit at 180,000 qubits + its Bernoulli(0.01)
       final measurements — tableau and every record entry identical
-Full c3 / c5 are hours on the CPU; their gate windows are covered by the c5
-prefix and their measurement path by the c1 / measure-heavy parity tests at smaller n.
+Full c3 / c5 are hours on the CPU: tests/test_gpu_scale.py covers them by
+snapshot parity at their widths (50,000 and 180,000 qubits).
 """
 import hashlib
 import os
@@ -15,8 +15,7 @@ import os
 import numpy as np
 import pytest
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow,
-              pytest.mark.skipif(os.environ.get("QSR_FULLSIZE") != "1", reason="set QSR_FULLSIZE=1")]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 
 
 def digest(*arrays):
