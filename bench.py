@@ -8,16 +8,21 @@ One step = one full run_single_shot of the configured circuit (every gate window
 transposes and every measurement collapse) on device-resident inputs. `value` is the circuit's
 gates/s, timed with CUDA events (max over ranks); `e2e` is the same metric through the public
 API with host buffers (schedule + upload + simulate + record and tableau download).
+--config c4: one step = one sample(circuit, 100000 shots) (frames.hpp:163-204) on the resident
+engine — the reference shot plus the Pauli frames riding the same device windows.
 N > 1 (torchrun): one process per GPU drives one generator-word shard of the SAME tableau
 (strong scaling): gate windows run shard-local, measurement windows exchange pivot blocks and
 partial products over NCCL inside libqsr (csrc/shard.cpp, csrc/exchange.cu).
 --local-shards S (N = 1): the sharded engine with all S shards on the one GPU (the
 multi-GPU protocol's overhead, measured on one device).
+--impl reference: the reference's own CPU path (oracle/_ref = proj/include/quasar compiled
+unmodified) on the host cores; this process never loads libqsr.so.
 """
 from __future__ import annotations
 
 import argparse
 import ctypes as C
+import importlib.util
 import json
 import os
 import subprocess
@@ -34,6 +39,7 @@ CONFIGS = {
     "c1": dict(n=1000, depth=100, seed=42, p=1.0, run_seed=7),
     "c2": dict(n=20000, depth=1000, seed=42, p=0.0, run_seed=7),
     "c3": dict(n=50000, depth=100, seed=1000, p=1.0, run_seed=7, segments=10),
+    "c4": dict(n=10000, depth=500, seed=42, p=1.0, run_seed=7, shots=100000),
     "c5": dict(n=180000, depth=1000, seed=42, p=0.01, run_seed=7),
 }
 DESCR = {
@@ -41,16 +47,30 @@ DESCR = {
     "c2": "random Clifford, 20,000 qubits, depth 1,000 (generate_random seed 42, run seed 7)",
     "c3": "mid-circuit-measurement-heavy: 50,000 qubits, 10 segments generate_random(50000,100,1000+r,1.0) "
           "(100 layers then measure every qubit), run seed 7",
+    "c4": "many-shot sampling: 10,000 qubits, depth 500, measure all (generate_random(10000,500,42,1.0)), "
+          "sample(100000 shots, seed 7)",
     "c5": "paper headline: random Clifford+measure, 180,000 qubits, depth 1,000, "
           "Bernoulli(0.01) final measurements (generate_random(180000,1000,42,0.01), run seed 7)",
 }
 METRIC = "gates/sec and wall-s for 180k-qubit depth-1000 Clifford+measure; HBM GB/s"
 # Kind-exact (reads, writes) in u64 words per generator-word, reference gates.hpp:35-115.
 RW = np.array([(1, 0), (2, 0), (1, 0), (2, 2), (2, 1), (2, 1), (4, 2), (4, 3), (4, 2), (4, 4), (4, 4), (0, 0)])
+# Frames (frames.hpp:76-94): X / Y / Z only flip signs, which frames do not track.
+RW_FRAMES = RW.copy()
+RW_FRAMES[0:3] = 0
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
+
+
+def load_dist():
+    """paper_2603_14641_b200/dist.py by path: importing the package would load libqsr.so,
+    and the reference arm must not map it."""
+    spec = importlib.util.spec_from_file_location("qsr_dist", ROOT / "paper_2603_14641_b200" / "dist.py")
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def peaks():
@@ -116,10 +136,10 @@ class Clocks:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": rows[0][1], "reasons": reasons, "samples": len(rows)}
 
 
-def gate_bytes(circuit, k: int, gate_windows: int) -> float:
-    kinds = np.bincount(circuit.gate_array["kind"], minlength=12)
-    words = float((kinds * RW.sum(axis=1)).sum())
-    return 8.0 * 2 * k * words + 16.0 * 2 * k * gate_windows
+def gate_bytes(kinds_count, k: int, gate_windows: int, frames: bool = False) -> float:
+    rw = RW_FRAMES if frames else RW
+    words = float((kinds_count * rw.sum(axis=1)).sum())
+    return 8.0 * 2 * k * words + (0.0 if frames else 16.0 * 2 * k * gate_windows)
 
 
 def barrier(dist):
@@ -127,14 +147,19 @@ def barrier(dist):
         dist.barrier()
 
 
-def cpu_reference_windows(cfg, warm: int, timed: int):
-    """Reference CPU path (oracle/_ref, all host cores) on the first warm+timed layers of the
-    configured circuit; returns (gates/s over the timed windows, per-window seconds, kind, cores)."""
+# ---- CPU legs (reference compiled unmodified, oracle/_ref; the C port if absent) ----------
+def cpu_oracle():
     from oracle.oracle import Oracle, available
     kind = "reference" if available("reference") else "port"
     o = Oracle(kind)
     cores = os.cpu_count() or 1
     o.set_threads(cores)
+    return o, kind, cores
+
+
+def cpu_reference_windows(o, cfg, warm: int, timed: int):
+    """Reference apply_window (gates.hpp:147-197) on the first warm+timed layers of the configured
+    circuit; returns (gates/s over the timed windows, per-window seconds, mean gates/window)."""
     L = warm + timed
     sec = np.zeros(L, dtype=np.float64)
     gts = np.zeros(L, dtype=np.uint64)
@@ -145,26 +170,88 @@ def cpu_reference_windows(cfg, warm: int, timed: int):
         raise RuntimeError(o.lib.orc_last_error().decode())
     t = sec[warm:]
     g = gts[warm:].astype(np.float64)
-    return float(g.sum() / t.sum()), t, kind, cores
+    return float(g.sum() / t.sum()), t, float(g.mean())
 
 
-def run_reference_arm(args, cfg, world, rank, dist):
-    if rank != 0:
+def run_reference_arm(args, cfg):
+    """`--impl reference`: the reference CPU path on the host cores, rank 0 only (the other
+    ranks exit without work). A step is one gate window (layer) of the configured circuit
+    through the reference apply_window: the full run is hours on the CPU."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return
     t0 = time.time()
-    rate, t, kind, cores = cpu_reference_windows(cfg, args.warmup, args.steps)
+    o, kind, cores = cpu_oracle()
+    rate, t, gpw = cpu_reference_windows(o, cfg, args.warmup, args.steps)
     ms = float(np.mean(t) * 1e3)
-    sample = (f"first {args.warmup}+{args.steps} gate windows (layers) of the {args.config} circuit on a "
-              f"{cfg['n']}-qubit zero-state tableau; reference apply_window, {cores} threads; "
-              f"{args.warmup} untimed, {args.steps} timed; gates/s over the timed windows")
-    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "gates/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-            "config": {"workload": DESCR[args.config], "step": "one gate window (bounded CPU sample)"},
+    sample = (f"CPU gate-window sample: layers {args.warmup + 1}..{args.warmup + args.steps} of the "
+              f"{args.config} circuit ({cfg['n']} qubits, {gpw:.0f} gates per layer) through the reference "
+              f"apply_window on a zero-state tableau, {cores} threads, after {args.warmup} untimed layers; "
+              f"gates/s over the timed layers. The measurement phase is not part of this arm's step (the "
+              f"repo arm's cpu_baseline adds a measurement sample and a whole-run projection)")
+    line = {"impl": "reference", "metric": METRIC, "value": rate, "unit": "gates/s",
+            "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic",
+            "config": {"workload": DESCR[args.config], "step": "CPU gate-window sample (one layer of the circuit)"},
             "cpu_baseline": {"value": rate, "unit": "gates/s", "cores": cores, "kind": kind, "sample": sample},
             "e2e": {"value": rate, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": time.time() - t0}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_with_measurement(q, o, kind, cores, circ, cfg, sched_arrays, record, args, G):
+    """The reference CPU path on a bounded sample of the SAME workload, projected to a whole run:
+    gate windows (reference apply_window on the circuit's first layers), the CM<->RM transpose
+    pair and the first collapses of the first measurement window (reference measure_window,
+    measure.hpp:381-442) on the actual scrambled state the circuit reaches there (computed on
+    the GPU, downloaded once)."""
+    rate, t, gpw = cpu_reference_windows(o, cfg, 1, args.cpu_windows)
+    t_win = float(np.mean(t))
+    g, off, fl = sched_arrays
+    W_u = int((fl == 0).sum())
+    n_mwin = int((fl != 0).sum())
+    n_prob = int((record["deterministic"] == 0).sum()) if len(record) else 0
+    out = {"gate_window_rate": rate, "gate_window_s": t_win, "gate_windows": W_u}
+    proj = W_u * t_win
+    sample = (f"reference apply_window on layers 2..{1 + args.cpu_windows} of the {args.config} circuit "
+              f"({t_win:.2f} s per layer)")
+    timed_s = float(np.sum(t))
+    if n_mwin and args.cpu_collapses > 0:
+        n = cfg["n"]
+        w_first = int(np.argmax(fl != 0))
+        t_gpu = q.Tableau.zero_state(n)
+        for w in range(w_first):
+            q.apply_window(t_gpu, g[off[w]:off[w + 1]])
+        x, z, s = t_gpu.planes()
+        del t_gpu
+        # measure_window = 2 transposes + the collapses: time it on m1 and m2 > m1 of the
+        # window's first measurements (each on the same snapshot), the difference is m2 - m1
+        # collapses; the intercept is the transpose pair.
+        m2 = min(args.cpu_collapses, int(off[w_first + 1] - off[w_first]))
+        m1 = max(1, m2 // 4)
+        t_mw, m_prob = [], []
+        for m in (m1, m2):
+            xs, zs, ss = (x.copy(), z.copy(), s.copy()) if m == m1 else (x, z, s)
+            t0 = time.perf_counter()
+            ent, _ = o.measure_window(n, 0, xs, zs, ss, g[off[w_first]:off[w_first] + m], cfg["run_seed"], 0)
+            t_mw.append(time.perf_counter() - t0)
+            m_prob.append(int((ent["deterministic"] == 0).sum()))
+            del xs, zs, ss
+        t_col = max(t_mw[1] - t_mw[0], 0.0) / max(m_prob[1] - m_prob[0], 1)
+        t_T = max(t_mw[0] - m_prob[0] * t_col, 0.0) / 2
+        proj += n_prob * t_col + n_mwin * 2 * t_T
+        timed_s += sum(t_mw)
+        out.update({"transpose_s": t_T, "collapse_s": t_col, "measure_window_s": t_mw,
+                    "collapses_sampled": m_prob, "probabilistic_collapses": n_prob, "measure_windows": n_mwin})
+        sample += (f"; reference measure_window on the first {m1} and {m2} measurements of the first "
+                   f"measurement window ({t_mw[0]:.1f} s, {t_mw[1]:.1f} s) on the circuit's actual state there "
+                   f"(GPU-computed snapshot): {t_col:.2f} s per collapse, {t_T:.2f} s per transpose")
+    out["projected_run_s"] = proj
+    value = G / proj
+    sample += (f"; whole-run projection {proj:.0f} s = {W_u} windows x layer time"
+               + (" + collapses x collapse time + 2 transposes per measurement window" if n_mwin else "")
+               + f"; {timed_s:.1f} s of CPU work timed on {cores} host threads")
+    return {"value": value, "unit": "gates/s", "cores": cores, "kind": kind, "sample": sample, "detail": out}
 
 
 def main():
@@ -175,18 +262,25 @@ def main():
     ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=None)
-    ap.add_argument("--cpu-windows", type=int, default=2, help="timed CPU-baseline windows (rank 0)")
+    ap.add_argument("--cpu-windows", type=int, default=2, help="timed CPU-baseline gate windows (rank 0)")
+    ap.add_argument("--cpu-collapses", type=int, default=None,
+                    help="CPU-baseline collapses on the GPU snapshot (default: 4 at c5, 32 below)")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-profile", action="store_true", help="skip the measurement-pass profile run")
     ap.add_argument("--local-shards", type=int, default=1,
                     help="N = 1 only: run the sharded engine with this many shards on the one GPU")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
-    from paper_2603_14641_b200 import dist as qd
-    world, rank, local, dist = qd.init_from_env("nccl")
+    if args.cpu_collapses is None:
+        args.cpu_collapses = 8 if cfg["n"] >= 100000 else 32
     if args.impl == "reference":
-        run_reference_arm(args, cfg, world, rank, dist)
+        run_reference_arm(args, cfg)
         return
+    if args.config == "c4":
+        return bench_sampling(args, cfg)
 
+    qd = load_dist()
+    world, rank, local, dist = qd.init_from_env("nccl")
     from paper_2603_14641_b200 import _lib
     from paper_2603_14641_b200 import quasar as q
     device = local
@@ -202,8 +296,10 @@ def main():
     log(f"[rank {rank}] generated {G} gates ({nm} measurements) in {time.time() - t0:.1f}s")
     t0 = time.time()
     sched = q.schedule_windows(circ)
-    _, offs, flags = sched.arrays()
+    sched_arrays = sched.arrays()
+    _, offs, flags = sched_arrays
     gate_windows = int((flags == 0).sum())
+    meas_windows = int((flags != 0).sum())
     log(f"[rank {rank}] scheduled {len(flags)} windows in {time.time() - t0:.2f}s")
     n = cfg["n"]
     k = (n + 63) // 64
@@ -230,7 +326,7 @@ def main():
 
     launches0 = q.launch_count()
     barrier(dist)
-    step_ms, gate_ms, gate_launch, gate_dev_bytes = [], 0.0, 0, 0.0
+    step_ms, gate_ms, gate_launch, gate_dev_bytes, tr_ms, meas_ms = [], 0.0, 0, 0.0, 0.0, 0.0
     with Clocks(device) as clk:
         for i in range(args.steps):
             ms = eng.run(run_seed)
@@ -239,39 +335,82 @@ def main():
             gate_ms += st["gate_ms"]
             gate_launch += st["gate_launches"]
             gate_dev_bytes += st.get("gate_bytes", 0.0)
+            tr_ms += st["transpose_ms"]
+            meas_ms += st["measure_ms"]
             log(f"[rank {rank}] step {i}: {ms:.1f} ms  {st}")
     barrier(dist)
     launches = q.launch_count() - launches0
     total_ms = qd.max_over_ranks(dist, float(np.sum(step_ms)))
     ms_per_step = total_ms / args.steps
     value = G * args.steps / (total_ms * 1e-3)
+    record = eng.record() if world == 1 and shards == 1 else None
 
-    # Roofline of the dominant kernel (gate windows): algorithmic bytes per launch over the
-    # average launch duration measured above with CUDA events on the engine's stream. The bytes
-    # are those of the device gates actually launched (kind-exact words), i.e. after
-    # the exact gate fusion (SWAP relabelling, single-qubit runs folded into the next two-qubit
-    # gate); `unfused_*` restates the reference-semantics bytes of the same windows and the
-    # resulting effective bandwidth.
-    launches_per_step = gate_launch / args.steps
-    gb_ref_step = gate_bytes(circ, k if (world == 1 and shards > 1) else kg_local, gate_windows)
-    gb_step = gate_dev_bytes / args.steps if gate_dev_bytes > 0 else gb_ref_step
-    per_launch_bytes = gb_step / launches_per_step
-    per_launch_s = (gate_ms / gate_launch) * 1e-3
-    achieved = per_launch_bytes / per_launch_s / 1e9
-    effective = gb_ref_step / (gate_ms / args.steps * 1e-3) / 1e9
+    # Roofline of the gate-window kernel: algorithmic bytes per launch over the average launch
+    # duration measured above with CUDA events on the engine's stream. The bytes are those of the
+    # device gates actually launched (kind-exact words), i.e. after the exact gate
+    # fusion (SWAP relabelling, single-qubit runs folded into the next two-qubit gate);
+    # `unfused_*` restates the reference-semantics bytes of the same windows.
     peak, peak_src = peaks()
-    kernel = "k_gate_segment" if os.environ.get("QSR_GATE_ENGINE") == "segment" else "k_gate_window"
-    traffic = None
+    kinds = np.bincount(circ.gate_array["kind"], minlength=12)
+    launches_per_step = gate_launch / args.steps
+    gb_ref_step = gate_bytes(kinds, k if (world == 1 and shards > 1) else kg_local, gate_windows)
+    gb_step = gate_dev_bytes / args.steps if gate_dev_bytes > 0 else gb_ref_step
+    per_launch_bytes = gb_step / max(launches_per_step, 1)
+    per_launch_s = (gate_ms / max(gate_launch, 1)) * 1e-3
+    traffic_entries = []
     tp = ROOT / "profiles" / "gate_window_traffic.json"
     if tp.exists():
         try:
-            for d in json.loads(tp.read_text()).get("entries", []):
-                fused = os.environ.get("QSR_FUSE", "1") != "0" and world == 1 and shards == 1
-                if (d.get("config") == args.config and d.get("kernel", "").startswith(kernel) and shards == 1
-                        and bool(d.get("fused", False)) == fused):
-                    traffic = d.get("dram_bytes_per_launch")
+            traffic_entries = json.loads(tp.read_text()).get("entries", [])
         except Exception:
-            pass
+            traffic_entries = []
+
+    def traffic_of(kernel):
+        fused = os.environ.get("QSR_FUSE", "1") != "0" and world == 1 and shards == 1
+        for d in traffic_entries:
+            if (d.get("config") == args.config and d.get("kernel", "").startswith(kernel) and shards == 1
+                    and bool(d.get("fused", fused)) == fused):
+                return d.get("dram_bytes_per_launch")
+        return None
+
+    gate_roof = None
+    if gate_launch:
+        achieved = per_launch_bytes / per_launch_s / 1e9
+        gate_roof = {"bound": "hbm", "kernel": "k_gate_window", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic_of("k_gate_window"),
+                     "bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_s * 1e3,
+                     "ms_per_step": gate_ms / args.steps, "unfused_bytes_per_step": gb_ref_step,
+                     "effective_unfused_gbs": gb_ref_step / (gate_ms / args.steps * 1e-3) / 1e9,
+                     "peak_source": peak_src}
+    # Transposes (k_transpose, 4 plane launches per measurement window): 2 planes x (read +
+    # write) x 8 B x n_pad x 2kg per direction.
+    tr_roof = None
+    if meas_windows and tr_ms > 0:
+        tr_bytes = meas_windows * 2 * (2 * 2 * 8.0 * n_pad * 2 * kg_local)
+        a = tr_bytes / (tr_ms / args.steps * 1e-3) / 1e9
+        tr_roof = {"bound": "hbm", "kernel": "k_transpose", "achieved": a, "peak": peak, "unit": "GB/s",
+                   "frac": a / peak, "bytes_per_step": tr_bytes, "ms_per_step": tr_ms / args.steps,
+                   "traffic": traffic_of("k_transpose")}
+    # Measurement pass (k_batch_absorb): one more run, outside the timed region, with CUDA events
+    # around every absorb launch and a device count of the rows each batch rewrites; algorithmic
+    # bytes per rewritten row = x and z read + written over its k words (32 k B) + one phase byte
+    # per 64-word slice.
+    absorb_roof = None
+    if meas_windows and world == 1 and shards == 1 and not args.no_profile:
+        prof = eng.profile(run_seed)
+        if prof["absorb_launches"]:
+            ab = prof["absorb_rows"] * (32.0 * prof["row_words"] + prof["absorb_slices"])
+            a = ab / (prof["absorb_ms"] * 1e-3) / 1e9
+            absorb_roof = {"bound": "hbm", "kernel": "k_batch_absorb", "achieved": a, "peak": peak, "unit": "GB/s",
+                           "frac": a / peak, "bytes_per_launch": ab / prof["absorb_launches"],
+                           "launch_ms": prof["absorb_ms"] / prof["absorb_launches"],
+                           "launches_per_step": prof["absorb_launches"], "ms_per_step": prof["absorb_ms"],
+                           "rows_per_launch": prof["absorb_rows"] / prof["absorb_launches"],
+                           "traffic": traffic_of("k_batch_absorb"),
+                           "how": "one profile run after the timed steps (events around each absorb launch)"}
+    # The line's roofline = the kernel class that dominates the step.
+    cands = [(r["ms_per_step"], r) for r in (gate_roof, tr_roof, absorb_roof) if r]
+    roofline = max(cands, key=lambda c: c[0])[1] if cands else None
     st = eng.stats()
     del eng
 
@@ -323,11 +462,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, t, kind, cores = cpu_reference_windows(cfg, 1, args.cpu_windows)
-            cpu = {"value": rate, "unit": "gates/s", "cores": cores, "kind": kind,
-                   "sample": f"reference apply_window on the first 1+{args.cpu_windows} layers of the "
-                             f"{args.config} circuit ({cfg['n']} qubits), first window untimed; "
-                             f"{float(np.sum(t)):.1f} s timed on {cores} host threads"}
+            o, kind, cores = cpu_oracle()
+            cpu = cpu_baseline_with_measurement(q, o, kind, cores, circ, cfg, sched_arrays,
+                                                record if record is not None else np.zeros(0, _lib.ENTRY_DTYPE),
+                                                args, G)
         except Exception as ex:  # report, never fake
             cpu = {"value": None, "unit": "gates/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"unavailable: {ex}"}
@@ -338,23 +476,157 @@ def main():
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": DESCR[args.config], "qubits": n, "depth": cfg["depth"], "gates": G,
-                   "measurements": nm, "windows": int(len(flags)), "gate_windows": gate_windows,
+        "config": {"workload": DESCR[args.config], "qubits": n, "depth": cfg["depth"] * cfg.get("segments", 1),
+                   "gates": G, "measurements": nm, "windows": int(len(flags)), "gate_windows": gate_windows,
+                   "measure_windows": meas_windows,
                    "parallelism": (f"generator-row shards x{world} (NCCL)" if world > 1 else
                                    f"generator-row shards x{shards} on one GPU (local exchange)"
                                    if shards > 1 else "single GPU"),
                    "l2": f"inputs larger than L2 (tableau {2 * n_pad * 2 * k * 8 / 1e9:.2f} GB vs 126 MB L2); "
                          "no flush needed"},
         "wall_s_per_step": ms_per_step / 1e3,
-        "phase_ms_per_step": {"gate_windows": gate_ms / args.steps, "transpose": st["transpose_ms"],
-                              "measure": st["measure_ms"]},
-        "roofline": {"bound": "hbm", "kernel": kernel, "achieved": achieved, "peak": peak,
-                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                     "bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_s * 1e3,
-                     "unfused_bytes_per_step": gb_ref_step, "effective_unfused_gbs": effective,
-                     "peak_source": peak_src},
+        "phase_ms_per_step": {"gate_windows": gate_ms / args.steps, "transpose": tr_ms / args.steps,
+                              "measure": meas_ms / args.steps},
+        "roofline": roofline,
+        "kernels": {"gate_window": gate_roof, "transpose": tr_roof, "measure_absorb": absorb_roof},
         "e2e": {"value": e2e_value, "unit": "gates/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "s_per_step": e2e_total / max(e2e_steps, 1)},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sampling(q, o, kind, cores, circ, cfg, sched_arrays, record, args, G, shots):
+    """Reference sample() (frames.hpp:163-204) on bounded samples of the c4 workload, projected to
+    a whole call: schedule_windows, the reference shot (gate windows + transposes + collapses on
+    the circuit's actual state, as cpu_baseline_with_measurement), the frames' windows on 100k
+    shots (apply_window_frames) and the final measure_sample."""
+    base = cpu_baseline_with_measurement(q, o, kind, cores, circ, cfg, sched_arrays, record, args, G)
+    d = base["detail"]
+    n = cfg["n"]
+    g, off, fl = sched_arrays
+    t0 = time.perf_counter()
+    o.schedule(n, circ.gate_array)
+    t_sched = time.perf_counter() - t0
+    xf, zf = o.init_frames(n, shots, cfg["run_seed"])
+    wins = [w for w in range(len(fl)) if not fl[w]][:1 + args.cpu_windows]
+    o.apply_window_frames(n, shots, xf, zf, g[off[wins[0]]:off[wins[0] + 1]])  # untimed
+    t0 = time.perf_counter()
+    for w in wins[1:]:
+        o.apply_window_frames(n, shots, xf, zf, g[off[w]:off[w + 1]])
+    t_fwin = (time.perf_counter() - t0) / max(len(wins) - 1, 1)
+    kf = (shots + 63) // 64
+    mw = [w for w in range(len(fl)) if fl[w]]
+    t_ms = 0.0
+    if mw:
+        meas = g[off[mw[0]]:off[mw[0] + 1]]
+        measured = np.zeros(n, dtype=np.uint32)
+        words = np.zeros(n * kf, dtype=np.uint64)
+        t0 = time.perf_counter()
+        o.measure_sample(n, shots, xf, zf, meas, cfg["run_seed"], 1, measured, 0, words)
+        t_ms = (time.perf_counter() - t0) * len(mw)
+    proj = d["projected_run_s"] + t_sched + d["gate_windows"] * t_fwin + t_ms
+    d.update({"schedule_s": t_sched, "frames_window_s": t_fwin, "measure_sample_s": t_ms, "projected_run_s": proj})
+    base["value"] = G / proj
+    base["sample"] += (f"; plus reference schedule_windows ({t_sched:.1f} s), apply_window_frames on {shots} "
+                       f"shots ({t_fwin:.2f} s per layer, {len(wins) - 1} layers timed) and measure_sample "
+                       f"({t_ms:.2f} s): whole sample() call projected at {proj:.0f} s")
+    return base
+
+
+def bench_sampling(args, cfg):
+    """c4: one step = sample(circuit, shots, seed) on the resident engine (reference shot + frames
+    riding its windows, record fold), CUDA-event timed. N > 1: each rank samples its shot-word
+    slice (frames.hpp:63 keys are global; no communication), weak in shots per GPU = strong in
+    the total (the SAME 100k shots are split)."""
+    qd = load_dist()
+    world, rank, local, dist = qd.init_from_env("nccl")
+    from paper_2603_14641_b200 import _lib
+    from paper_2603_14641_b200 import quasar as q
+    device = local
+    n, shots, seed = cfg["n"], cfg["shots"], cfg["run_seed"]
+    t0 = time.time()
+    circ = q.generate_random(n, cfg["depth"], cfg["seed"], cfg["p"])
+    G = len(circ)
+    nm = circ.measure_count()
+    sched_arrays = q.schedule_windows(circ).arrays()
+    _, offs, flags = sched_arrays
+    gate_windows = int((flags == 0).sum())
+    log(f"[rank {rank}] generated + scheduled {G} gates in {time.time() - t0:.1f}s")
+    eng = q.Engine(circ, device=device)
+    for i in range(args.warmup):
+        _, ms = eng.sample(shots, seed, record=False, world=world, rank=rank)
+        log(f"[rank {rank}] warmup {i}: {ms:.1f} ms")
+    launches0 = q.launch_count()
+    barrier(dist)
+    step_ms, gate_ms, gb, fb = [], 0.0, 0.0, 0.0
+    with Clocks(device) as clk:
+        for i in range(args.steps):
+            _, ms = eng.sample(shots, seed, record=False, world=world, rank=rank)
+            st = eng.stats()
+            step_ms.append(ms)
+            gate_ms += st["gate_ms"]
+            gb += st["gate_bytes"]
+            fb += eng.frames_bytes()
+            log(f"[rank {rank}] step {i}: {ms:.1f} ms  {st}")
+    barrier(dist)
+    launches = q.launch_count() - launches0
+    total_ms = qd.max_over_ranks(dist, float(np.sum(step_ms)))
+    ms_per_step = total_ms / args.steps
+    value = G * args.steps / (total_ms * 1e-3)
+    peak, peak_src = peaks()
+    # Gate windows of the reference shot AND the frames (both k_gate_window instances, launched
+    # alternately on one stream): their algorithmic bytes over the unitary runs' event time.
+    a = (gb + fb) / (gate_ms * 1e-3) / 1e9 if gate_ms else None
+    roof = {"bound": "hbm", "kernel": "k_gate_window (reference-shot tableau + frames instances)",
+            "achieved": a, "peak": peak, "unit": "GB/s", "frac": a / peak if a else None, "traffic": None,
+            "bytes_per_step": (gb + fb) / args.steps, "frames_bytes_per_step": fb / args.steps,
+            "ms_per_step": gate_ms / args.steps, "peak_source": peak_src}
+    record = eng.record()
+    del eng
+    # e2e: the public sample() call (qsr_sample / qsr_sample_shard: schedule + upload streamed,
+    # reference shot + frames, fold) and the ShotRecord download to the host.
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
+    e2e_s = []
+    rec_bytes = 0
+    barrier(dist)
+    for i in range(e2e_steps):
+        t1 = time.perf_counter()
+        if world > 1:
+            _, r = q.sample_shard(circ, shots, seed, world, rank, device=device)
+        else:
+            r = q.sample(circ, shots, seed, device=device)
+        e2e_s.append(time.perf_counter() - t1)
+        rec_bytes = int(r.words.nbytes + 4 * len(r.measured))
+        log(f"[rank {rank}] e2e {i}: {e2e_s[-1]:.3f} s")
+    barrier(dist)
+    e2e_total = qd.max_over_ranks(dist, float(np.sum(e2e_s)))
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            o, kind, cores = cpu_oracle()
+            cpu = cpu_baseline_sampling(q, o, kind, cores, circ, cfg, sched_arrays, record, args, G, shots)
+        except Exception as ex:  # report, never fake
+            cpu = {"value": None, "unit": "gates/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": DESCR["c4"], "qubits": n, "depth": cfg["depth"], "gates": G, "measurements": nm,
+                   "shots": shots, "gate_windows": gate_windows,
+                   "parallelism": f"shot-word slices x{world}" if world > 1 else "single GPU",
+                   "step": "one sample() call on the resident engine (gates/s of the circuit per call)",
+                   "l2": "frames planes 2 x 125 MB + record 125 MB > 126 MB L2; no flush needed"},
+        "shots_per_s": shots * args.steps / (total_ms * 1e-3),
+        "wall_s_per_step": ms_per_step / 1e3,
+        "roofline": roof,
+        "e2e": {"value": G * e2e_steps / e2e_total, "unit": "gates/s", "h2d_bytes_per_step": world * 12 * G,
+                "d2h_bytes_per_step": world * rec_bytes, "s_per_step": e2e_total / max(e2e_steps, 1)},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

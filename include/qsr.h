@@ -227,10 +227,32 @@ qsr_status qsr_engine_stats(const qsr_engine *e, double *gate_ms, uint64_t *gate
 qsr_status qsr_engine_gate_bytes(const qsr_engine *e, double *bytes);
 qsr_status qsr_engine_record(const qsr_engine *e, qsr_record_entry *record);
 qsr_status qsr_engine_tableau(const qsr_engine *e, uint64_t *x, uint64_t *z, uint64_t *s);
+/* Measurement-pass profile (bench.py's per-phase roofline): one more run with CUDA events around
+ * every k_batch_absorb launch and a device count of the rows each batch rewrites. Not used by
+ * timed runs (the events split the programmatic-launch chain). */
+typedef struct qsr_kernel_profile {
+    double absorb_ms;          /* summed device time of the absorb launches */
+    uint64_t absorb_launches;
+    uint64_t absorb_rows;      /* rows that absorbed >= 1 pivot row, summed over the launches */
+    uint64_t absorb_slices;    /* 64-word slices per row (one phase byte each) */
+    uint64_t row_words;        /* qubit-words per RM row (k) */
+    double total_ms;           /* device time of the whole profiled run */
+} qsr_kernel_profile;
+qsr_status qsr_engine_profile(qsr_engine *e, uint64_t seed, qsr_kernel_profile *out);
+/* sample<uint64_t>(circuit, shots, seed) (frames.hpp:163-204) on the resident engine: the
+ * engine's run is the reference shot and the Pauli frames ride its (fused) windows on the same
+ * stream; *device_ms = CUDA-event time of the call (frames init, run, record fold). The result
+ * is the same ShotRecord as qsr_sample (world = 1) or shot-word slice `rank` of `world` as
+ * qsr_sample_shard; release it with qsr_frames_destroy. */
+typedef struct qsr_frames qsr_frames;
+qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int world, int rank,
+                             qsr_frames **out, double *device_ms);
+/* Algorithmic bytes of the last qsr_engine_sample's frames-window launches (frames rule words,
+ * no signs: X / Y / Z move nothing, frames.hpp:76-94) = 8 B x shot-words x words. */
+qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes);
 void qsr_engine_destroy(qsr_engine *e);
 
 /* ---- Pauli frames (frames.hpp:32-204) ------------------------------------------ */
-typedef struct qsr_frames qsr_frames;
 /* init_frames<uint64_t>(n, shots, seed) (frames.hpp:46-72). */
 qsr_status qsr_init_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
                            qsr_frames **out);

@@ -77,6 +77,11 @@ class Report_t(C.Structure):
                 ("total_seconds", C.c_double)]
 
 
+class KernelProfile_t(C.Structure):  # qsr_kernel_profile
+    _fields_ = [("absorb_ms", C.c_double), ("absorb_launches", C.c_uint64), ("absorb_rows", C.c_uint64),
+                ("absorb_slices", C.c_uint64), ("row_words", C.c_uint64), ("total_ms", C.c_double)]
+
+
 class ShardConfig_t(C.Structure):
     _fields_ = [("world", C.c_int), ("rank", C.c_int), ("device", C.c_int), ("exchange", C.c_int),
                 ("nccl_id", C.POINTER(C.c_uint8))]
@@ -152,6 +157,9 @@ SIGNATURES = {
     "qsr_engine_gate_bytes": (i32, [P, pd]),
     "qsr_sharded_gate_bytes": (i32, [P, pd]),
     "qsr_engine_tableau": (i32, [P, pu64, pu64, pu64]),
+    "qsr_engine_profile": (i32, [P, u64, C.POINTER(KernelProfile_t)]),
+    "qsr_engine_sample": (i32, [P, u64, u64, i32, i32, C.POINTER(P), pd]),
+    "qsr_engine_frames_bytes": (i32, [P, pd]),
     "qsr_engine_destroy": (None, [P]),
     "qsr_init_frames": (i32, [u64, u64, u64, i32, C.POINTER(P)]),
     "qsr_frames_info": (i32, [P, pu64, pu64, pu64]),

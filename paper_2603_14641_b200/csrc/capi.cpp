@@ -36,7 +36,14 @@ void cuda_check(cudaError_t e, const char *what) {
 namespace {
 struct PlaneCache {
     std::mutex mu;
-    struct Entry { int device; uint64_t bytes; void *p; };
+    // ready: recorded on the releasing owner's stream when a block is released mid-life, so the
+    // next owner never races the kernels still queued on it; null = already idle.
+    struct Entry { int device; uint64_t bytes; void *p; cudaEvent_t ready; };
+    static void wait_ready(cudaEvent_t ev) {
+        if (!ev) return;
+        cudaEventSynchronize(ev);
+        cudaEventDestroy(ev);
+    }
     std::vector<Entry> free_list;
     static bool enabled() {
         static const bool on = [] {
@@ -51,7 +58,9 @@ struct PlaneCache {
             for (size_t i = 0; i < free_list.size(); ++i)
                 if (free_list[i].device == device && free_list[i].bytes == bytes) {
                     void *p = free_list[i].p;
+                    const cudaEvent_t ev = free_list[i].ready;
                     free_list.erase(free_list.begin() + long(i));
+                    wait_ready(ev);
                     return p;
                 }
         }
@@ -65,17 +74,28 @@ struct PlaneCache {
         QSR_CUDA(e);
         return p;
     }
-    void release(int device, uint64_t bytes, void *p) {
+    void release(int device, uint64_t bytes, void *p, cudaStream_t after = nullptr) {
         if (!p) return;
-        if (!enabled()) { cudaFree(p); return; }
+        cudaEvent_t ev = nullptr;
+        if (after) {
+            QSR_CUDA(cudaSetDevice(device));
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            QSR_CUDA(cudaStreamIsCapturing(after, &cs));
+            if (cs != cudaStreamCaptureStatusNone) // graphs are captured once every buffer is sized
+                fail(QSR_INTERNAL, "scratch block released during stream capture");
+            QSR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            QSR_CUDA(cudaEventRecord(ev, after));
+        }
+        if (!enabled()) { wait_ready(ev); cudaFree(p); return; }
         std::lock_guard<std::mutex> g(mu);
-        free_list.push_back({device, bytes, p});
+        free_list.push_back({device, bytes, p, ev});
     }
     void flush(int device) {
         std::lock_guard<std::mutex> g(mu);
         for (auto it = free_list.begin(); it != free_list.end();) {
             if (device < 0 || it->device == device) {
                 cudaSetDevice(it->device);
+                wait_ready(it->ready);
                 cudaFree(it->p);
                 it = free_list.erase(it);
             } else {
@@ -113,7 +133,9 @@ void pinned_slot_release(uint32_t *p) {
 } // namespace
 
 void *cache_acquire(int device, uint64_t bytes) { return plane_cache().acquire(device, bytes); }
-void cache_release(int device, uint64_t bytes, void *p) { plane_cache().release(device, bytes, p); }
+void cache_release(int device, uint64_t bytes, void *p, cudaStream_t after) {
+    plane_cache().release(device, bytes, p, after);
+}
 
 DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : device(dev), n(n_) {
     if (n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
@@ -191,7 +213,6 @@ DeviceTableau::~DeviceTableau() {
     plane_cache().release(device, arena_bytes, arena);
     // Lazily sized scratch returns to the cache too (the next tableau of this shape reuses it).
     plane_cache().release(device, sign_partial_chunks * cm_pitch * 8, sign_partials);
-    plane_cache().release(device, 256, seg_bar);
     plane_cache().release(device, ms.partial_bytes, ms.partial);
     release_window_cap();
     if (stream) cudaStreamDestroy(stream);
@@ -199,7 +220,7 @@ DeviceTableau::~DeviceTableau() {
 
 void DeviceTableau::ensure_gate_buf(uint64_t ng) {
     if (ng <= gate_buf_cap) return;
-    if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf);
+    if (gate_buf) plane_cache().release(device, gate_buf_cap * 8, gate_buf, stream);
     gate_buf_cap = std::max<uint64_t>(ng, 1024);
     gate_buf = static_cast<uint64_t *>(plane_cache().acquire(device, gate_buf_cap * 8));
 }
@@ -208,7 +229,7 @@ void DeviceTableau::ensure_gate_buf(uint64_t ng) {
 static uint64_t window_block_bytes(uint64_t cap) { return cap * (1 + 1 + sizeof(qsr_record_entry) + 4 + 4 + 4) + 256; }
 
 void DeviceTableau::release_window_cap() {
-    if (ms.window_cap) plane_cache().release(device, window_block_bytes(ms.window_cap), ms.coin_buf);
+    if (ms.window_cap) plane_cache().release(device, window_block_bytes(ms.window_cap), ms.coin_buf, stream);
     ms.coin_buf = ms.flags = nullptr;
     ms.out = nullptr;
     ms.mqubits = ms.fq = ms.fidx = nullptr;
@@ -915,12 +936,53 @@ qsr_status qsr_engine_tableau(const qsr_engine *e, uint64_t *x, uint64_t *z, uin
     });
 }
 
+qsr_status qsr_engine_profile(qsr_engine *e, uint64_t seed, qsr_kernel_profile *out) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        REQUIRE_PTR(out);
+        DeviceTableau &t = *e->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        DeviceTableau::AbsorbProfile prof;
+        QSR_CUDA(cudaMalloc(&prof.d_rows, sizeof(unsigned long long)));
+        QSR_CUDA(cudaMemsetAsync(prof.d_rows, 0, sizeof(unsigned long long), t.stream));
+        t.prof = &prof;
+        RunTimes rt;
+        try {
+            run_device(t, *e->ds, seed, e->d_rec, rt);
+        } catch (...) {
+            t.prof = nullptr;
+            for (auto &p : prof.ev) cudaEventDestroy(p.first), cudaEventDestroy(p.second);
+            cudaFree(prof.d_rows);
+            throw;
+        }
+        t.prof = nullptr;
+        t.sync();
+        *out = qsr_kernel_profile{};
+        for (auto &p : prof.ev) {
+            float ms = 0;
+            QSR_CUDA(cudaEventElapsedTime(&ms, p.first, p.second));
+            out->absorb_ms += ms;
+            cudaEventDestroy(p.first);
+            cudaEventDestroy(p.second);
+        }
+        unsigned long long rows = 0;
+        QSR_CUDA(cudaMemcpy(&rows, prof.d_rows, sizeof(rows), cudaMemcpyDeviceToHost));
+        cudaFree(prof.d_rows);
+        out->absorb_launches = prof.ev.size();
+        out->absorb_rows = rows;
+        out->absorb_slices = (t.rm_pitch + 63) / 64;
+        out->row_words = t.k;
+        out->total_ms = rt.total_ms;
+    });
+}
+
 void qsr_engine_destroy(qsr_engine *e) { delete e; }
 
 // ---- frames -----------------------------------------------------------------------
 struct qsr_frames {
     int device = 0;
     cudaStream_t stream = nullptr;
+    bool owns_stream = true; // false while riding a resident engine's stream (qsr_engine_sample)
     int num_sms = 148;
     uint64_t n = 0, shots = 0, kf = 0, pitch = 0; // kf: shot-words held here
     uint64_t j0 = 0;                                // global index of the first one
@@ -932,8 +994,7 @@ struct qsr_frames {
     std::vector<int64_t> row_of; // qubit -> record row
     uint64_t *gate_buf = nullptr;
     uint64_t gate_cap = 0;
-    unsigned int *seg_bar = nullptr; // segment-kernel grid barrier
-    uint64_t *xs = nullptr, *zs = nullptr; // slab-major scratch planes of the segment kernel
+    uint64_t *xs = nullptr, *zs = nullptr; // row un-permute targets (fused windows)
     uint32_t *d_idx = nullptr;   // qubits + rows staging
     uint64_t idx_cap = 0;
     uint64_t plane_bytes = 0; // xf / zf come from the plane cache (no cudaMalloc per sample())
@@ -942,9 +1003,15 @@ struct qsr_frames {
         if (stream) cudaStreamSynchronize(stream);
         for (uint64_t *p : {xf, zf, xs, zs}) plane_cache().release(device, plane_bytes, p);
         if (rec) plane_cache().release(device, rec_cap * pitch * 8, rec);
-        for (void *p : {(void *)gate_buf, (void *)d_idx, (void *)seg_bar})
+        for (void *p : {(void *)gate_buf, (void *)d_idx})
             if (p) cudaFree(p);
-        if (stream) cudaStreamDestroy(stream);
+        if (stream && owns_stream) cudaStreamDestroy(stream);
+    }
+    void own_stream() { // leave the borrowed stream: later calls (downloads) run on a private one
+        if (owns_stream) return;
+        QSR_CUDA(cudaStreamSynchronize(stream));
+        QSR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        owns_stream = true;
     }
     void ensure_rows(uint64_t rows) {
         if (rows <= rec_cap) return;
@@ -975,7 +1042,8 @@ void check_word_bits(unsigned wbits) {
 }
 
 std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
-                                        uint64_t j0 = 0, uint64_t nw = 0, unsigned wbits = 64) {
+                                        uint64_t j0 = 0, uint64_t nw = 0, unsigned wbits = 64,
+                                        cudaStream_t borrow = nullptr) {
     check_word_bits(wbits);
     if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "init_frames: n exceeds the supported maximum");
@@ -983,7 +1051,12 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     f->device = device;
     QSR_CUDA(cudaSetDevice(device));
     QSR_CUDA(cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device));
-    QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    if (borrow) {
+        f->stream = borrow;
+        f->owns_stream = false;
+    } else {
+        QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
+    }
     f->n = n;
     f->shots = shots;
     f->kf = nw ? nw : (shots + 63) / 64;
@@ -1030,6 +1103,56 @@ void frames_measure_q(qsr_frames &f, QubitOf qubit_of, uint64_t ng, uint64_t see
 
 void frames_measure(qsr_frames &f, const qsr_gate *gates, uint64_t ng, uint64_t seed, uint32_t epoch) {
     frames_measure_q(f, [&](uint64_t i) { return gates[i].q0; }, ng, seed, epoch);
+}
+
+// sample()'s frames as the passenger of a reference-shot run (streamed or resident): the same
+// device windows, row un-permutes and measurement windows, on the tableau's stream.
+struct FramesRider final : FramesSink {
+    qsr_frames &f;
+    uint64_t seed;
+    uint32_t epoch = 1;
+    FramesRider(qsr_frames &ff, uint64_t s) : f(ff), seed(s) { row_words = ff.kf; }
+    void unitary(const uint64_t *g, uint64_t cnt, cudaStream_t st) override {
+        launch_frame_window(f.xf, f.zf, f.pitch, g, cnt, f.num_sms, st);
+    }
+    void unpermute(const uint32_t *perm, cudaStream_t st) override {
+        if (!f.xs) {
+            f.xs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
+            f.zs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
+        }
+        launch_unpermute_frame_rows(f.xf, f.xs, f.pitch, f.n, perm, f.num_sms, st);
+        launch_unpermute_frame_rows(f.zf, f.zs, f.pitch, f.n, perm, f.num_sms, st);
+        std::swap(f.xf, f.xs);
+        std::swap(f.zf, f.zs);
+    }
+    void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) override {
+        frames_measure_q(f, [&](uint64_t i) { return qubits[i]; }, m, seed, epoch++, st);
+    }
+};
+
+// Fold in the reference outcomes: per_qubit() = last outcome per qubit (measure.hpp:50-64,
+// frames.hpp:183-202); rows whose reference bit is 1 are flipped on the device.
+void fold_reference(qsr_frames &f, const std::vector<qsr_record_entry> &ref, uint64_t num_qubits,
+                    cudaStream_t st) {
+    std::vector<int8_t> last(num_qubits, -1);
+    for (const auto &e : ref) last[e.qubit] = int8_t(e.outcome ? 1 : 0);
+    std::vector<uint32_t> flip_rows;
+    for (uint64_t r = 0; r < f.measured.size(); ++r)
+        if (last[f.measured[r]] == 1) flip_rows.push_back(uint32_t(r));
+    if (!flip_rows.empty()) {
+        f.ensure_idx(flip_rows.size());
+        QSR_CUDA(cudaMemcpyAsync(f.d_idx, flip_rows.data(), flip_rows.size() * 4, cudaMemcpyHostToDevice, st));
+        launch_record_fold(f.rec, f.pitch, f.kf, f.j0, f.shots, f.d_idx, flip_rows.size(), st);
+    }
+    QSR_CUDA(cudaStreamSynchronize(st));
+}
+
+uint64_t circuit_distinct_measured(const Circuit &c) {
+    std::vector<uint8_t> seen(c.num_qubits, 0);
+    uint64_t distinct = 0;
+    for (const qsr_gate &g : c.gates)
+        if (g.kind == QSR_MEASURE && g.q0 < c.num_qubits && !seen[g.q0]) { seen[g.q0] = 1; ++distinct; }
+    return distinct;
 }
 
 void validate_frames_window(const qsr_frames &f, const qsr_gate *gates, uint64_t ng, bool meas,
@@ -1184,21 +1307,14 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
         const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
         TraceScope tr_all("sample");
         // One record allocation: the distinct measured qubits of the circuit.
-        auto distinct_measured = [&] {
-            std::vector<uint8_t> seen(c->num_qubits, 0);
-            uint64_t distinct = 0;
-            for (const qsr_gate &g : c->gates)
-                if (g.kind == QSR_MEASURE && g.q0 < c->num_qubits && !seen[g.q0]) { seen[g.q0] = 1; ++distinct; }
-            return distinct;
-        };
+        auto distinct_measured = [&] { return circuit_distinct_measured(*c); };
         DeviceTableau t(c->num_qubits, device);
         const uint64_t nm = c->measure_count();
         qsr_record_entry *d_rec = nullptr;
         QSR_CUDA(cudaMalloc(&d_rec, std::max<uint64_t>(nm, 1) * sizeof(qsr_record_entry)));
         std::vector<qsr_record_entry> ref(nm);
         std::unique_ptr<qsr_frames> f;
-        const bool streaming = !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0') &&
-                               !gate_segment_enabled();
+        const bool streaming = !(getenv("QSR_STREAM") && getenv("QSR_STREAM")[0] == '0');
         try {
             if (streaming) {
                 // The reference shot (frames.hpp:167) streamed as in run_single_shot (schedule
@@ -1210,28 +1326,7 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
                 f = make_frames(c->num_qubits, shots, seed, device, w0, nw, wbits);
                 if (const uint64_t d = distinct_measured()) f->ensure_rows(d);
                 QSR_CUDA(cudaStreamSynchronize(f->stream));
-                struct Sink final : FramesSink {
-                    qsr_frames &f;
-                    uint64_t seed;
-                    uint32_t epoch = 1;
-                    Sink(qsr_frames &ff, uint64_t s) : f(ff), seed(s) {}
-                    void unitary(const uint64_t *g, uint64_t cnt, cudaStream_t st) override {
-                        launch_frame_window(f.xf, f.zf, f.pitch, g, cnt, f.num_sms, st);
-                    }
-                    void unpermute(const uint32_t *perm, cudaStream_t st) override {
-                        if (!f.xs) {
-                            f.xs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
-                            f.zs = static_cast<uint64_t *>(plane_cache().acquire(f.device, f.plane_bytes));
-                        }
-                        launch_unpermute_frame_rows(f.xf, f.xs, f.pitch, f.n, perm, f.num_sms, st);
-                        launch_unpermute_frame_rows(f.zf, f.zs, f.pitch, f.n, perm, f.num_sms, st);
-                        std::swap(f.xf, f.xs);
-                        std::swap(f.zf, f.zs);
-                    }
-                    void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) override {
-                        frames_measure_q(f, [&](uint64_t i) { return qubits[i]; }, m, seed, epoch++, st);
-                    }
-                } sink(*f, seed);
+                FramesRider sink(*f, seed);
                 RunTimes rt;
                 StreamCounts sc;
                 run_circuit_streaming(t, *c, seed, d_rec, rt, sc, &sink);
@@ -1280,18 +1375,8 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
                     }
                     uint64_t w1 = w;
                     while (w1 < W && !ds->is_meas[w1]) ++w1;
-                    if (gate_segment_enabled() && w1 - w >= 2 && f->n) {
-                        if (!f->seg_bar) QSR_CUDA(cudaMalloc(&f->seg_bar, 256));
-                        if (!f->xs) {
-                            f->xs = static_cast<uint64_t *>(plane_cache().acquire(f->device, f->plane_bytes));
-                            f->zs = static_cast<uint64_t *>(plane_cache().acquire(f->device, f->plane_bytes));
-                        }
-                        launch_frame_segment(f->xf, f->zf, f->pitch, f->n, ds->d_gates, ds->d_offsets + w,
-                                             uint32_t(w1 - w), f->num_sms, f->stream, f->seg_bar, f->xs, f->zs);
-                    } else {
-                        for (uint64_t v = w; v < w1; ++v)
-                            frames_window(*f, ds->d_gates + ds->offsets[v], ds->offsets[v + 1] - ds->offsets[v]);
-                    }
+                    for (uint64_t v = w; v < w1; ++v)
+                        frames_window(*f, ds->d_gates + ds->offsets[v], ds->offsets[v + 1] - ds->offsets[v]);
                     w = w1;
                 }
             }
@@ -1300,21 +1385,7 @@ static qsr_status sample_impl(const qsr_circuit *c, uint64_t shots, uint64_t see
             throw;
         }
         cudaFree(d_rec);
-        // Fold in the reference outcomes: per_qubit() = last outcome per qubit
-        // (measure.hpp:50-64, frames.hpp:183-202).
-        std::vector<int8_t> last(c->num_qubits, -1);
-        for (const auto &e : ref) last[e.qubit] = int8_t(e.outcome ? 1 : 0);
-        std::vector<uint32_t> flip_rows;
-        for (uint64_t r = 0; r < f->measured.size(); ++r)
-            if (last[f->measured[r]] == 1) flip_rows.push_back(uint32_t(r));
-        if (!flip_rows.empty()) {
-            f->ensure_idx(flip_rows.size());
-            QSR_CUDA(cudaMemcpyAsync(f->d_idx, flip_rows.data(), flip_rows.size() * 4,
-                                     cudaMemcpyHostToDevice, f->stream));
-            launch_record_fold(f->rec, f->pitch, f->kf, f->j0, f->shots, f->d_idx, flip_rows.size(),
-                               f->stream);
-        }
-        QSR_CUDA(cudaStreamSynchronize(f->stream));
+        fold_reference(*f, ref, c->num_qubits, f->stream);
         *out = f.release();
     });
 }
@@ -1333,6 +1404,64 @@ qsr_status qsr_frames_word_bits(const qsr_frames *f, unsigned *word_bits) {
     return guard([&] {
         REQUIRE_PTR(f); REQUIRE_PTR(word_bits);
         *word_bits = f->wbits;
+    });
+}
+
+// sample(circuit, shots, seed) on a resident engine (frames.hpp:163-204): the reference shot is
+// the engine's run, and the frames ride its windows on the same stream; *device_ms = CUDA-event
+// time of the whole call on that stream (frames init, reference shot + frames, record fold).
+qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int world, int rank,
+                             qsr_frames **out, double *device_ms) {
+    return guard([&] {
+        REQUIRE_PTR(e); REQUIRE_PTR(out);
+        if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
+        const uint64_t kf_all = (shots + 63) / 64;
+        if (world < 1 || uint64_t(world) > kf_all || rank < 0 || rank >= world)
+            fail(QSR_INVALID_ARGUMENT, "sample: world must be in [1, ceil(shots/64)], 0 <= rank < world");
+        const uint64_t w0 = kf_all * uint64_t(rank) / uint64_t(world);
+        const uint64_t nw = kf_all * uint64_t(rank + 1) / uint64_t(world) - w0;
+        DeviceTableau &t = *e->t;
+        QSR_CUDA(cudaSetDevice(t.device));
+        std::vector<uint8_t> seen(t.n, 0);
+        uint64_t distinct = 0;
+        for (const auto &mq : e->ds->mqubits)
+            for (uint32_t q : mq)
+                if (!seen[q]) { seen[q] = 1; ++distinct; }
+        cudaEvent_t a, b;
+        QSR_CUDA(cudaEventCreate(&a));
+        QSR_CUDA(cudaEventCreate(&b));
+        QSR_CUDA(cudaEventRecord(a, t.stream));
+        const uint64_t l0 = g_launches;
+        auto f = make_frames(t.n, shots, seed, t.device, w0, nw, 64, t.stream);
+        if (distinct) f->ensure_rows(distinct);
+        FramesRider rider(*f, seed);
+        e->last = RunTimes{};
+        run_device(t, *e->ds, seed, e->d_rec, e->last, &rider);
+        const uint64_t nm = e->ds->measure_count;
+        std::vector<qsr_record_entry> ref(nm);
+        if (nm)
+            QSR_CUDA(cudaMemcpyAsync(ref.data(), e->d_rec, nm * sizeof(qsr_record_entry), cudaMemcpyDeviceToHost,
+                                     t.stream));
+        t.sync();
+        fold_reference(*f, ref, t.n, t.stream);
+        QSR_CUDA(cudaEventRecord(b, t.stream));
+        QSR_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        QSR_CUDA(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        e->launches = g_launches - l0;
+        if (device_ms) *device_ms = ms;
+        f->own_stream();
+        *out = f.release();
+    });
+}
+
+qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes) {
+    return guard([&] {
+        REQUIRE_PTR(e);
+        REQUIRE_PTR(bytes);
+        *bytes = e->last.frames_bytes;
     });
 }
 

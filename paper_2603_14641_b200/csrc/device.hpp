@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "host.hpp"
@@ -23,9 +24,10 @@ namespace qsr {
 
 void cuda_check(cudaError_t e, const char *what);
 // The per-device caching allocator behind tableau planes and scratch (capi.cpp): a released
-// block is reused by the next acquire of the same size on the same device.
+// block is reused by the next acquire of the same size on the same device. `after`: the owner's
+// stream when the block may still be read by queued work; the next acquire waits for it.
 void *cache_acquire(int device, uint64_t bytes);
-void cache_release(int device, uint64_t bytes, void *p);
+void cache_release(int device, uint64_t bytes, void *p, cudaStream_t after = nullptr);
 #define QSR_CUDA(call) ::qsr::cuda_check((call), #call)
 
 extern uint64_t g_launches; // kernel launches issued by the library
@@ -103,10 +105,15 @@ struct DeviceTableau {
     uint64_t *sign_partials = nullptr;
     uint64_t sign_partial_chunks = 0;
     uint32_t *tile_counters = nullptr;
-    unsigned int *seg_bar = nullptr;       // grid barrier of the segment kernel
     uint64_t *gate_buf = nullptr;          // staging for single-window API calls
     uint64_t gate_buf_cap = 0;
     MeasureScratch ms;
+    // Optional measurement-pass profile (qsr_engine_profile): events around every absorb launch
+    // and a device counter of rows rewritten. Null on every timed path.
+    struct AbsorbProfile {
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+        unsigned long long *d_rows = nullptr;
+    } *prof = nullptr;
     uint8_t *arena = nullptr; // fixed-size scratch (signs, counters, measurement scratch), one block
     uint64_t arena_bytes = 0;
     int num_sms = 148;
@@ -122,20 +129,6 @@ struct DeviceTableau {
 // ---- launchers --------------------------------------------------------------------
 // Gate window on a CM tableau: `gates` is a device array of packed gate words.
 void launch_gate_window(DeviceTableau &t, const uint64_t *gates, uint64_t ngates);
-// Two consecutive windows as component records (pair.hpp; k_gates.cu K1p).
-constexpr int kPairRows = 6, kPairGates = 8, kPairRecWords = 16;
-void launch_gate_pairs(DeviceTableau &t, const uint64_t *recs, uint64_t nrec);
-void launch_frame_pairs(uint64_t *xf, uint64_t *zf, uint64_t pitch, const uint64_t *recs, uint64_t nrec,
-                        int num_sms, cudaStream_t st);
-// All windows of a unitary segment in one persistent launch (temporally blocked, L2-resident
-// slabs; k_gates.cu). d_woff = device window offsets into `gates` (nwin + 1 entries).
-bool gate_segment_enabled();
-void launch_gate_segment(DeviceTableau &t, const uint64_t *gates, const uint64_t *d_woff,
-                         uint32_t nwin);
-void launch_frame_segment(uint64_t *xf, uint64_t *zf, uint64_t pitch, uint64_t rows,
-                          const uint64_t *gates, const uint64_t *d_woff, uint32_t nwin,
-                          int num_sms, cudaStream_t st, unsigned int *bar, uint64_t *xs,
-                          uint64_t *zs); // xs, zs: scratch planes of the same size (slab-major)
 // Gate fusion support (fuse.hpp): the CM rows un-permuted (logical q <- physical perm[q]) into
 // the spare planes, which then become the current ones.
 void launch_unpermute_rows(DeviceTableau &t, const uint32_t *d_perm);
@@ -160,11 +153,7 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
                            bool timed, double *t_ms, double *ge_ms, double *cmp_ms);
 
 void configure_measure_kernels(DeviceTableau &t);
-// Up to kMaxBatch flagged collapses in one pass; returns how many were collapsed and whether
-// the batch stopped at a measurement that became deterministic (k_batch.cu).
-void measure_batch(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                   uint64_t seed, uint32_t &done, bool &det);
-// The three phases of measure_batch, separately (the sharded engine exchanges between them):
+// The three phases of a batch of <= kMaxBatch collapses (the sharded engine exchanges between them):
 // column bits + stabilizer OR-mask (bctl[2]); pivots / V rows / coins / record (leader
 // shard only); every row absorbs its V's.
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b);
@@ -172,7 +161,7 @@ void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b);
 // *d_pos = expect + len). nullptr: unconditional.
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
                   uint64_t seed, uint32_t *d_pos = nullptr, uint32_t expect = 0);
-bool batch_speculation(); // the split pivot kernels support speculative batches
+void configure_batch_kernels(int device); // per-device kernel attributes (current device)
 void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st);
 void batch_apply(DeviceTableau &t);
 // Deterministic outcome of measuring q (measure.hpp:343-376), sharded form: this shard's

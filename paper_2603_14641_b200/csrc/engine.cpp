@@ -1,7 +1,6 @@
 // Device-resident schedules, the single-shot driver and layout conversion (engine.hpp).
 #include "engine.hpp"
 #include "fuse.hpp"
-#include "pair.hpp"
 
 #include <cstring>
 #include <algorithm>
@@ -38,8 +37,6 @@ std::unique_ptr<DeviceSchedule> upload_schedule(uint64_t n, const Schedule &s, i
     const uint64_t G = s.gates.size();
     std::unique_ptr<uint64_t[]> packed(new uint64_t[std::max<uint64_t>(G, 1)]);
     for (uint64_t i = 0; i < G; ++i) packed[i] = pack_gate(s.gates[i]);
-    if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
-        sort_unitary_windows(packed.get(), s.offsets, s.is_meas);
     upload_packed(*ds, uint32_t(n), packed.get(), G, device, st, fuse);
     return ds;
 }
@@ -55,9 +52,9 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &
     const std::vector<uint8_t> is_meas = ds.is_meas;
     ds.offsets.assign(1, 0);
     ds.is_meas.clear();
-    ds.wkind.clear();
     ds.mqubits.clear();
     ds.wwords.clear();
+    ds.fwords.clear();
     constexpr uint32_t kDeferredWords = ~0u; // gate-window words, computed after fusion in parallel
     auto gate_words = [](const uint64_t *g, size_t cnt) {
         uint32_t words = 0;
@@ -65,60 +62,15 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &
             words += uint32_t(__builtin_popcount(packed_reads(g[i])) + __builtin_popcount(packed_writes(g[i])));
         return words;
     };
-    auto push_window = [&](uint8_t kind, uint64_t words) {
+    auto push_window = [&](uint64_t words) {
         ds.offsets.push_back(out.size());
         ds.is_meas.push_back(0);
-        ds.wkind.push_back(kind);
         ds.mqubits.emplace_back();
         ds.wwords.push_back(uint32_t(words));
-    };
-    // Window pairing (pair.hpp): a finished unitary window is held until the next one, and the
-    // two are rewritten as component records + the two windows' oversized remainders.
-    const bool pairing = pairing_enabled() && !gate_segment_enabled();
-    Pairer pairer(pairing ? n : 0);
-    PairOut po;
-    size_t held = SIZE_MAX; // start of the held window in `out` (it runs to out.size())
-    auto flush_held = [&] {
-        if (held == SIZE_MAX) return;
-        push_window(0, kDeferredWords);
-        held = SIZE_MAX;
+        ds.fwords.push_back(kDeferredWords);
     };
     auto close_unitary = [&](size_t s0) {
-        if (out.size() == s0) return;
-        if (!pairing) {
-            push_window(0, kDeferredWords);
-            return;
-        }
-        if (held == SIZE_MAX) {
-            held = s0;
-            return;
-        }
-        if (!pair_windows_of(s0 - held, out.size() - s0)) { // the held one goes alone, hold this one
-            const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
-            out.resize(s0);
-            push_window(0, kDeferredWords);
-            out.insert(out.end(), B.begin(), B.end());
-            held = s0;
-            return;
-        }
-        const std::vector<uint64_t> A(out.begin() + long(held), out.begin() + long(s0));
-        const std::vector<uint64_t> B(out.begin() + long(s0), out.end());
-        out.resize(held);
-        held = SIZE_MAX;
-        pairer.pair(A.data(), A.size(), B.data(), B.size(), po);
-        if (!po.records.empty()) {
-            if (out.size() & 1) out.push_back(0); // records start 16-byte aligned (see dispatch)
-            out.insert(out.end(), po.records.begin(), po.records.end());
-            push_window(1, po.record_words);
-        }
-        if (!po.rest_a.empty()) {
-            out.insert(out.end(), po.rest_a.begin(), po.rest_a.end());
-            push_window(0, kDeferredWords);
-        }
-        if (!po.rest_b.empty()) {
-            out.insert(out.end(), po.rest_b.begin(), po.rest_b.end());
-            push_window(0, kDeferredWords);
-        }
+        if (out.size() != s0) push_window(kDeferredWords);
     };
     for (size_t w = 0; w + 1 < offsets.size(); ++w) {
         const uint64_t b = offsets[w], e = offsets[w + 1];
@@ -130,7 +82,6 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &
         }
         f.flush(out);
         close_unitary(s0);
-        flush_held();
         auto unpermute_here = [&] {
             ds.perm_at.resize(ds.is_meas.size() + 1, -1);
             if (f.identity_permutation()) return;
@@ -147,14 +98,13 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &
         }
         ds.offsets.push_back(out.size());
         ds.is_meas.push_back(1);
-        ds.wkind.push_back(0);
         ds.mqubits.push_back(std::move(qs));
         ds.wwords.push_back(0);
+        ds.fwords.push_back(0);
     }
     const size_t s0 = out.size();
     f.flush(out);
     close_unitary(s0);
-    flush_held();
     ds.perm_at.resize(ds.is_meas.size() + 1, -1);
     if (!f.identity_permutation()) {
         ds.perm_at[ds.is_meas.size()] = int64_t(perms.size());
@@ -166,8 +116,16 @@ void fuse_into(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, WordVec &
     parallel_chunks(W, std::max(1u, std::min<unsigned>(host_threads(), unsigned(W / 8) + 1)),
                     [&](unsigned, uint64_t b, uint64_t e) {
                         for (uint64_t w = b; w < e; ++w)
-                            if (ds.wwords[w] == kDeferredWords)
-                                ds.wwords[w] = gate_words(out.data() + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
+                            if (ds.wwords[w] == kDeferredWords) {
+                                const uint64_t *g = out.data() + ds.offsets[w];
+                                const size_t cnt = ds.offsets[w + 1] - ds.offsets[w];
+                                ds.wwords[w] = gate_words(g, cnt);
+                                uint32_t fw = 0;
+                                for (size_t i = 0; i < cnt; ++i)
+                                    fw += uint32_t(__builtin_popcount(packed_reads_frames(g[i])) +
+                                                   __builtin_popcount(packed_writes(g[i])));
+                                ds.fwords[w] = fw;
+                            }
                     });
 }
 
@@ -199,12 +157,16 @@ void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint6
         }
     } else {
         for (size_t w = 0; w + 1 < ds.offsets.size(); ++w) {
-            uint32_t words = 0;
+            uint32_t words = 0, fw = 0;
             if (!ds.is_meas[w])
-                for (uint64_t i = ds.offsets[w]; i < ds.offsets[w + 1]; ++i)
+                for (uint64_t i = ds.offsets[w]; i < ds.offsets[w + 1]; ++i) {
                     words += uint32_t(__builtin_popcount(packed_reads(packed[i])) +
                                       __builtin_popcount(packed_writes(packed[i])));
+                    fw += uint32_t(__builtin_popcount(packed_reads_frames(packed[i])) +
+                                   __builtin_popcount(packed_writes(packed[i])));
+                }
             ds.wwords.push_back(words);
+            ds.fwords.push_back(fw);
         }
     }
     ds.d_gates_bytes = std::max<uint64_t>(DG, 1) * 8;
@@ -214,7 +176,6 @@ void upload_packed(DeviceSchedule &ds, uint32_t n, const uint64_t *packed, uint6
         QSR_CUDA(cudaMemcpyAsync(ds.d_gates, dev_gates, DG * 8, cudaMemcpyHostToDevice, st));
     }
     QSR_CUDA(cudaStreamSynchronize(st));
-    upload_offsets(ds, st);
 }
 
 // Circuit -> device schedule without materialising the API Schedule: the O(G) plan, then a
@@ -235,8 +196,6 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
         TraceScope tr("  scatter_windows");
         scatter_windows(c, p, packed.get(), [](const qsr_gate &g) { return pack_gate(g); });
     }
-    if (getenv("QSR_SORT_WINDOWS") && getenv("QSR_SORT_WINDOWS")[0] == '1')
-        sort_unitary_windows(packed.get(), p.offsets, p.is_meas);
 
     auto ds = std::make_unique<DeviceSchedule>();
     ds->device = device;
@@ -257,58 +216,10 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
     return ds;
 }
 
-// Device gate order inside a unitary window is free (operands are disjoint and the sign fold
-// is an XOR), so each window's packed gates are grouped by kind. The gate kernels hand gates to
-// CTAs / chunks strided (b, b + NB, ...), so every CTA still gets a representative kind mix,
-// while consecutive gates of a CTA share a kind and the 8-lane groups of a warp stay
-// convergent in the per-kind rule switch.
-// Measurement windows keep their order (it is the record order).
-void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
-                          const std::vector<uint8_t> &is_meas) {
-    const uint64_t W = is_meas.size();
-    const unsigned nt = std::max(1u, std::min(16u, host_threads()));
-    std::vector<std::thread> th;
-    for (unsigned t = 0; t < nt; ++t)
-        th.emplace_back([&, t] {
-            std::vector<uint64_t> tmp;
-            for (uint64_t w = t; w < W; w += nt) {
-                if (is_meas[w]) continue;
-                const uint64_t b = offsets[w], e = offsets[w + 1];
-                uint64_t cnt[16] = {0};
-                for (uint64_t i = b; i < e; ++i) ++cnt[(packed[i] >> 28) & 0xF];
-                uint64_t pos[16], acc = 0;
-                for (int k = 0; k < 16; ++k) { pos[k] = acc; acc += cnt[k]; }
-                tmp.resize(e - b);
-                for (uint64_t i = b; i < e; ++i) tmp[pos[(packed[i] >> 28) & 0xF]++] = packed[i];
-                std::copy(tmp.begin(), tmp.end(), packed + b);
-            }
-        });
-    for (auto &x : th) x.join();
-}
-
-void upload_offsets(DeviceSchedule &ds, cudaStream_t st) {
-    ds.d_offsets_bytes = ds.offsets.size() * 8;
-    ds.d_offsets = static_cast<uint64_t *>(cache_acquire(ds.device, ds.d_offsets_bytes));
-    QSR_CUDA(cudaMemcpyAsync(ds.d_offsets, ds.offsets.data(), ds.offsets.size() * 8,
-                             cudaMemcpyHostToDevice, st));
-    QSR_CUDA(cudaStreamSynchronize(st));
-}
-
 namespace {
 uint64_t launch_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1) {
-    if (gate_segment_enabled() && w1 - w0 >= 2) {
-        launch_gate_segment(t, ds.d_gates, ds.d_offsets + w0, uint32_t(w1 - w0));
-        return 1;
-    }
-    for (uint64_t w = w0; w < w1; ++w) {
-        const uint64_t cnt = ds.offsets[w + 1] - ds.offsets[w];
-        if (w < ds.wkind.size() && ds.wkind[w] == 1) {
-            const uint64_t b = ds.offsets[w] + (ds.offsets[w] & 1); // a pad word keeps 16-B alignment
-            launch_gate_pairs(t, ds.d_gates + b, (ds.offsets[w + 1] - b) / kPairRecWords);
-        } else {
-            launch_gate_window(t, ds.d_gates + ds.offsets[w], cnt);
-        }
-    }
+    for (uint64_t w = w0; w < w1; ++w)
+        launch_gate_window(t, ds.d_gates + ds.offsets[w], ds.offsets[w + 1] - ds.offsets[w]);
     return w1 - w0;
 }
 } // namespace
@@ -351,7 +262,7 @@ uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_
 // The single-shot driver on device-resident inputs (simulator.hpp:46-70). `record` is a
 // device array of measure_count entries.
 void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
-                qsr_record_entry *d_record, RunTimes &rt) {
+                qsr_record_entry *d_record, RunTimes &rt, FramesSink *frames) {
     cudaEvent_t e_start, e_end, a, b;
     QSR_CUDA(cudaEventCreate(&e_start));
     QSR_CUDA(cudaEventCreate(&e_end));
@@ -370,7 +281,21 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             QSR_CUDA(cudaEventRecord(a, t.stream));
             uint64_t w1 = w;
             while (w1 < W && !ds.is_meas[w1]) ++w1;
-            rt.gate_launches += run_unitary_windows(t, ds, w, w1, &rt.gate_bytes);
+            if (!frames) {
+                rt.gate_launches += run_unitary_windows(t, ds, w, w1, &rt.gate_bytes);
+            } else {
+                for (uint64_t v = w; v < w1; ++v) {
+                    const uint64_t *g = ds.d_gates + ds.offsets[v];
+                    const uint64_t cnt = ds.offsets[v + 1] - ds.offsets[v];
+                    launch_gate_window(t, g, cnt);
+                    frames->unitary(g, cnt, t.stream);
+                    if (v < ds.wwords.size()) {
+                        rt.gate_bytes += (8.0 * ds.wwords[v] + 16.0) * 2.0 * double(t.kg);
+                        rt.frames_bytes += 8.0 * ds.fwords[v] * double(frames->row_words);
+                    }
+                }
+                rt.gate_launches += 2 * (w1 - w);
+            }
             w = w1;
             QSR_CUDA(cudaEventRecord(b, t.stream));
             QSR_CUDA(cudaEventSynchronize(b));
@@ -379,18 +304,25 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             rt.to_ms += ms;
             continue;
         }
-        if (const uint32_t *perm = ds.perm_before(w)) launch_unpermute_rows(t, perm);
+        if (const uint32_t *perm = ds.perm_before(w)) {
+            launch_unpermute_rows(t, perm);
+            if (frames) frames->unpermute(perm, t.stream);
+        }
         const auto &mq = ds.mqubits[w];
         const uint64_t m = mq.size();
         t.ensure_window_cap(m);
         QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
         measure_window_device(t, m, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
+        if (frames) frames->measure(mq.data(), m, t.stream);
         QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, m * sizeof(qsr_record_entry),
                                  cudaMemcpyDeviceToDevice, t.stream));
         rec_off += m;
         ++w;
     }
-    if (const uint32_t *perm = ds.perm_before(W)) launch_unpermute_rows(t, perm);
+    if (const uint32_t *perm = ds.perm_before(W)) {
+        launch_unpermute_rows(t, perm);
+        if (frames) frames->unpermute(perm, t.stream);
+    }
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));
     float total = 0;

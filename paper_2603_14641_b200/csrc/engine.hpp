@@ -14,15 +14,14 @@ namespace qsr {
 struct DeviceSchedule {
     int device = 0;
     uint64_t *d_gates = nullptr;
-    uint64_t *d_offsets = nullptr; // device copy of offsets (segment kernel)
     std::vector<uint64_t> offsets;
     std::vector<uint8_t> is_meas;
-    std::vector<uint8_t> wkind; // unitary windows: 0 = packed gates, 1 = pair records (pair.hpp)
     std::vector<std::vector<uint32_t>> mqubits; // per window (empty for unitary windows)
     uint64_t measure_count = 0, unitary_count = 0; // of the circuit (before fusion)
     // Gate fusion (fuse.hpp): per-window device words moved per generator-word (reads + writes,
     // for the bytes accounting) and where the CM rows return to logical order.
     std::vector<uint32_t> wwords;
+    std::vector<uint32_t> fwords; // the same for the Pauli frames (no sign words)
     // perm_at[w] >= 0: before window w (w == num_windows: after the last one) un-permute the CM
     // rows with the logical -> physical map at d_perms + perm_at[w].
     std::vector<int64_t> perm_at;
@@ -39,12 +38,12 @@ struct DeviceSchedule {
         uint64_t kernels;
     };
     mutable std::vector<Graph> graphs;
-    uint64_t d_gates_bytes = 0, d_offsets_bytes = 0, d_perms_bytes = 0; // cached blocks
+    uint64_t d_gates_bytes = 0, d_perms_bytes = 0; // cached blocks
     ~DeviceSchedule() {
         cudaSetDevice(device);
+        cudaDeviceSynchronize(); // kernels reading d_gates may still be queued on the owner's stream
         for (auto &g : graphs) cudaGraphExecDestroy(g.exec);
         cache_release(device, d_gates_bytes, d_gates);
-        cache_release(device, d_offsets_bytes, d_offsets);
         cache_release(device, d_perms_bytes, d_perms);
     }
     const uint32_t *perm_before(uint64_t w) const {
@@ -63,22 +62,30 @@ std::unique_ptr<DeviceSchedule> upload_circuit(const Circuit &c, int device, cud
 struct RunTimes {
     double to_ms = 0, t_ms = 0, ge_ms = 0, cmp_ms = 0, total_ms = 0;
     double gate_bytes = 0; // algorithmic bytes of the gate-window launches (device gates)
-    uint64_t gate_launches = 0; // gate-window kernel launches (a segment launch covers many windows)
+    uint64_t gate_launches = 0; // gate-window kernel launches
+    double frames_bytes = 0;    // algorithmic bytes of the frames' window launches (sampling)
 };
 
-// Windows [w0, w1) (all unitary) on t: one temporally blocked segment launch when the segment
-// engine is on and there are >= 2 windows, else one launch per window. Returns launches.
+// Windows [w0, w1) (all unitary) on t: one launch per window (replayed as one CUDA graph from a
+// resident engine's second run on). Returns launches.
 uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_t w0, uint64_t w1,
                              double *bytes = nullptr);
-// Groups each unitary window's packed gates by kind (device order inside a window is free).
-void sort_unitary_windows(uint64_t *packed, const std::vector<uint64_t> &offsets,
-                          const std::vector<uint8_t> &is_meas);
-// Uploads ds.offsets to ds.d_offsets.
-void upload_offsets(DeviceSchedule &ds, cudaStream_t st);
 
-// The single-shot driver on device-resident inputs; `d_record` has measure_count entries.
+// Optional passenger of the stream: sample()'s Pauli frames ride the same (fused) device windows,
+// measurement windows and row un-permutes, on the tableau's stream (capi.cpp).
+struct FramesSink {
+    uint64_t row_words = 0; // shot-words per frames row (bytes accounting)
+    virtual ~FramesSink() = default;
+    virtual void unitary(const uint64_t *d_gates, uint64_t cnt, cudaStream_t st) = 0;
+    virtual void unpermute(const uint32_t *d_perm, cudaStream_t st) = 0;
+    virtual void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) = 0;
+};
+
+// The single-shot driver on device-resident inputs; `d_record` has measure_count entries. With
+// `frames`, the Pauli frames ride every window on t.stream (sample() on a resident schedule; the
+// unitary runs are then launched window by window, not replayed as graphs).
 void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
-                qsr_record_entry *d_record, RunTimes &rt);
+                qsr_record_entry *d_record, RunTimes &rt, FramesSink *frames = nullptr);
 void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,
                  const std::vector<qsr_record_entry> &record, double total_s);
 
@@ -86,14 +93,6 @@ void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &
 // (stream.cpp): windows are uploaded and launched as soon as they are final.
 struct StreamCounts {
     uint64_t unitary = 0, measures = 0, windows = 0;
-};
-// Optional passenger of the stream: sample()'s Pauli frames ride the same (fused) device windows,
-// measurement windows and row un-permutes, on the tableau's stream (capi.cpp).
-struct FramesSink {
-    virtual ~FramesSink() = default;
-    virtual void unitary(const uint64_t *d_gates, uint64_t cnt, cudaStream_t st) = 0;
-    virtual void unpermute(const uint32_t *d_perm, cudaStream_t st) = 0;
-    virtual void measure(const uint32_t *qubits, uint64_t m, cudaStream_t st) = 0;
 };
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                            qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,

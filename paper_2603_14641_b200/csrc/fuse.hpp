@@ -34,6 +34,8 @@ extern const uint8_t kCliff1Compose[24][6];
 // with signs (kind_reads / gate_writes of common.cuh). For the bytes-moved accounting.
 uint32_t packed_reads(uint64_t w);
 uint32_t packed_writes(uint64_t w);
+// The same without signs (Pauli frames, frames.hpp:76-94: X / Y / Z read nothing).
+uint32_t packed_reads_frames(uint64_t w);
 
 class Fuser {
   public:

@@ -455,56 +455,45 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
             det_partial(t);
             finish(t, seed, t.ms.out + fidx[pos]);
         };
-        if (!batch_speculation()) {
-            size_t pos = 0;
-            while (pos < fq.size()) {
-                uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - pos)), done = 0;
-                bool det = false;
-                measure_batch(t, t.ms.fq + pos, t.ms.fidx + pos, b, seed, done, det);
-                pos += done;
-                if (det) deterministic_at(pos++);
+        // Speculative double buffering: batch k+1 is enqueued (assuming batch k collapses all
+        // of its measurements) before the host reads batch k's length, so the device never
+        // waits for the host. A speculative batch behind one that stopped early finds the
+        // device position unequal to its start and does nothing (k_pivot_select).
+        MeasureScratch &ms = t.ms;
+        struct Pending { size_t start; uint32_t b; int slot; };
+        Pending queue[2];
+        int qhead = 0, qsize = 0, slot = 0;
+        size_t pos = 0, spec = 0;
+        set_device_u32(ms.d_pos, 0, t.stream);
+        while (pos < fq.size()) {
+            while (qsize < 2 && spec < fq.size()) {
+                const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
+                batch_colbits(t, ms.fq + spec, b);
+                batch_pivots(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec));
+                batch_apply(t);
+                QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 4 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
+                QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
+                queue[(qhead + qsize) % 2] = Pending{spec, b, slot};
+                ++qsize;
+                slot ^= 1;
+                spec += b;
             }
-        } else {
-            // Speculative double buffering: batch k+1 is enqueued (assuming batch k collapses all
-            // of its measurements) before the host reads batch k's length, so the device never
-            // waits for the host. A speculative batch behind one that stopped early finds the
-            // device position unequal to its start and does nothing (k_pivot_select).
-            MeasureScratch &ms = t.ms;
-            struct Pending { size_t start; uint32_t b; int slot; };
-            Pending queue[2];
-            int qhead = 0, qsize = 0, slot = 0;
-            size_t pos = 0, spec = 0;
-            set_device_u32(ms.d_pos, 0, t.stream);
-            while (pos < fq.size()) {
-                while (qsize < 2 && spec < fq.size()) {
-                    const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
-                    batch_colbits(t, ms.fq + spec, b);
-                    batch_pivots(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec));
-                    batch_apply(t);
-                    QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 4 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
-                    QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
-                    queue[(qhead + qsize) % 2] = Pending{spec, b, slot};
-                    ++qsize;
-                    slot ^= 1;
-                    spec += b;
+            const Pending p = queue[qhead];
+            qhead = (qhead + 1) % 2;
+            --qsize;
+            QSR_CUDA(cudaEventSynchronize(ms.bev[p.slot]));
+            const uint32_t *h = ms.h_bctl + 4 * p.slot;
+            if (h[3]) continue; // skipped (behind a batch that stopped early)
+            pos = p.start + h[0];
+            if (h[1]) {         // stopped: the measurement at pos is deterministic now
+                while (qsize) { // the speculative batch behind it is a no-op; drain it
+                    QSR_CUDA(cudaEventSynchronize(ms.bev[queue[qhead].slot]));
+                    qhead = (qhead + 1) % 2;
+                    --qsize;
                 }
-                const Pending p = queue[qhead];
-                qhead = (qhead + 1) % 2;
-                --qsize;
-                QSR_CUDA(cudaEventSynchronize(ms.bev[p.slot]));
-                const uint32_t *h = ms.h_bctl + 4 * p.slot;
-                if (h[3]) continue; // skipped (behind a batch that stopped early)
-                pos = p.start + h[0];
-                if (h[1]) {         // stopped: the measurement at pos is deterministic now
-                    while (qsize) { // the speculative batch behind it is a no-op; drain it
-                        QSR_CUDA(cudaEventSynchronize(ms.bev[queue[qhead].slot]));
-                        qhead = (qhead + 1) % 2;
-                        --qsize;
-                    }
-                    deterministic_at(pos++);
-                    set_device_u32(ms.d_pos, uint32_t(pos), t.stream);
-                    spec = pos;
-                }
+                deterministic_at(pos++);
+                set_device_u32(ms.d_pos, uint32_t(pos), t.stream);
+                spec = pos;
             }
         }
     } else {

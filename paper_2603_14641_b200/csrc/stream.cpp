@@ -17,6 +17,7 @@
 // planned; the tableau being built is then discarded, so no caller-visible state was mutated.
 #include <algorithm>
 #include <thread>
+#include <map>
 #include <mutex>
 #include <exception>
 #include <condition_variable>
@@ -26,7 +27,6 @@
 
 #include "engine.hpp"
 #include "fuse.hpp"
-#include "pair.hpp"
 
 namespace qsr {
 
@@ -46,6 +46,14 @@ struct PinnedRing {
             QSR_CUDA(cudaMallocHost(&buf[i], kRingGates * 8));
             QSR_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
         }
+    }
+    void reset() { // the previous call's copies have completed; start from slot 0, empty
+        for (int i = 0; i < 2; ++i) {
+            if (used[i]) QSR_CUDA(cudaEventSynchronize(done[i]));
+            used[i] = false;
+        }
+        cur = 0;
+        fill = 0;
     }
     ~PinnedRing() {
         for (int i = 0; i < 2; ++i) {
@@ -85,9 +93,16 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
     const uint32_t n = c.num_qubits;
     t.ensure_gate_buf(std::max<uint64_t>(G, 1));
     uint64_t *d_gates = t.gate_buf;
-    static thread_local std::unique_ptr<PinnedRing> ring_store;
-    if (!ring_store) ring_store = std::make_unique<PinnedRing>();
+    // One ring per (host thread, device): its events belong to the device whose stream records
+    // them, and every call starts from an empty ring.
+    static thread_local std::map<int, std::unique_ptr<PinnedRing>> rings;
+    std::unique_ptr<PinnedRing> &ring_store = rings[t.device];
+    if (!ring_store) {
+        QSR_CUDA(cudaSetDevice(t.device));
+        ring_store = std::make_unique<PinnedRing>();
+    }
     PinnedRing &ring = *ring_store;
+    ring.reset();
     using clk = std::chrono::steady_clock;
     auto since = [](clk::time_point a) { return std::chrono::duration<double, std::milli>(clk::now() - a).count(); };
 
@@ -152,11 +167,9 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
             // Stage one device window through the pinned ring (async H2D) and launch it. The device
             // gate buffer is used as a ring too: copies and kernels share t.stream, so a copy
             // into a recycled region runs after every kernel that read it.
-            // kind 1 = pair records (pair.hpp), 16-byte aligned.
-            auto launch_staged = [&](const uint64_t *src, uint64_t cnt, int kind = 0) {
+            auto launch_staged = [&](const uint64_t *src, uint64_t cnt) {
                 const auto ts = clk::now();
                 open_run();
-                if (kind == 1 && (dev_off & 1)) ++dev_off;
                 if (dev_off + cnt > t.gate_buf_cap) dev_off = 0;
                 for (uint64_t i = 0; i < cnt;) {
                     if (ring.fill == kRingGates) {
@@ -178,47 +191,14 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                     ring.fill += take;
                     i += take;
                 }
-                if (kind == 1) {
-                    launch_gate_pairs(t, d_gates + dev_off, cnt / kPairRecWords);
-                } else {
-                    launch_gate_window(t, d_gates + dev_off, cnt);
-                    if (frames) frames->unitary(d_gates + dev_off, cnt, t.stream);
-                }
+                launch_gate_window(t, d_gates + dev_off, cnt);
+                if (frames) frames->unitary(d_gates + dev_off, cnt, t.stream);
                 ++rt.gate_launches;
                 dev_off += cnt;
                 t_stage += since(ts);
             };
-            // Window pairing (pair.hpp): each finished unitary window is held until the next.
-            const bool pairing = fuse && pairing_enabled() && !gate_segment_enabled() && !frames;
-            Pairer pairer(pairing ? n : 0);
-            WordVec held;
-            PairOut po;
             auto unitary_window = [&](WordVec &w) {
-                if (w.empty()) return;
-                if (!pairing) {
-                    launch_staged(w.data(), w.size());
-                    return;
-                }
-                if (held.empty()) {
-                    held.swap(w);
-                    return;
-                }
-                if (!pair_windows_of(held.size(), w.size())) {
-                    launch_staged(held.data(), held.size());
-                    held.swap(w);
-                    return;
-                }
-                const auto tf = clk::now();
-                pairer.pair(held.data(), held.size(), w.data(), w.size(), po);
-                t_fuse += since(tf);
-                if (!po.records.empty()) launch_staged(po.records.data(), po.records.size(), 1);
-                if (!po.rest_a.empty()) launch_staged(po.rest_a.data(), po.rest_a.size());
-                if (!po.rest_b.empty()) launch_staged(po.rest_b.data(), po.rest_b.size());
-                held.clear();
-            };
-            auto flush_held = [&] {
-                if (!held.empty()) launch_staged(held.data(), held.size());
-                held.clear();
+                if (!w.empty()) launch_staged(w.data(), w.size());
             };
             // CM rows back to logical order (before a measurement window and at the end).
             auto unpermute = [&] {
@@ -263,7 +243,6 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                             dev.clear();
                             fuser.flush(dev);
                             unitary_window(dev);
-                            flush_held();
                             close_run();
                             unpermute();
                         }
@@ -295,7 +274,6 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                 dev.clear();
                 fuser.flush(dev);
                 unitary_window(dev);
-                flush_held();
                 close_run();
                 unpermute();
                 QSR_CUDA(cudaStreamSynchronize(t.stream));

@@ -49,7 +49,7 @@ def share_bytes(dist, payload: Optional[bytes], src: int = 0) -> bytes:
 
 def share_nccl_id(dist, rank: int) -> bytes:
     """Rank 0 creates the ncclUniqueId (through libqsr's NCCL); every rank receives it."""
-    from . import quasar as q
+    from paper_2603_14641_b200 import quasar as q  # (absolute: bench.py loads this file by path)
     uid = q.nccl_unique_id() if rank == 0 else None
     return share_bytes(dist, uid)
 

@@ -687,6 +687,27 @@ class Engine:
         check(lib.qsr_engine_record(self._h, ptr(rec)))
         return rec[:self._nm]
 
+    def sample(self, shots: int, seed: int, record: bool = True, world: int = 1, rank: int = 0):
+        """sample(circuit, shots, seed) (frames.hpp:163-204) on the resident schedule: returns
+        (ShotRecord or None, device ms); world > 1: shot-word slice `rank` (sample_shard).
+        record=False leaves the shot record on the device."""
+        h = C.c_void_p()
+        ms = C.c_double()
+        check(lib.qsr_engine_sample(self._h, shots, seed, world, rank, C.byref(h), C.byref(ms)))
+        f = FrameTableau(h)
+        return (f.record() if record else None), ms.value
+
+    def frames_bytes(self) -> float:
+        b = C.c_double()
+        check(lib.qsr_engine_frames_bytes(self._h, C.byref(b)))
+        return b.value
+
+    def profile(self, seed: int) -> dict:
+        """One extra run with CUDA events around every k_batch_absorb launch (not a timed run)."""
+        p = _lib.KernelProfile_t()
+        check(lib.qsr_engine_profile(self._h, seed, C.byref(p)))
+        return {f: getattr(p, f) for f, _ in p._fields_}
+
     def tableau_planes(self, n: int) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
         k = (n + 63) // 64
         x = np.empty(64 * k * 2 * k, dtype=np.uint64)

@@ -70,8 +70,10 @@ def test_large_window_many_chunks(q, oracle):
     assert_same(t, x, z, s)
 
 
-@pytest.mark.parametrize("n", [1, 5, 63, 64, 65, 130, 700])
+@pytest.mark.parametrize("n", [1, 5, 63, 64, 65, 130, 700, 1088, 9000])
 def test_transpose_matches_reference_layout(q, oracle, n):
+    """k_transpose (TMA blocks of 8 row-tiles x 16 words, both planes per launch): partial blocks
+    in both directions, RM row padding of up to 15 words (n = 1088: k = 17, rm_pitch = 32)."""
     t, x, z, s = scrambled(q, oracle, n, seed=100 + n, depth=5)
     t.transpose_in_place()
     lay = oracle.transpose(n, CM, x, z)
@@ -296,17 +298,13 @@ def test_mixed_bell_and_random(q, oracle):
     np.testing.assert_array_equal(r.record_array, rec)
 
 
-@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_GATE_ENGINE": "segment"},
-                                 {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"}, {"QSR_APPLY": "rows"},
-                                 {"QSR_PIVOTS": "fused"}, {"QSR_PAIR": "1", "QSR_STREAM": "0"},
-                                 {"QSR_PAIR": "1"}, {"QSR_GRAPHS": "0"}, {"QSR_PDL": "0"}])
+@pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"},
+                                 {"QSR_GRAPHS": "0"}, {"QSR_PDL": "0"}])
 def test_alternate_collapse_paths_match(q, env):
     """Every alternate path must agree with the default and the oracle: QSR_MEASURE_BATCH=0 (one
-    collapse per pass), QSR_GATE_ENGINE=segment (temporally blocked gates), QSR_FUSE=0 (no gate
-    fusion), QSR_STREAM=0 (schedule first, then run), QSR_APPLY=rows (row-major absorb, one V at
-    a time), QSR_PIVOTS=fused (single-CTA pivot kernel), QSR_PAIR=1 (consecutive windows as
-    component records, k_gate_pairs), QSR_GRAPHS=0 (no graph replay), QSR_PDL=0 (plain gate-window
-    launches instead of programmatic dependent launches)."""
+    collapse per pass, the path of uploaded tableaux), QSR_FUSE=0 (no gate fusion), QSR_STREAM=0
+    (schedule first, then run), QSR_GRAPHS=0 (no graph replay), QSR_PDL=0 (plain launches instead
+    of programmatic dependent launches)."""
     import subprocess
     import sys
     code = (
