@@ -96,14 +96,72 @@ inline TableauPtr upload(const Tableau<uint64_t> &t) {
     return p;
 }
 
-// Download into a reference Tableau (ColumnMajor results only, which is every result of the
-// functions below: run_single_shot, apply_window and measure_window all end ColumnMajor).
+// Download into a reference Tableau of the same layout (the device converts its internal
+// generator-major RowMajor back to the reference's i-major storage, tableau.hpp:91-94).
 inline void download(qsr_tableau *h, Tableau<uint64_t> &t) {
     int layout = 0;
     check(qsr_tableau_info(h, nullptr, nullptr, nullptr, &layout));
-    if (layout != QSR_COLUMN_MAJOR || t.layout() != Layout::ColumnMajor)
-        throw std::logic_error("quasar::gpu: only ColumnMajor tableaux are downloaded");
+    if ((layout == QSR_ROW_MAJOR) != (t.layout() == Layout::RowMajor))
+        throw std::logic_error("quasar::gpu: host and device layouts differ");
     check(qsr_tableau_download(h, t.x_plane().data(), t.z_plane().data(), t.signs().data()));
+}
+
+// A zero Tableau<W> in `layout`. tableau.hpp has no layout setter: the only way to a RowMajor
+// object is its own transpose_in_place, run here on zeros (a flag flip, no user data).
+template <Word W>
+Tableau<W> blank(size_t n, Layout layout) {
+    Tableau<W> t(n);
+    if (layout == Layout::RowMajor) t.transpose_in_place();
+    return t;
+}
+
+// Logical-bit copy between word types (same n, same layout): x / z bit of every (generator,
+// qubit) and every sign, through the reference's own accessors (tableau.hpp:98-114).
+template <Word A, Word B>
+void copy_bits(const Tableau<A> &a, Tableau<B> &b) {
+    const size_t n = a.num_qubits();
+    for (size_t g = 0; g < 2 * n; ++g) {
+        for (size_t q = 0; q < n; ++q) {
+            b.set_x_bit(g, q, a.x_bit(g, q));
+            b.set_z_bit(g, q, a.z_bit(g, q));
+        }
+        b.set_sign_bit(g, a.sign_bit(g));
+    }
+}
+
+// Runs `op(qsr_tableau *)` on the device copy of t and writes the result back into t (in the
+// layout the device ends in). Every W: other word types go through a 64-bit image.
+template <Word W, typename Op>
+void on_device(Tableau<W> &t, Op op) {
+    if constexpr (std::is_same_v<W, uint64_t>) {
+        auto h = upload(t);
+        op(h.get());
+        int layout = 0;
+        check(qsr_tableau_info(h.get(), nullptr, nullptr, nullptr, &layout));
+        const Layout lay = layout == QSR_ROW_MAJOR ? Layout::RowMajor : Layout::ColumnMajor;
+        if (lay != t.layout()) t = blank<uint64_t>(t.num_qubits(), lay);
+        download(h.get(), t);
+    } else {
+        Tableau<uint64_t> t64 = blank<uint64_t>(t.num_qubits(), t.layout());
+        copy_bits(t, t64);
+        on_device(t64, op);
+        Tableau<W> out = blank<W>(t.num_qubits(), t64.layout());
+        copy_bits(t64, out);
+        t = std::move(out);
+    }
+}
+
+// Read-only device query on t (every W).
+template <Word W, typename Op>
+void query_device(const Tableau<W> &t, Op op) {
+    if constexpr (std::is_same_v<W, uint64_t>) {
+        auto h = upload(t);
+        op(h.get());
+    } else {
+        Tableau<uint64_t> t64 = blank<uint64_t>(t.num_qubits(), t.layout());
+        copy_bits(t, t64);
+        query_device(t64, op);
+    }
 }
 
 // Tableau<W> <-> Tableau<uint64_t>, ColumnMajor (tableau.hpp:51-61): the generator bits of every
@@ -337,6 +395,167 @@ ShotRecord<W> sample(const Circuit &circuit, size_t shots, uint64_t seed, RunRep
                 static_cast<W>(words[row * kf64 + j / per] >> (8 * sizeof(W) * (j % per)));
     if (report) *report = detail::report(rep);
     return r;
+}
+
+// ---- measurement kernels of measure_window, one at a time (measure.hpp:104-376) -----------
+// Same preconditions and exceptions as the reference (RowMajor tableaux, invalid_argument on an
+// empty pivot list, a block size of 0 or a swap precondition; logic_error on an odd phase).
+
+// find_probabilistic(t, window)   (measure.hpp:104-126)
+template <Word W>
+std::vector<int64_t> find_probabilistic(const Tableau<W> &t, const Window &window) {
+    if (t.layout() != Layout::RowMajor) throw std::invalid_argument("find_probabilistic: tableau must be RowMajor");
+    std::vector<int64_t> out(window.gates.size(), -1);
+    detail::query_device(t, [&](qsr_tableau *h) {
+        check(qsr_find_probabilistic(h, detail::gates(window.gates), window.gates.size(), out.data()));
+    });
+    return out;
+}
+
+// find_and_compact_pivots(t, q, scratch)   (measure.hpp:130-150)
+template <Word W>
+PivotList find_and_compact_pivots(const Tableau<W> &t, size_t q, MeasureScratch<W> &) {
+    if (t.layout() != Layout::RowMajor)
+        throw std::invalid_argument("find_and_compact_pivots: tableau must be RowMajor");
+    PivotList p;
+    p.entries.assign(t.num_qubits(), -1);
+    uint64_t count = 0;
+    detail::query_device(t, [&](qsr_tableau *h) { check(qsr_find_and_compact_pivots(h, q, p.entries.data(), &count)); });
+    p.count = count;
+    return p;
+}
+
+// parallel_ge(t, pivots, scratch, block_targets)   (measure.hpp:161-273); the block size never
+// changes bits (test_measure.cpp:112-145) and is validated like the reference's.
+template <Word W>
+void parallel_ge(Tableau<W> &t, const PivotList &pivots, MeasureScratch<W> &, size_t block_targets = kGeBlockTargets) {
+    if (t.layout() != Layout::RowMajor) throw std::invalid_argument("parallel_ge: tableau must be RowMajor");
+    if (pivots.count == 0) throw std::invalid_argument("parallel_ge: empty pivot list");
+    if (block_targets < 1) throw std::invalid_argument("parallel_ge: block size must be >= 1");
+    detail::on_device(t, [&](qsr_tableau *h) {
+        check(qsr_parallel_ge(h, pivots.entries.data(), pivots.count, block_targets));
+    });
+}
+
+// swap_anti_commuting(t, p, q, scratch)   (measure.hpp:279-332)
+template <Word W>
+void swap_anti_commuting(Tableau<W> &t, size_t p, size_t q, MeasureScratch<W> &) {
+    if (t.layout() != Layout::RowMajor) throw std::invalid_argument("swap_anti_commuting: tableau must be RowMajor");
+    detail::on_device(t, [&](qsr_tableau *h) { check(qsr_swap_anti_commuting(h, p, q)); });
+}
+
+// inject_x(t, p)   (measure.hpp:335-338)
+template <Word W>
+void inject_x(Tableau<W> &t, size_t p) {
+    detail::on_device(t, [&](qsr_tableau *h) { check(qsr_inject_x(h, p)); });
+}
+
+// deterministic_outcome(t, q, scratch)   (measure.hpp:343-376)
+template <Word W>
+bool deterministic_outcome(const Tableau<W> &t, size_t q, MeasureScratch<W> &) {
+    if (t.layout() != Layout::RowMajor)
+        throw std::invalid_argument("deterministic_outcome: tableau must be RowMajor");
+    uint8_t o = 0;
+    detail::query_device(t, [&](qsr_tableau *h) { check(qsr_deterministic_outcome(h, q, &o)); });
+    return o != 0;
+}
+
+// Tableau::transpose_in_place()   (tableau.hpp:166-176) as a free function (a member cannot
+// be replaced from outside the class): the device's one-pass TMA transpose, every W.
+template <Word W>
+void transpose_in_place(Tableau<W> &t) {
+    detail::on_device(t, [&](qsr_tableau *h) { check(qsr_transpose_in_place(h)); });
+}
+
+// ---- Pauli frames one step at a time (frames.hpp:46-158), every W ---------------------------
+namespace detail {
+template <Word W>
+FramesPtr frames_upload(const FrameTableau<W> &f) {
+    qsr_frames *h = nullptr;
+    check(qsr_init_frames_word(f.n, f.shots, 0, unsigned(8 * sizeof(W)), device(), &h));
+    FramesPtr p(h);
+    uint64_t kf64 = 0;
+    check(qsr_frames_info(h, nullptr, nullptr, &kf64));
+    std::vector<uint64_t> x(f.n * kf64, 0), z(f.n * kf64, 0);
+    constexpr size_t bits = 8 * sizeof(W), per = 64 / bits;
+    for (size_t q = 0; q < f.n; ++q)
+        for (size_t j = 0; j < f.kf; ++j) {
+            x[q * kf64 + j / per] |= uint64_t(f.xf[q * f.kf + j]) << (bits * (j % per));
+            z[q * kf64 + j / per] |= uint64_t(f.zf[q * f.kf + j]) << (bits * (j % per));
+        }
+    check(qsr_frames_upload(h, x.data(), z.data()));
+    return p;
+}
+template <Word W>
+void frames_download(qsr_frames *h, FrameTableau<W> &f) {
+    uint64_t kf64 = 0;
+    check(qsr_frames_info(h, nullptr, nullptr, &kf64));
+    std::vector<uint64_t> x(f.n * kf64), z(f.n * kf64);
+    check(qsr_frames_download(h, x.data(), z.data()));
+    constexpr size_t bits = 8 * sizeof(W), per = 64 / bits;
+    for (size_t q = 0; q < f.n; ++q)
+        for (size_t j = 0; j < f.kf; ++j) {
+            f.xf[q * f.kf + j] = static_cast<W>(x[q * kf64 + j / per] >> (bits * (j % per)));
+            f.zf[q * f.kf + j] = static_cast<W>(z[q * kf64 + j / per] >> (bits * (j % per)));
+        }
+}
+} // namespace detail
+
+// init_frames<W>(n, shots, seed)   (frames.hpp:46-72): Z frames drawn on the device with
+// sample<W>'s keys (Philox(seed, 1, 0, (q << 24) | j) per W-word j).
+template <Word W>
+FrameTableau<W> init_frames(size_t n, size_t shots, uint64_t seed) {
+    if (shots < 1) throw std::invalid_argument("init_frames: shots must be >= 1");
+    qsr_frames *h = nullptr;
+    check(qsr_init_frames_word(n, shots, seed, unsigned(8 * sizeof(W)), device(), &h));
+    detail::FramesPtr p(h);
+    FrameTableau<W> f;
+    f.n = n;
+    f.shots = shots;
+    f.kf = words_for<W>(shots);
+    f.xf.assign(n * f.kf, W{0});
+    f.zf.assign(n * f.kf, W{0});
+    detail::frames_download(h, f);
+    return f;
+}
+
+// apply_window_frames(f, window)   (frames.hpp:76-94)
+template <Word W>
+void apply_window_frames(FrameTableau<W> &f, const Window &window) {
+    if (window.is_measurement) throw std::invalid_argument("apply_window_frames: measurement window");
+    auto h = detail::frames_upload(f);
+    check(qsr_apply_window_frames(h.get(), detail::gates(window.gates), window.gates.size(), 0));
+    detail::frames_download(h.get(), f);
+}
+
+// measure_sample(f, window, record, seed, epoch)   (frames.hpp:111-158): the device records the
+// window's X frames and redraws their Z frames; rows merge into `record` with the reference's
+// row reuse for qubits measured before.
+template <Word W>
+void measure_sample(FrameTableau<W> &f, const Window &window, ShotRecord<W> &record, uint64_t seed, uint32_t epoch) {
+    if (!window.is_measurement) throw std::invalid_argument("measure_sample: not a measurement window");
+    auto h = detail::frames_upload(f);
+    check(qsr_measure_sample(h.get(), detail::gates(window.gates), window.gates.size(), 1, seed, epoch));
+    uint64_t nrows = 0, kf64 = 0;
+    check(qsr_frames_record(h.get(), &nrows, nullptr, nullptr));
+    check(qsr_frames_info(h.get(), nullptr, nullptr, &kf64));
+    std::vector<uint32_t> measured(nrows);
+    std::vector<uint64_t> words(nrows * kf64);
+    if (nrows) check(qsr_frames_record(h.get(), &nrows, measured.data(), words.data()));
+    detail::frames_download(h.get(), f);
+    constexpr size_t bits = 8 * sizeof(W), per = 64 / bits;
+    for (size_t m = 0; m < measured.size(); ++m) {
+        const uint32_t q = measured[m];
+        size_t row = record.measured.size();
+        for (size_t r = 0; r < record.measured.size(); ++r)
+            if (record.measured[r] == q) { row = r; break; }
+        if (row == record.measured.size()) {
+            record.measured.push_back(q);
+            record.words.resize(record.measured.size() * f.kf, W{0});
+        }
+        for (size_t j = 0; j < f.kf; ++j)
+            record.words[row * f.kf + j] = static_cast<W>(words[m * kf64 + j / per] >> (bits * (j % per)));
+    }
 }
 
 // parse_qasm(text)   (qasm.hpp:159-252): same Circuit, same QasmError (line, column, reason);

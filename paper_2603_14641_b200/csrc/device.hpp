@@ -156,11 +156,17 @@ void configure_measure_kernels(DeviceTableau &t);
 // The three phases of a batch of <= kMaxBatch collapses (the sharded engine exchanges between them):
 // column bits + stabilizer OR-mask (bctl[2]); pivots / V rows / coins / record (leader
 // shard only); every row absorbs its V's.
-void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b);
+void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b, bool zero_block = false);
+// Sharded batch plan from the all-gathered masks (k_batch.cu k_shard_plan): plan[4] =
+// {this shard leads, lim, deterministic now, skipped}, on the device.
+void shard_plan(DeviceTableau &t, const uint32_t *d_masks, int world, int rank, uint32_t b, uint32_t expect,
+                uint32_t *d_plan);
 // d_pos / expect: speculative batches (the batch is a no-op unless *d_pos == expect; on success
 // *d_pos = expect + len). nullptr: unconditional.
+// d_plan (sharded): only the plan's leader selects, at most plan[1] collapses.
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                  uint64_t seed, uint32_t *d_pos = nullptr, uint32_t expect = 0);
+                  uint64_t seed, uint32_t *d_pos = nullptr, uint32_t expect = 0,
+                  const uint32_t *d_plan = nullptr);
 void configure_batch_kernels(int device); // per-device kernel attributes (current device)
 void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st);
 void batch_apply(DeviceTableau &t);
@@ -170,8 +176,9 @@ void batch_apply(DeviceTableau &t);
 // written to *out (deterministic entry) and ctl.
 uint64_t det_slot_words(const DeviceTableau &t);
 void det_local_partial(DeviceTableau &t, uint64_t q, uint64_t *slot);
+// slot_stride: words between consecutive shards' slots (0 = det_slot_words).
 void det_combine(DeviceTableau &t, uint64_t q, const uint64_t *slots, uint32_t nslots,
-                 qsr_record_entry *out);
+                 qsr_record_entry *out, uint64_t slot_stride = 0);
 // Probabilistic flags of a measurement window on this tableau/shard (find_probabilistic,
 // measure.hpp:104-126) into t.ms.flags (device; m bytes).
 void flags_cm(DeviceTableau &t, uint64_t m);

@@ -27,6 +27,15 @@ __global__ void k_max_u8(PtrList bufs, int nbuf, size_t bytes) {
     }
 }
 
+__global__ void k_max_u64(PtrList bufs, int nbuf, size_t words) {
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < words;
+         i += size_t(gridDim.x) * blockDim.x) {
+        uint64_t v = reinterpret_cast<const uint64_t *>(bufs.p[0])[i];
+        for (int b = 1; b < nbuf; ++b) v = max(v, reinterpret_cast<const uint64_t *>(bufs.p[b])[i]);
+        for (int b = 0; b < nbuf; ++b) reinterpret_cast<uint64_t *>(bufs.p[b])[i] = v;
+    }
+}
+
 class LocalExchange final : public Exchange {
   public:
     LocalExchange(int w, const std::vector<cudaStream_t> &st) {
@@ -72,6 +81,17 @@ class LocalExchange final : public Exchange {
         for (int i = 0; i < world; ++i) pl.p[i] = static_cast<uint8_t *>(buf[i]);
         const unsigned blocks = unsigned(std::min<size_t>((bytes + 255) / 256, 1024));
         k_max_u8<<<blocks, 256, 0, streams[0]>>>(pl, world, bytes);
+        QSR_CUDA(cudaGetLastError());
+        count_launch();
+        barrier();
+    }
+    void allreduce_max_u64(const std::vector<void *> &buf, size_t words) override {
+        if (words == 0) return;
+        barrier();
+        PtrList pl{};
+        for (int i = 0; i < world; ++i) pl.p[i] = static_cast<uint8_t *>(buf[i]);
+        const unsigned blocks = unsigned(std::min<size_t>((words + 255) / 256, 1024));
+        k_max_u64<<<blocks, 256, 0, streams[0]>>>(pl, world, words);
         QSR_CUDA(cudaGetLastError());
         count_launch();
         barrier();
@@ -176,6 +196,11 @@ class NcclExchange final : public Exchange {
     void allreduce_max_u8(const std::vector<void *> &buf, size_t bytes) override {
         if (bytes == 0) return;
         nccl_check(nccl().AllReduce(buf[0], buf[0], bytes, ncclUint8, ncclMax, comm, streams[0]),
+                   "ncclAllReduce");
+    }
+    void allreduce_max_u64(const std::vector<void *> &buf, size_t words) override {
+        if (words == 0) return;
+        nccl_check(nccl().AllReduce(buf[0], buf[0], words, ncclUint64, ncclMax, comm, streams[0]),
                    "ncclAllReduce");
     }
     const char *kind() const override { return "nccl"; }

@@ -36,6 +36,9 @@ class Exchange {
                            size_t bytes) = 0;
     // In place, element-wise max over uint8.
     virtual void allreduce_max_u8(const std::vector<void *> &buf, size_t bytes) = 0;
+    // In place, element-wise max over uint64: a broadcast from a root the host does not know
+    // when every other shard contributes zeros (the batch block, shard.cpp).
+    virtual void allreduce_max_u64(const std::vector<void *> &buf, size_t words) = 0;
     virtual const char *kind() const = 0;
 };
 

@@ -74,8 +74,13 @@ __device__ __forceinline__ uint32_t membership(uint32_t cb, const uint32_t *vbco
 __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64_t nrows,
                           uint64_t ng, const uint32_t *__restrict__ fq, uint32_t b,
                           uint32_t *__restrict__ colbits, uint32_t *__restrict__ stab_or,
-                          uint32_t *__restrict__ nz) {
+                          uint32_t *__restrict__ nz, uint64_t *__restrict__ zero, uint64_t zero_words) {
     pdl_wait();
+    // Sharded engine: the pivot rows + vinfo of this shard's batch block start at zero, so the
+    // block exchange can be a root-free max-all-reduce (only the leader writes non-zeros).
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < zero_words;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        zero[i] = 0;
     __shared__ uint32_t sq[kB];
     if (threadIdx.x < b) sq[threadIdx.x] = fq[threadIdx.x];
     __syncthreads();
@@ -115,8 +120,13 @@ constexpr int kWin = kSelThreads * kSelRows;
 __global__ void __launch_bounds__(kSelThreads)
 k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
                uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
-               uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect) {
+               uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect,
+               const uint32_t *__restrict__ plan) {
     pdl_wait();
+    if (plan) { // sharded: only the batch's leader selects (the others' blocks stay zero)
+        if (!plan[0]) return;
+        b = min(b, plan[1]);
+    }
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
     __shared__ uint32_t s_scan[kSelThreads / 32];
@@ -126,7 +136,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     if (tid < kB) s_vbcol[tid] = 0;
     // Speculative batches (measure_window_device): a batch enqueued behind one that stopped
     // early starts at the wrong position and turns into a no-op.
-    if (d_pos && *d_pos != expect) {
+    if (!plan && d_pos && *d_pos != expect) {
         if (tid < kB) vinfo[VI_C + tid] = 0xFFFFFFFFu;
         if (tid == 0) { bctl[BL_LEN] = 0; bctl[BL_DET] = 0; bctl[BL_SKIP] = 1; }
         return;
@@ -247,14 +257,35 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     }
     if (tid == 0) {
         bctl[BL_LEN] = len;
-        bctl[BL_DET] = s_stop;
-        if (d_pos) *d_pos = expect + len;
+        bctl[BL_DET] = s_stop; // (d_pos advances in k_batch_member, on every shard)
     }
 }
 
 
 
 __global__ void k_set_u32(uint32_t *p, uint32_t v) { *p = v; }
+
+// Sharded batch plan, computed identically on every shard from the all-gathered stabilizer
+// OR-masks (shard.cpp): the leader L = first shard with bit 0 set holds the global pivot of
+// collapse 0; a shard d < L has no stabilizer with X at q_m for m < ctz(mask_d), so L can run
+// the batch's first lim = min(b, min_{d<L} ctz(mask_d)) collapses alone. No L: the measurement
+// is deterministic now (measure.hpp:417-421). A speculative batch whose start is not the device
+// position is skipped. plan = {this shard leads, lim, deterministic, skipped}.
+__global__ void k_shard_plan(const uint32_t *__restrict__ masks, int world, int rank, uint32_t b,
+                             uint32_t expect, const uint32_t *__restrict__ d_pos, uint32_t *__restrict__ plan) {
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    const bool skip = *d_pos != expect;
+    int L = -1;
+    for (int r = 0; r < world && L < 0; ++r)
+        if (masks[r] & 1u) L = r;
+    uint32_t lim = b;
+    for (int r = 0; r < L; ++r) lim = min(lim, masks[r] ? uint32_t(__ffs(masks[r]) - 1) : 32u);
+    plan[0] = (!skip && L == rank) ? 1u : 0u;
+    plan[1] = lim;
+    plan[2] = (!skip && L < 0) ? 1u : 0u;
+    plan[3] = skip ? 1u : 0u;
+}
 
 // Batch start: control words and the pivot kernels' phase sums (one launch instead of two
 // memsets, so the whole batch chain is kernel-to-kernel).
@@ -376,7 +407,8 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
     __shared__ int s_e[kB];
     const uint32_t lane = threadIdx.x;
     const uint32_t len = bctl[BL_LEN];
-    const uint64_t idx0 = *coin_index;
+    if (len == 0) return;
+    const uint64_t idx0 = *coin_index; // advanced by len in k_batch_member
     if (lane < len) {
         const uint64_t c = vinfo[VI_C + lane] - g0, rs = ng + c;
         s_c[lane] = uint32_t(c);
@@ -414,7 +446,6 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
         if (s_coin[lane]) atomicOr(sw + (rs >> 6), br); else atomicAnd(sw + (rs >> 6), ~br);
     }
     if (__any_sync(0xffffffffu, odd) && lane == 0) atomicExch(err, 1);
-    if (lane == 0) *coin_index = idx0 + len;
     __syncwarp();
     if (lane < len) {
         out[fidx[lane]] = qsr_record_entry{fq[lane], uint8_t(s_coin[lane]), 0};
@@ -455,12 +486,19 @@ __global__ void __launch_bounds__(256)
 k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint64_t g0,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-               uint32_t *__restrict__ pmat, uint32_t row_blocks, unsigned long long *__restrict__ touched) {
+               uint32_t *__restrict__ pmat, uint32_t row_blocks, unsigned long long *__restrict__ touched,
+               uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index) {
     pdl_wait();
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
     __shared__ uint32_t s_p;
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
+    // The batch's collapses are done deciding: advance the speculation position and the coin
+    // index on every shard alike (k_pivot_finish drew coins idx0 .. idx0 + len - 1).
+    if (blockIdx.x == 0 && tid == 0 && len) {
+        if (d_pos) *d_pos += len;
+        *coin_index += len;
+    }
     if (blockIdx.x >= row_blocks) {
         // Pair-parity row j over one word chunk (chunks x 256 threads stride the words); the
         // chunks' partial rows are XOR-combined by k_batch_signs (no zeroing, no atomics).
@@ -725,15 +763,26 @@ static void launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cu
     QSR_CUDA(cudaGetLastError());
 }
 
-void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b) {
+void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b, bool zero_block) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     // Control words and the pivot kernels' phase sums, zeroed ahead of the chain.
     launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount);
+    // The pivot rows and vinfo of the block (everything before bctl), zeroed for a sharded batch.
+    const uint64_t zw = zero_block ? uint64_t(reinterpret_cast<uint64_t *>(ms.vinfo) - ms.batch_block) +
+                                         (kVinfoWords * 4 + 7) / 8
+                                   : 0;
     launch_chain(k_colbits, dim3(unsigned((nrows + 255) / 256)), dim3(256), 0, t.stream,
                  static_cast<const uint64_t *>(t.x), t.rm_pitch, nrows, t.ng, d_fq, b, ms.colbits,
-                 ms.bctl + BL_STAB_OR, ms.nz);
+                 ms.bctl + BL_STAB_OR, ms.nz, ms.batch_block, zw);
     count_launch(2);
+}
+
+void shard_plan(DeviceTableau &t, const uint32_t *d_masks, int world, int rank, uint32_t b, uint32_t expect,
+                uint32_t *d_plan) {
+    launch_chain(k_shard_plan, dim3(1), dim3(32), 0, t.stream, d_masks, world, rank, b, expect,
+                 static_cast<const uint32_t *>(t.ms.d_pos), d_plan);
+    count_launch();
 }
 
 void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st) {
@@ -743,11 +792,11 @@ void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st) {
 }
 
 void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                  uint64_t seed, uint32_t *d_pos, uint32_t expect) {
+                  uint64_t seed, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
     MeasureScratch &ms = t.ms;
     // (ms.pcount was zeroed by batch_colbits, which always precedes on this tableau.)
     launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
-                 t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect);
+                 t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan);
     launch_chain(k_pivot_rows, dim3(unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads)),
                  dim3(kRowThreads), 0, t.stream, t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz,
                  ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
@@ -792,7 +841,7 @@ void batch_apply(DeviceTableau &t) {
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
     launch_chain(k_batch_member, dim3(row_blocks + kB * kPmatChunks), dim3(256), 0, t.stream, ms.colbits,
                  nrows, t.ng, t.g0, ms.Vx, ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl, ms.gconst, row_blocks,
-                 t.prof ? t.prof->d_rows : nullptr);
+                 t.prof ? t.prof->d_rows : nullptr, ms.d_pos, ms.coin_index);
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (t.prof) {
         QSR_CUDA(cudaEventCreate(&ea));

@@ -548,8 +548,8 @@ void det_local_partial(DeviceTableau &t, uint64_t q, uint64_t *slot) {
 }
 
 void det_combine(DeviceTableau &t, uint64_t q, const uint64_t *slots, uint32_t nslots,
-                 qsr_record_entry *out) {
-    const uint64_t sw = det_slot_words(t);
+                 qsr_record_entry *out, uint64_t slot_stride) {
+    const uint64_t sw = slot_stride ? slot_stride : det_slot_words(t);
     k_det_reduce<<<1, 1024, 0, t.stream>>>(
         slots, slots + t.rm_pitch,
         reinterpret_cast<int64_t *>(const_cast<uint64_t *>(slots) + 2 * t.rm_pitch), sw, sw,

@@ -9,24 +9,30 @@
 // and both transposes are shard-local: zero communication for ~all of the bytes.
 //
 // Measurement window (measure.hpp:381-442), per process:
-//   flags      local find_probabilistic (CM) -> max-all-reduce (u8 per measurement)
-//   collapses  batches of <= 32 flagged measurements (k_batch.cu). The reference's pivot is
-//              the smallest stabilizer with X at q. Each shard ORs its stabilizers' batch-start
-//              bits into a 32-bit mask (all-gather, 4 B per shard). The leader L = the first
-//              shard with bit 0 set holds the global pivot of collapse 0. A shard d < L has no
-//              stabilizer with X at q_m for m < ctz(mask_d): its rows can neither be pivots nor
-//              change before that. So L alone computes pivots, pivot rows and coins for
-//              m < lim = min(b, min_{d<L} ctz(mask_d)); it stops earlier if it has no candidate.
-//              The pivot block (V rows + vinfo) is broadcast from L. Every shard then absorbs it
-//              into its own rows in one pass, including the leader.
+//   flags      local find_probabilistic (CM) -> max-all-reduce (u8 per measurement); the host
+//              reads them once per window.
+//   collapses  batches of <= 32 flagged measurements (k_batch.cu), enqueued two ahead with no
+//              host round trip inside a batch. The reference's pivot is the smallest stabilizer
+//              with X at q. Each shard ORs its stabilizers' batch-start bits into a 32-bit mask
+//              (all-gather, 4 B per shard); every shard then computes the same plan on the
+//              device (k_shard_plan): the leader L = the first shard with bit 0 set holds the
+//              global pivot of collapse 0, and a shard d < L has no stabilizer with X at q_m for
+//              m < ctz(mask_d), so its rows can neither be pivots nor change before that: L alone
+//              computes pivots, pivot rows and coins for m < lim = min(b, min_{d<L} ctz(mask_d)),
+//              stopping earlier if it has no candidate. The batch block (V rows + vinfo) then
+//              moves by a root-free max-all-reduce: every other shard's block is zero, so no
+//              host needs to know L. Every shard absorbs it into its own rows in one pass.
 //              No shard with bit 0 => the measurement is deterministic now (measure.hpp:417-421).
-//   deterministic  each shard folds its ordered partial product (k_det_partial), the partials
-//              are all-gathered, and every shard folds them in shard order (associativity of
-//              the ordered product), so every shard knows the outcome.
+//              The host reads each batch's plan one batch behind (pinned copy + event): a batch
+//              that ended early makes the speculative one behind it a no-op (device position),
+//              and the loop re-plans from there.
+//   deterministic  each shard folds its ordered partial product (k_det_partial), the partials of
+//              up to 16 measurements are all-gathered together, and every shard folds them in
+//              shard order (associativity of the ordered product).
 //   record     the leader writes collapse entries; a max-all-reduce of the window's record
 //              (zero-initialised everywhere) gives every shard the whole record.
-// Coins: the coin index advances only on collapses, in window order, so the host tracks it
-// and hands it to each batch's leader.
+// Coins: the coin index advances only on collapses, in window order, on every shard alike
+// (k_batch_member), so each batch's leader draws from the same position.
 #include <algorithm>
 #include <chrono>
 #include <cstring>
@@ -54,9 +60,12 @@ struct Shard {
     uint64_t j0 = 0;
     qsr_record_entry *d_rec = nullptr;   // whole record (every shard)
     uint32_t *d_masks = nullptr;         // [world] gathered stabilizer OR-masks
-    uint64_t *det_send = nullptr;        // [det_slot_words]
-    uint64_t *det_recv = nullptr;        // [world][det_slot_words]
+    uint32_t *d_plan = nullptr;          // [4] batch plan (k_shard_plan)
+    uint64_t *det_send = nullptr;        // [kDetChunk][det_slot_words]
+    uint64_t *det_recv = nullptr;        // [world][kDetChunk][det_slot_words]
 };
+
+constexpr uint32_t kDetChunk = 16; // deterministic outcomes whose partials share one all-gather
 
 } // namespace
 
@@ -69,42 +78,83 @@ struct qsr_sharded {
     std::unique_ptr<DeviceSchedule> ds;    // one copy per process (all local shards share a device)
     RunTimes last;
     uint64_t launches = 0;
+    uint32_t *h_ctl = nullptr;             // pinned [2][8]: shard 0's plan + block control per slot
+    cudaEvent_t bev[2] = {nullptr, nullptr};
     ~qsr_sharded() {
         cudaSetDevice(device);
         for (auto &s : sh) {
             if (s.t) s.t->sync();
-            for (void *p : {(void *)s.d_rec, (void *)s.d_masks, (void *)s.det_send, (void *)s.det_recv})
+            for (void *p : {(void *)s.d_rec, (void *)s.d_masks, (void *)s.d_plan, (void *)s.det_send,
+                            (void *)s.det_recv})
                 if (p) cudaFree(p);
         }
+        if (h_ctl) cudaFreeHost(h_ctl);
+        for (auto e : bev)
+            if (e) cudaEventDestroy(e);
     }
 
-    int leader_local(int rank) const {
-        for (size_t i = 0; i < sh.size(); ++i)
-            if (ex->ranks[i] == rank) return int(i);
-        return -1;
-    }
-
-    // Deterministic outcome of q into entry `idx` of every shard's window record.
-    void deterministic(uint32_t q, uint64_t idx) {
-        std::vector<const void *> send;
-        std::vector<void *> recv;
-        for (auto &s : sh) {
-            det_local_partial(*s.t, q, s.det_send);
-            send.push_back(s.det_send);
-            recv.push_back(s.det_recv);
-        }
+    // Deterministic outcomes of qubits qs[i] into entries idx[i] of every shard's window record
+    // (measure.hpp:343-376): each shard folds its ordered partial product per measurement, one
+    // all-gather moves up to kDetChunk of them, and every shard folds the world's partials in
+    // shard order (the ordered product is associative).
+    void deterministic(const uint32_t *qs, const uint32_t *idx, size_t cnt) {
         const uint64_t sw = det_slot_words(*sh[0].t);
-        ex->allgather(send, recv, sw * 8);
-        for (auto &s : sh) det_combine(*s.t, q, s.det_recv, uint32_t(world), s.t->ms.out + idx);
+        for (size_t c0 = 0; c0 < cnt; c0 += kDetChunk) {
+            const uint32_t c = uint32_t(std::min<size_t>(kDetChunk, cnt - c0));
+            std::vector<const void *> send;
+            std::vector<void *> recv;
+            for (auto &s : sh) {
+                for (uint32_t i = 0; i < c; ++i) det_local_partial(*s.t, qs[c0 + i], s.det_send + i * sw);
+                send.push_back(s.det_send);
+                recv.push_back(s.det_recv);
+            }
+            ex->allgather(send, recv, c * sw * 8);
+            for (auto &s : sh)
+                for (uint32_t i = 0; i < c; ++i)
+                    det_combine(*s.t, qs[c0 + i], s.det_recv + i * sw, uint32_t(world), s.t->ms.out + idx[c0 + i],
+                                c * sw);
+        }
     }
 
-    void measure_window(const std::vector<uint32_t> &mq, uint64_t seed, uint64_t &coin,
-                        RunTimes &rt) {
+    // One batch of <= kMaxBatch flagged measurements starting at `start` (speculatively: it is a
+    // no-op unless every shard's device position equals `start` when it runs), with no host
+    // round trip: column bits and stabilizer masks -> all-gather -> the plan on every shard ->
+    // the leader's pivots -> a root-free max-all-reduce of the batch block (the others' blocks
+    // are zero) -> every shard absorbs. Shard 0's plan and block control are copied to pinned
+    // slot `slot` for the host, which reads them one batch behind.
+    void enqueue_batch(size_t start, uint32_t b, uint64_t seed, int slot) {
+        std::vector<const void *> msend;
+        std::vector<void *> mrecv, blocks;
+        for (auto &s : sh) {
+            batch_colbits(*s.t, s.t->ms.fq + start, b, /*zero_block=*/true);
+            msend.push_back(s.t->ms.bctl + 2);
+            mrecv.push_back(s.d_masks);
+            blocks.push_back(s.t->ms.batch_block);
+        }
+        ex->allgather(msend, mrecv, 4);
+        for (size_t i = 0; i < sh.size(); ++i) {
+            DeviceTableau &t = *sh[i].t;
+            shard_plan(t, sh[i].d_masks, world, ex->ranks[i], b, uint32_t(start), sh[i].d_plan);
+            batch_pivots(t, t.ms.fq + start, t.ms.fidx + start, b, seed, nullptr, 0, sh[i].d_plan);
+        }
+        ex->allreduce_max_u64(blocks, sh[0].t->ms.batch_block_bytes / 8);
+        for (auto &s : sh) batch_apply(*s.t);
+        DeviceTableau &t0 = *sh[0].t;
+        QSR_CUDA(cudaMemcpyAsync(h_ctl + 8 * slot, sh[0].d_plan, 16, cudaMemcpyDeviceToHost, t0.stream));
+        QSR_CUDA(cudaMemcpyAsync(h_ctl + 8 * slot + 4, t0.ms.bctl, 16, cudaMemcpyDeviceToHost, t0.stream));
+        QSR_CUDA(cudaEventRecord(bev[slot], t0.stream));
+    }
+
+    void set_position(uint32_t pos) {
+        for (auto &s : sh) set_device_u32(s.t->ms.d_pos, pos, s.t->stream);
+    }
+
+    void measure_window(const std::vector<uint32_t> &mq, uint64_t seed, RunTimes &rt) {
         const uint64_t m = mq.size();
         DeviceTableau &t0 = *sh[0].t;
         cudaEvent_t ev[4];
         for (auto &e : ev) QSR_CUDA(cudaEventCreate(&e));
-        std::vector<void *> flag_bufs, out_bufs, blocks;
+        std::vector<void *> flag_bufs, out_bufs;
         for (auto &s : sh) {
             DeviceTableau &t = *s.t;
             t.ensure_window_cap(m);
@@ -113,7 +163,6 @@ struct qsr_sharded {
             flags_cm(t, m);
             flag_bufs.push_back(t.ms.flags);
             out_bufs.push_back(t.ms.out);
-            blocks.push_back(t.ms.batch_block);
         }
         ex->allreduce_max_u8(flag_bufs, m);
         std::vector<uint8_t> flags(m);
@@ -121,7 +170,7 @@ struct qsr_sharded {
         QSR_CUDA(cudaEventRecord(ev[0], t0.stream));
         for (auto &s : sh) transpose_to_rm(*s.t);
         QSR_CUDA(cudaEventRecord(ev[1], t0.stream));
-        QSR_CUDA(cudaStreamSynchronize(t0.stream));
+        QSR_CUDA(cudaStreamSynchronize(t0.stream)); // flags (once per window)
 
         std::vector<uint32_t> fq, fidx;
         for (uint64_t i = 0; i < m; ++i)
@@ -133,48 +182,58 @@ struct qsr_sharded {
                 QSR_CUDA(cudaMemcpyAsync(t.ms.fidx, fidx.data(), fidx.size() * 4, cudaMemcpyHostToDevice,
                                          t.stream));
             }
-        std::vector<uint32_t> masks(world);
-        size_t pos = 0;
-        while (pos < fq.size()) {
-            const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - pos));
-            std::vector<const void *> msend;
-            std::vector<void *> mrecv;
-            for (auto &s : sh) {
-                batch_colbits(*s.t, s.t->ms.fq + pos, b);
-                msend.push_back(s.t->ms.bctl + 2);
-                mrecv.push_back(s.d_masks);
+        // Collapses in window order (measure.hpp:409-431), two batches in flight: batch k + 1 is
+        // enqueued (assuming batch k collapses all its measurements) before the host looks at
+        // batch k, so the devices never wait for the host.
+        struct Pending { size_t start; uint32_t b; int slot; };
+        Pending queue[2];
+        int qhead = 0, qsize = 0, slot = 0;
+        size_t pos = 0, spec = 0;
+        set_position(0);
+        auto drain = [&] {
+            while (qsize) {
+                QSR_CUDA(cudaEventSynchronize(bev[queue[qhead].slot]));
+                qhead = (qhead + 1) % 2;
+                --qsize;
             }
-            ex->allgather(msend, mrecv, 4);
-            QSR_CUDA(cudaMemcpyAsync(masks.data(), sh[0].d_masks, 4 * world, cudaMemcpyDeviceToHost,
-                                     t0.stream));
-            QSR_CUDA(cudaStreamSynchronize(t0.stream));
-            int L = -1;
-            for (int r = 0; r < world && L < 0; ++r)
-                if (masks[r] & 1u) L = r;
-            if (L < 0) { // no stabilizer anywhere anticommutes with Z_q now: deterministic
-                deterministic(fq[pos], fidx[pos]);
-                ++pos;
+        };
+        while (pos < fq.size()) {
+            while (qsize < 2 && spec < fq.size()) {
+                const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
+                enqueue_batch(spec, b, seed, slot);
+                queue[(qhead + qsize) % 2] = Pending{spec, b, slot};
+                ++qsize;
+                slot ^= 1;
+                spec += b;
+            }
+            const Pending p = queue[qhead];
+            qhead = (qhead + 1) % 2;
+            --qsize;
+            QSR_CUDA(cudaEventSynchronize(bev[p.slot]));
+            const uint32_t *plan = h_ctl + 8 * p.slot, *bctl = plan + 4;
+            if (plan[3]) continue; // skipped: behind a batch that ended early
+            if (plan[2]) {         // no stabilizer anywhere anticommutes with Z_q: deterministic now
+                drain();           // (measure.hpp:417-421)
+                deterministic(&fq[p.start], &fidx[p.start], 1);
+                pos = p.start + 1;
+                set_position(uint32_t(pos));
+                spec = pos;
                 continue;
             }
-            uint32_t lim = b;
-            for (int r = 0; r < L; ++r) lim = std::min<uint32_t>(lim, uint32_t(__builtin_ctz(masks[r])));
-            const int li = leader_local(L);
-            if (li >= 0) {
-                DeviceTableau &t = *sh[li].t;
-                QSR_CUDA(cudaMemcpyAsync(t.ms.coin_index, &coin, 8, cudaMemcpyHostToDevice, t.stream));
-                batch_pivots(t, t.ms.fq + pos, t.ms.fidx + pos, lim, seed);
-            }
-            ex->broadcast(blocks, t0.ms.batch_block_bytes, L);
-            for (auto &s : sh) batch_apply(*s.t);
-            uint32_t len = 0;
-            QSR_CUDA(cudaMemcpyAsync(&len, t0.ms.bctl, 4, cudaMemcpyDeviceToHost, t0.stream));
-            QSR_CUDA(cudaStreamSynchronize(t0.stream));
+            const uint32_t len = bctl[0];
             if (len == 0) fail(QSR_INTERNAL, "sharded measure: leader found no pivot");
-            coin += len;
-            pos += len;
+            pos = p.start + len;
+            if (len < p.b) { // ended early (another shard holds a later pivot): re-plan from pos
+                drain();
+                spec = pos;
+            }
         }
+        drain();
+        // Deterministic outcomes of the unflagged measurements (measure.hpp:432-438), batched.
+        std::vector<uint32_t> dq, didx;
         for (uint64_t i = 0; i < m; ++i)
-            if (!flags[i]) deterministic(mq[i], i);
+            if (!flags[i]) { dq.push_back(mq[i]); didx.push_back(uint32_t(i)); }
+        if (!dq.empty()) deterministic(dq.data(), didx.data(), dq.size());
         ex->allreduce_max_u8(out_bufs, m * sizeof(qsr_record_entry));
         QSR_CUDA(cudaEventRecord(ev[2], t0.stream));
         for (auto &s : sh) transpose_to_cm(*s.t);
@@ -199,8 +258,9 @@ struct qsr_sharded {
             s.t->sync();
             launch_zero_state(*s.t, nullptr);
         }
+        for (auto &s : sh) QSR_CUDA(cudaMemsetAsync(s.t->ms.coin_index, 0, 8, s.t->stream));
         QSR_CUDA(cudaEventRecord(e_start, t0.stream));
-        uint64_t coin = 0, rec_off = 0;
+        uint64_t rec_off = 0;
         const uint64_t W = ds->is_meas.size();
         uint64_t w = 0;
         while (w < W) {
@@ -224,7 +284,7 @@ struct qsr_sharded {
             if (const uint32_t *perm = ds->perm_before(w))
                 for (auto &s : sh) launch_unpermute_rows(*s.t, perm);
             const auto &mq = ds->mqubits[w];
-            measure_window(mq, seed, coin, rt);
+            measure_window(mq, seed, rt);
             for (auto &s : sh)
                 QSR_CUDA(cudaMemcpyAsync(s.d_rec + rec_off, s.t->ms.out, mq.size() * sizeof(qsr_record_entry),
                                          cudaMemcpyDeviceToDevice, s.t->stream));
@@ -312,10 +372,13 @@ qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
             const uint64_t sw = det_slot_words(*sd.t);
             QSR_CUDA(cudaMalloc(&sd.d_rec, nm * sizeof(qsr_record_entry)));
             QSR_CUDA(cudaMalloc(&sd.d_masks, 4 * size_t(cfg->world)));
-            QSR_CUDA(cudaMalloc(&sd.det_send, sw * 8));
-            QSR_CUDA(cudaMemset(sd.det_send, 0, sw * 8));
-            QSR_CUDA(cudaMalloc(&sd.det_recv, sw * 8 * size_t(cfg->world)));
+            QSR_CUDA(cudaMalloc(&sd.d_plan, 16));
+            QSR_CUDA(cudaMalloc(&sd.det_send, kDetChunk * sw * 8));
+            QSR_CUDA(cudaMemset(sd.det_send, 0, kDetChunk * sw * 8));
+            QSR_CUDA(cudaMalloc(&sd.det_recv, kDetChunk * sw * 8 * size_t(cfg->world)));
         }
+        QSR_CUDA(cudaMallocHost(&e->h_ctl, 2 * 8 * sizeof(uint32_t)));
+        for (auto &ev : e->bev) QSR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         if (cfg->exchange == QSR_EXCHANGE_LOCAL)
             e->ex = make_local_exchange(cfg->world, streams);
         else

@@ -21,3 +21,42 @@ def test_cpp_dropin_matches_reference():
     out = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stdout[-4000:] + out.stderr[-2000:]
     assert "dropin ok" in out.stdout
+
+
+# The reference's own unit suites (proj/tests/test_*.cpp: 9 suites, 91 cases) compiled from
+# where they lie with tests/cpp/refsuite/route_gpu.hpp force-included, so their calls to
+# apply_window, measure_window, find_probabilistic, find_and_compact_pivots, parallel_ge,
+# swap_anti_commuting, inject_x, deterministic_outcome, run_single_shot, init_frames,
+# apply_window_frames, measure_sample and sample run on the device through the C++ shim
+# ("the reference tests be rebuilt against it").
+SUITE_GPU = BIN.parent / "refsuite_gpu"
+SUITE_CPU = BIN.parent / "refsuite_cpu"
+
+
+def _summary(stdout):
+    line = [l for l in stdout.splitlines() if l.startswith("cases:")][-1]
+    f = line.split()
+    return {f[i].rstrip(":"): float(f[i + 1]) for i in range(0, len(f) - 1, 2)}
+
+
+def test_reference_suites_on_the_catch2_standin():
+    """The stand-in runner itself: the suites on the reference alone (91 cases, 115,542
+    assertions)."""
+    if not SUITE_CPU.exists():
+        pytest.skip("reference suites not built (reference tree absent)")
+    out = subprocess.run([str(SUITE_CPU)], capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-4000:]
+    s = _summary(out.stdout)
+    assert s["cases"] == 91 and s["failed"] == 0 and s["assertions"] >= 115000
+
+
+@pytest.mark.gpu
+def test_reference_suites_through_the_gpu_shim():
+    if not SUITE_GPU.exists():
+        pytest.skip("reference suites not built (reference tree absent)")
+    out = subprocess.run([str(SUITE_GPU)], capture_output=True, text=True, timeout=1200)
+    print(out.stdout[-3000:])
+    assert out.returncode == 0, out.stdout[-6000:] + out.stderr[-2000:]
+    s = _summary(out.stdout)
+    assert s["cases"] == 91 and s["failed"] == 0
+    assert s["libqsr_kernel_launches"] > 1000  # the routed calls ran on the device
