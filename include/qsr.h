@@ -248,8 +248,9 @@ typedef struct qsr_frames qsr_frames;
 qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int world, int rank,
                              qsr_frames **out, double *device_ms);
 /* Algorithmic bytes of the last qsr_engine_sample's frames-window launches (frames rule words,
- * no signs: X / Y / Z move nothing, frames.hpp:76-94) = 8 B x shot-words x words. */
-qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes);
+ * no signs: X / Y / Z move nothing, frames.hpp:76-94) = 8 B x shot-words x words, and their
+ * summed device time (ms; the frames run on their own stream, beside the reference shot). */
+qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes, double *ms);
 void qsr_engine_destroy(qsr_engine *e);
 
 /* ---- Pauli frames (frames.hpp:32-204) ------------------------------------------ */

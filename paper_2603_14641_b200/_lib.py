@@ -159,7 +159,7 @@ SIGNATURES = {
     "qsr_engine_tableau": (i32, [P, pu64, pu64, pu64]),
     "qsr_engine_profile": (i32, [P, u64, C.POINTER(KernelProfile_t)]),
     "qsr_engine_sample": (i32, [P, u64, u64, i32, i32, C.POINTER(P), pd]),
-    "qsr_engine_frames_bytes": (i32, [P, pd]),
+    "qsr_engine_frames_bytes": (i32, [P, pd, pd]),
     "qsr_engine_destroy": (None, [P]),
     "qsr_init_frames": (i32, [u64, u64, u64, i32, C.POINTER(P)]),
     "qsr_frames_info": (i32, [P, pu64, pu64, pu64]),

@@ -858,6 +858,7 @@ struct qsr_engine {
     std::unique_ptr<DeviceSchedule> ds;
     qsr_record_entry *d_rec = nullptr;
     RunTimes last;
+    double frames_ms = 0; // frames-window device time of the last qsr_engine_sample
     uint64_t launches = 0;
     ~qsr_engine() {
         if (d_rec) cudaFree(d_rec);
@@ -1427,16 +1428,23 @@ qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int w
         for (const auto &mq : e->ds->mqubits)
             for (uint32_t q : mq)
                 if (!seen[q]) { seen[q] = 1; ++distinct; }
-        cudaEvent_t a, b;
+        cudaEvent_t a, b, fdone;
         QSR_CUDA(cudaEventCreate(&a));
         QSR_CUDA(cudaEventCreate(&b));
+        QSR_CUDA(cudaEventCreateWithFlags(&fdone, cudaEventDisableTiming));
         QSR_CUDA(cudaEventRecord(a, t.stream));
         const uint64_t l0 = g_launches;
-        auto f = make_frames(t.n, shots, seed, t.device, w0, nw, 64, t.stream);
+        // The frames never read the tableau: on their own stream their windows overlap the
+        // reference shot's (small, L2-resident tableau windows and the collapse chain).
+        auto f = make_frames(t.n, shots, seed, t.device, w0, nw, 64);
+        QSR_CUDA(cudaStreamWaitEvent(f->stream, a, 0));
         if (distinct) f->ensure_rows(distinct);
         FramesRider rider(*f, seed);
+        rider.own = f->stream;
         e->last = RunTimes{};
         run_device(t, *e->ds, seed, e->d_rec, e->last, &rider);
+        QSR_CUDA(cudaEventRecord(fdone, f->stream));
+        QSR_CUDA(cudaStreamWaitEvent(t.stream, fdone, 0));
         const uint64_t nm = e->ds->measure_count;
         std::vector<qsr_record_entry> ref(nm);
         if (nm)
@@ -1444,6 +1452,15 @@ qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int w
                                      t.stream));
         t.sync();
         fold_reference(*f, ref, t.n, t.stream);
+        e->frames_ms = 0;
+        for (auto &r : rider.runs) {
+            float fm = 0;
+            QSR_CUDA(cudaEventElapsedTime(&fm, r.first, r.second));
+            e->frames_ms += fm;
+            cudaEventDestroy(r.first);
+            cudaEventDestroy(r.second);
+        }
+        cudaEventDestroy(fdone);
         QSR_CUDA(cudaEventRecord(b, t.stream));
         QSR_CUDA(cudaEventSynchronize(b));
         float ms = 0;
@@ -1457,11 +1474,12 @@ qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int w
     });
 }
 
-qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes) {
+qsr_status qsr_engine_frames_bytes(const qsr_engine *e, double *bytes, double *ms) {
     return guard([&] {
         REQUIRE_PTR(e);
         REQUIRE_PTR(bytes);
         *bytes = e->last.frames_bytes;
+        if (ms) *ms = e->frames_ms;
     });
 }
 

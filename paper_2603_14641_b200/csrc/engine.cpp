@@ -284,17 +284,28 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             if (!frames) {
                 rt.gate_launches += run_unitary_windows(t, ds, w, w1, &rt.gate_bytes);
             } else {
+                const cudaStream_t fs = frames->own ? frames->own : t.stream;
+                cudaEvent_t fa = nullptr, fb = nullptr;
+                if (frames->own) {
+                    QSR_CUDA(cudaEventCreate(&fa));
+                    QSR_CUDA(cudaEventCreate(&fb));
+                    QSR_CUDA(cudaEventRecord(fa, fs));
+                }
                 for (uint64_t v = w; v < w1; ++v) {
                     const uint64_t *g = ds.d_gates + ds.offsets[v];
                     const uint64_t cnt = ds.offsets[v + 1] - ds.offsets[v];
                     launch_gate_window(t, g, cnt);
-                    frames->unitary(g, cnt, t.stream);
+                    frames->unitary(g, cnt, fs);
                     if (v < ds.wwords.size()) {
                         rt.gate_bytes += (8.0 * ds.wwords[v] + 16.0) * 2.0 * double(t.kg);
                         rt.frames_bytes += 8.0 * ds.fwords[v] * double(frames->row_words);
                     }
                 }
                 rt.gate_launches += 2 * (w1 - w);
+                if (frames->own) {
+                    QSR_CUDA(cudaEventRecord(fb, fs));
+                    frames->runs.emplace_back(fa, fb);
+                }
             }
             w = w1;
             QSR_CUDA(cudaEventRecord(b, t.stream));
@@ -306,14 +317,14 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
         }
         if (const uint32_t *perm = ds.perm_before(w)) {
             launch_unpermute_rows(t, perm);
-            if (frames) frames->unpermute(perm, t.stream);
+            if (frames) frames->unpermute(perm, frames->own ? frames->own : t.stream);
         }
         const auto &mq = ds.mqubits[w];
         const uint64_t m = mq.size();
         t.ensure_window_cap(m);
         QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), m * 4, cudaMemcpyHostToDevice, t.stream));
         measure_window_device(t, m, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
-        if (frames) frames->measure(mq.data(), m, t.stream);
+        if (frames) frames->measure(mq.data(), m, frames->own ? frames->own : t.stream);
         QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, m * sizeof(qsr_record_entry),
                                  cudaMemcpyDeviceToDevice, t.stream));
         rec_off += m;
@@ -321,7 +332,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
     }
     if (const uint32_t *perm = ds.perm_before(W)) {
         launch_unpermute_rows(t, perm);
-        if (frames) frames->unpermute(perm, t.stream);
+        if (frames) frames->unpermute(perm, frames->own ? frames->own : t.stream);
     }
     QSR_CUDA(cudaEventRecord(e_end, t.stream));
     QSR_CUDA(cudaEventSynchronize(e_end));

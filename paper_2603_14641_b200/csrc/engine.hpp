@@ -75,6 +75,11 @@ uint64_t run_unitary_windows(DeviceTableau &t, const DeviceSchedule &ds, uint64_
 // measurement windows and row un-permutes, on the tableau's stream (capi.cpp).
 struct FramesSink {
     uint64_t row_words = 0; // shot-words per frames row (bytes accounting)
+    // Resident engines only: the frames' own stream. Frames never read the tableau, so their
+    // windows run concurrently with the reference shot's (the caller joins the streams); each
+    // unitary run is bracketed by an event pair on it (frames-window device time).
+    cudaStream_t own = nullptr;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> runs;
     virtual ~FramesSink() = default;
     virtual void unitary(const uint64_t *d_gates, uint64_t cnt, cudaStream_t st) = 0;
     virtual void unpermute(const uint32_t *d_perm, cudaStream_t st) = 0;
@@ -82,8 +87,8 @@ struct FramesSink {
 };
 
 // The single-shot driver on device-resident inputs; `d_record` has measure_count entries. With
-// `frames`, the Pauli frames ride every window on t.stream (sample() on a resident schedule; the
-// unitary runs are then launched window by window, not replayed as graphs).
+// `frames`, the Pauli frames ride every window, on t.stream or on frames->own (sample() on a
+// resident schedule; the unitary runs are then launched window by window, not as graphs).
 void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
                 qsr_record_entry *d_record, RunTimes &rt, FramesSink *frames = nullptr);
 void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &ds,

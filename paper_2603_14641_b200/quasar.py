@@ -697,10 +697,11 @@ class Engine:
         f = FrameTableau(h)
         return (f.record() if record else None), ms.value
 
-    def frames_bytes(self) -> float:
-        b = C.c_double()
-        check(lib.qsr_engine_frames_bytes(self._h, C.byref(b)))
-        return b.value
+    def frames_stats(self) -> Tuple[float, float]:
+        """(algorithmic bytes, device ms) of the last sample()'s frames windows."""
+        b, ms = C.c_double(), C.c_double()
+        check(lib.qsr_engine_frames_bytes(self._h, C.byref(b), C.byref(ms)))
+        return b.value, ms.value
 
     def profile(self, seed: int) -> dict:
         """One extra run with CUDA events around every k_batch_absorb launch (not a timed run)."""
