@@ -571,16 +571,61 @@ void flags_cm(DeviceTableau &t, uint64_t m) {
 // ---- API-parity operations on a (transposed) RM tableau ------------------------------
 void rm_column_mask(DeviceTableau &t, uint64_t q) { column_mask(t, q); }
 
+namespace {
+// find_and_compact_pivots' scatter + stable compaction (measure.hpp:130-150,
+// bitplane.hpp:126-136) on the device: the stabilizer half of q's column mask (bit g = X bit of
+// stabilizer g at q) becomes the ascending pivot list with a -1 tail. One CTA: contiguous word
+// chunks per thread, a popcount block scan for the output offsets, then every thread writes its
+// pivots in order and the tail.
+__global__ void __launch_bounds__(1024)
+k_pivot_list(const uint64_t *__restrict__ mask, uint64_t words, uint64_t n, int64_t *__restrict__ entries,
+             uint64_t *__restrict__ count) {
+    __shared__ uint32_t s_warp[32];
+    __shared__ uint32_t s_total;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, T = blockDim.x;
+    const uint64_t per = (words + T - 1) / T, w0 = min(words, uint64_t(tid) * per), w1 = min(words, w0 + per);
+    uint32_t cnt = 0;
+    for (uint64_t w = w0; w < w1; ++w) cnt += uint32_t(__popcll(mask[w]));
+    uint32_t incl = cnt; // inclusive scan: warp, then warp totals
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= uint32_t(o)) incl += v;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t v = lane < (T + 31) / 32 ? s_warp[lane] : 0u, x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t u = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= uint32_t(o)) x += u;
+        }
+        s_warp[lane] = x - v; // exclusive warp offsets
+        if (lane == 31) s_total = x;
+    }
+    __syncthreads();
+    uint64_t pos = s_warp[warp] + incl - cnt;
+    for (uint64_t w = w0; w < w1; ++w)
+        for (uint64_t m = mask[w]; m; m &= m - 1) entries[pos++] = int64_t(w * 64 + uint64_t(__ffsll(m) - 1));
+    const uint32_t total = s_total;
+    for (uint64_t i = uint64_t(total) + tid; i < n; i += T) entries[i] = -1;
+    if (tid == 0) *count = total;
+}
+} // namespace
+
 void rm_find_pivots(DeviceTableau &t, uint64_t q, std::vector<int64_t> &entries, uint64_t &count) {
     column_mask(t, q);
-    std::vector<uint64_t> mask(t.kg);
-    QSR_CUDA(cudaMemcpyAsync(mask.data(), t.ms.mask + t.kg, t.kg * 8, cudaMemcpyDeviceToHost,
-                             t.stream));
+    int64_t *d_entries = nullptr;
+    uint64_t *d_count = nullptr;
+    QSR_CUDA(cudaMallocAsync(&d_entries, t.n * 8 + 8, t.stream));
+    d_count = reinterpret_cast<uint64_t *>(d_entries + t.n);
+    k_pivot_list<<<1, 1024, 0, t.stream>>>(t.ms.mask + t.kg, t.kg, t.n, d_entries, d_count);
+    QSR_CUDA(cudaGetLastError());
+    count_launch();
+    entries.resize(t.n);
+    QSR_CUDA(cudaMemcpyAsync(entries.data(), d_entries, t.n * 8, cudaMemcpyDeviceToHost, t.stream));
+    QSR_CUDA(cudaMemcpyAsync(&count, d_count, 8, cudaMemcpyDeviceToHost, t.stream));
+    QSR_CUDA(cudaFreeAsync(d_entries, t.stream));
     QSR_CUDA(cudaStreamSynchronize(t.stream));
-    entries.assign(t.n, -1);
-    count = 0;
-    for (uint64_t g = 0; g < t.n; ++g)
-        if ((mask[g / 64] >> (g % 64)) & 1) entries[count++] = int64_t(g);
 }
 
 void rm_find_probabilistic(DeviceTableau &t, const std::vector<uint32_t> &qubits,

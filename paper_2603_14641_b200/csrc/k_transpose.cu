@@ -40,7 +40,7 @@ namespace {
 // in the buffer the block was just read from, so a CTA needs ST x (block bytes) of shared memory.
 template <int RT, int W, int ST>
 struct Shape {
-    static_assert(W % 16 == 0, "block shape");
+    static_assert(W % 16 == 0 && ST >= 2, "block shape");
     static constexpr int kThreads = RT * W * 2;
     static constexpr uint32_t kInWords = RT * 64 * W;
     static constexpr uint32_t kBoxRows = RT * 64 > 256 ? 256 : RT * 64; // TMA box rows
