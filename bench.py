@@ -633,8 +633,9 @@ def bench_sampling(args, cfg):
         "wall_s_per_step": ms_per_step / 1e3,
         "roofline": roof,
         "kernels": {"frames_window": roof, "tableau_window": tab},
-        "e2e": {"value": G * e2e_steps / e2e_total, "unit": "gates/s", "h2d_bytes_per_step": world * 12 * G,
-                "d2h_bytes_per_step": world * rec_bytes, "s_per_step": e2e_total / max(e2e_steps, 1)},
+        "e2e": {"value": G * e2e_steps / e2e_total if e2e_steps else None, "unit": "gates/s",
+                "h2d_bytes_per_step": world * 12 * G, "d2h_bytes_per_step": world * rec_bytes,
+                "s_per_step": e2e_total / max(e2e_steps, 1)},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "cpu_baseline": cpu,

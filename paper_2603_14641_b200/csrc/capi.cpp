@@ -176,7 +176,6 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
         {reinterpret_cast<void **>(&ms.err), 4},
         {reinterpret_cast<void **>(&ms.colbits), 2 * ng * 4},
         {reinterpret_cast<void **>(&ms.batch_block), ms.batch_block_bytes},
-        {reinterpret_cast<void **>(&ms.gconst), kMaxBatch * kPmatChunks * 4},
         {reinterpret_cast<void **>(&ms.nz), (ng / 32 + 1) * 4},
         {reinterpret_cast<void **>(&ms.pcount), 2 * kMaxBatch * sizeof(int)},
         {reinterpret_cast<void **>(&ms.d_pos), 4},

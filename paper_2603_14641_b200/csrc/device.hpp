@@ -36,8 +36,7 @@ inline void count_launch(uint64_t n = 1) { g_launches += n; }
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
-constexpr int kPmatChunks = 8; // word chunks of the pair-parity rows (k_batch_member)
-constexpr int kVinfoWords = 5 * kMaxBatch; // per-batch pivot info (k_batch.cu)
+constexpr int kVinfoWords = 7 * kMaxBatch; // per-batch pivot info (k_batch.cu)
 
 // Scratch used by the measurement pipeline; sized for one tableau.
 struct MeasureScratch {
@@ -69,7 +68,6 @@ struct MeasureScratch {
     cudaEvent_t bev[2] = {nullptr, nullptr};
     uint8_t *partial = nullptr;     // [slices][2ng] per-(row, slice) phase bytes (k_batch.cu)
     uint64_t partial_bytes = 0;
-    uint32_t *gconst = nullptr;     // [kMaxBatch][kPmatChunks] pair-parity matrix rows, per word chunk
     uint32_t *nz = nullptr;         // [ng/32] active-stabilizer ballot of the batch
     int *pcount = nullptr;          // [2*kMaxBatch] per-pivot phase / beta counters
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]

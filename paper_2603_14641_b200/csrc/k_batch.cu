@@ -26,8 +26,8 @@
 // per-collapse path, which checks every product exactly.)
 //
 // Traffic: one read + write of the touched rows per batch instead of per collapse; the pivot
-// rows are staged through shared memory (cp.async, double-buffered 64-word slices) and each
-// staged word is reused by the 4 rows a warp carries.
+// rows reach every CTA of the absorb pass as a shared-memory table of their XOR combinations
+// per 64-word slice, reused by every row the CTA absorbs into.
 #include <mutex>
 #include <string>
 #include <utility>
@@ -43,18 +43,17 @@ namespace {
 using u64 = unsigned long long;
 constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
 enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2, BL_SKIP = 3 };
-// vinfo layout (u32 [5*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m
-enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_MC = 4 * kB };
-static_assert(5 * kB == kVinfoWords, "vinfo layout");
+// vinfo layout (u32 [7*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m |
+// L_m = row m of (I + Mc)^-1 over GF(2) (V_m = XOR_{j in L_m} S_{c_j} at batch start) |
+// pair-parity row P_m (bit j' < m: parity(sum_i |V_mz[i] & V_j'x[i]|))
+enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_MC = 4 * kB, VI_L = 5 * kB,
+                  VI_PMAT = 6 * kB };
+static_assert(7 * kB == kVinfoWords, "vinfo layout");
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
 // Kernels of the batch chain launch with programmatic stream serialization (launch_chain): each
 // waits here for its predecessor before touching memory; the launch itself overlaps its tail.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async8(void *smem, const void *gmem) {
-    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
 
 // Membership vector of a row given its batch-start column bits `cb` (bit m = X at q_m),
 // the per-collapse VB columns and the first collapse it can take part in.
@@ -253,7 +252,16 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         const bool v = tid < len;
         vinfo[VI_VB + tid] = v ? s_vb[tid] : 0u;
         vinfo[VI_C + tid] = v ? uint32_t(g0 + s_c[tid]) : 0xFFFFFFFFu; // global generator
-        vinfo[VI_MC + tid] = v ? s_mc[tid] : 0u;
+        const uint32_t mc = v ? s_mc[tid] : 0u;
+        vinfo[VI_MC + tid] = mc;
+        // L = (I + Mc)^-1: V_m = S_{c_m} * prod_{j in Mc_m} V_j, so L_m = e_m ^ XOR_{j in Mc_m} L_j.
+        // Lane m accumulates the L_j of its members as they become final (one shuffle per j).
+        uint32_t acc = 0;
+        for (uint32_t j = 0; j < kB; ++j) {
+            const uint32_t lj = __shfl_sync(0xffffffffu, acc ^ (1u << tid), j); // L_j is final at step j
+            if ((mc >> j) & 1u) acc ^= lj;
+        }
+        vinfo[VI_L + tid] = v ? (acc ^ (1u << tid)) : 0u;
     }
     if (tid == 0) {
         bctl[BL_LEN] = len;
@@ -289,107 +297,84 @@ __global__ void k_shard_plan(const uint32_t *__restrict__ masks, int world, int 
 
 // Batch start: control words and the pivot kernels' phase sums (one launch instead of two
 // memsets, so the whole batch chain is kernel-to-kernel).
-__global__ void k_batch_reset(uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
+__global__ void k_batch_reset(uint32_t *__restrict__ bctl, int *__restrict__ pcount, uint32_t *__restrict__ vinfo) {
     pdl_wait();
     if (threadIdx.x < 4) bctl[threadIdx.x] = 0u;
     if (threadIdx.x < 2 * kB) pcount[threadIdx.x] = 0;
+    if (threadIdx.x < kB) vinfo[VI_PMAT + threadIdx.x] = 0u; // accumulated by k_pivot_rows
 }
 
-// B2. Pivot rows, word-parallel: thread = word i of every V_m (m in order, V_j of the same
-// word kept in shared memory), with the telescoped phase pieces of each V_m reduced into
-// pcount[m] (E part) and pcount[kB + m] (beta(V_m)). Then the pivot pairs are replaced
-// (D_c <- V_m, S_c <- Z_{q_m}); each word is read and rewritten by one thread only.
-constexpr int kRowThreads = 64;
+// B2. Pivot rows, parallel over (collapse, word): with L = (I + Mc)^-1 from B1, V_m = XOR over
+// j in L_m of the pivot stabilizers S_{c_j} as they stood at batch start, so every V_m word is
+// independent. A CTA owns kRowWords words of all V's: it stages the batch-start pivot rows of its
+// words in shared memory, thread (m, w) forms V_m, the telescoped phase pieces of V_m (its
+// products' cross terms are the pair-parity matrix, file header) and row m of the pair-parity
+// matrix over its words; then the pivot pairs are replaced (D_c <- V_m, S_c <- Z_{q_m}).
+constexpr int kRowWords = 8;
+constexpr int kRowThreads = kB * kRowWords;
 
 __global__ void __launch_bounds__(kRowThreads)
 k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t ng,
              uint64_t g0, const uint32_t *__restrict__ fq, uint64_t *__restrict__ Vx,
-             uint64_t *__restrict__ Vz, uint64_t vstride, const uint32_t *__restrict__ vinfo,
+             uint64_t *__restrict__ Vz, uint64_t vstride, uint32_t *__restrict__ vinfo,
              const uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
     pdl_wait();
-    __shared__ u64 sv[kB][2][kRowThreads];
-    __shared__ uint32_t s_c[kB], s_mc[kB], s_q[kB];
-    __shared__ int8_t s_e[kB][kRowThreads], s_bend[kB][kRowThreads]; // per word: |e| <= 66, bend <= 64
+    __shared__ u64 s_sx[kB][kRowWords], s_sz[kB][kRowWords], s_vx[kB][kRowWords];
+    __shared__ uint32_t s_c[kB], s_l[kB];
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
-    const uint32_t tid = threadIdx.x, lane = tid & 31;
+    const uint32_t tid = threadIdx.x, m = tid / kRowWords, w = tid % kRowWords;
     if (tid < kB) {
         s_c[tid] = tid < len ? uint32_t(vinfo[VI_C + tid] - g0) : 0u;
-        s_mc[tid] = tid < len ? vinfo[VI_MC + tid] : 0u;
-        s_q[tid] = tid < len ? fq[tid] : 0u;
+        s_l[tid] = tid < len ? vinfo[VI_L + tid] : 0u;
     }
     __syncthreads();
-    const uint64_t i = uint64_t(blockIdx.x) * kRowThreads + tid;
+    const uint64_t i = uint64_t(blockIdx.x) * kRowWords + w;
     const bool act = i < pitch;
-    // All pivot rows' batch-start words first (independent loads, all in flight at once).
-    // (cp.async: one DRAM round trip for all of them, no registers held per load.)
-    for (uint32_t m = 0; m < len; ++m) {
+    {   // stage: thread (m, w) loads S_{c_m} word i (x and z)
         const uint64_t rs = ng + s_c[m];
-        if (act) {
-            cp_async8(&sv[m][0][tid], x + rs * pitch + i);
-            cp_async8(&sv[m][1][tid], z + rs * pitch + i);
-        } else {
-            sv[m][0][tid] = 0ull;
-            sv[m][1][tid] = 0ull;
-        }
+        const bool ld = act && m < len;
+        s_sx[m][w] = ld ? __ldcg(x + rs * pitch + i) : 0ull;
+        s_sz[m][w] = ld ? __ldcg(z + rs * pitch + i) : 0ull;
     }
-    asm volatile("cp.async.commit_group;\n" ::);
-    asm volatile("cp.async.wait_group 0;\n" ::); // each thread reads back only its own words
-    for (uint32_t m = 0; m < len; ++m) {
-        u64 cx = sv[m][0][tid], cz = sv[m][1][tid];
-        int e = __popcll(cx & cz);
-        u64 acc = 0;
-        uint32_t U = s_mc[m];
-        if (U) { // the next member's words are read while this one is applied
-            uint32_t j = __ffs(U) - 1;
-            U &= U - 1;
-            u64 vx = sv[j][0][tid], vz = sv[j][1][tid];
-            for (;;) {
-                const bool more = U != 0;
-                u64 nx = 0, nzv = 0;
-                if (more) {
-                    j = __ffs(U) - 1;
-                    U &= U - 1;
-                    nx = sv[j][0][tid];
-                    nzv = sv[j][1][tid];
-                }
-                acc ^= vz & cx;
-                cx ^= vx;
-                cz ^= vz;
-                if (!more) break;
-                vx = nx;
-                vz = nzv;
-            }
-        }
-        const int bend = __popcll(cx & cz);
-        e += 2 * (__popcll(acc) & 1) - bend;
-        sv[m][0][tid] = cx;
-        sv[m][1][tid] = cz;
-        if (act) {
-            Vx[uint64_t(m) * vstride + i] = cx;
-            Vz[uint64_t(m) * vstride + i] = cz;
-        }
-        s_e[m][tid] = int8_t(e);
-        s_bend[m][tid] = int8_t(bend);
-    }
-    // Per-collapse sums over this CTA's words, off the sequential loop: thread m folds row m.
     __syncthreads();
-    for (uint32_t m = tid; m < len; m += kRowThreads) {
-        int es = 0, bs = 0;
-        for (uint32_t u = 0; u < kRowThreads; ++u) es += s_e[m][u], bs += s_bend[m][u];
-        if (es) atomicAdd(pcount + m, es);
-        if (bs) atomicAdd(pcount + kB + m, bs);
+    u64 vx = 0, vz = 0;
+    for (uint32_t L = s_l[m]; L; L &= L - 1) {
+        const uint32_t j = __ffs(L) - 1;
+        vx ^= s_sx[j][w];
+        vz ^= s_sz[j][w];
     }
-    (void)lane;
-    if (!act) return;
-    // Replace the pivot pairs: D_c <- V_m (bits), S_c <- Z_{q_m}.
-    for (uint32_t m = 0; m < len; ++m) {
-        const uint64_t c = s_c[m], q = s_q[m];
-        x[c * pitch + i] = sv[m][0][tid];
-        z[c * pitch + i] = sv[m][1][tid];
-        x[(ng + c) * pitch + i] = 0ull;
-        z[(ng + c) * pitch + i] = i == (q >> 6) ? (1ull << (q & 63)) : 0ull;
+    s_vx[m][w] = vx;
+    const u64 x0 = s_sx[m][w], z0 = s_sz[m][w];
+    // E_m pieces: beta(S_c) - beta(V_m) + 2 parity(|dz & x0|), dz = V_mz ^ S_cz (the cross terms
+    // between members, Q(Mc_m), come from the pair-parity rows in k_pivot_finish).
+    int e = __popcll(x0 & z0) - __popcll(vx & vz) + 2 * (__popcll((vz ^ z0) & x0) & 1);
+    int bend = __popcll(vx & vz);
+    __syncthreads();
+    uint32_t prow = 0; // bit j' < m: parity(|V_mz & V_j'x|) over this word
+    for (uint32_t jp = 0; jp < m; ++jp) prow |= uint32_t(__popcll(vz & s_vx[jp][w]) & 1) << jp;
+    // Reduce over the kRowWords lanes of collapse m (consecutive lanes of one warp).
+#pragma unroll
+    for (int o = kRowWords / 2; o >= 1; o >>= 1) {
+        e += __shfl_xor_sync(0xffffffffu, e, o);
+        bend += __shfl_xor_sync(0xffffffffu, bend, o);
+        prow ^= __shfl_xor_sync(0xffffffffu, prow, o);
     }
+    if (w == 0 && m < len) {
+        if (e) atomicAdd(pcount + m, e);
+        if (bend) atomicAdd(pcount + kB + m, bend);
+        if (prow) atomicXor(vinfo + VI_PMAT + m, prow);
+    }
+    if (!act || m >= len) return;
+    Vx[uint64_t(m) * vstride + i] = vx;
+    Vz[uint64_t(m) * vstride + i] = vz;
+    // Replace the pivot pairs: D_c <- V_m (bits), S_c <- Z_{q_m}; word i of row S_c was staged
+    // above, and only this CTA touches word i.
+    const uint64_t c = s_c[m], q = fq[m];
+    x[c * pitch + i] = vx;
+    z[c * pitch + i] = vz;
+    x[(ng + c) * pitch + i] = 0ull;
+    z[(ng + c) * pitch + i] = i == (q >> 6) ? (1ull << (q & 63)) : 0ull;
 }
 
 // B3. Signs of the V_m (telescoped phase, file header), coins, record entries and the signs of
@@ -403,7 +388,7 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
                uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
                int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
     pdl_wait();
-    __shared__ uint32_t s_c[kB], s_mc[kB], s_ss[kB], s_coin[kB], s_vsign[kB], s_beta[kB];
+    __shared__ uint32_t s_c[kB], s_mc[kB], s_ss[kB], s_coin[kB], s_vsign[kB], s_beta[kB], s_p[kB];
     __shared__ int s_e[kB];
     const uint32_t lane = threadIdx.x;
     const uint32_t len = bctl[BL_LEN];
@@ -416,6 +401,7 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
         s_e[lane] = pcount[lane];
         s_beta[lane] = uint32_t(pcount[kB + lane]) & 3u;
         s_ss[lane] = uint32_t((s[rs >> 6] >> (rs & 63)) & 1u); // S_c sign at batch start
+        s_p[lane] = vinfo[VI_PMAT + lane];
         s_coin[lane] = draw_coin(seed, idx0 + lane, coin_table);
     }
     __syncwarp();
@@ -426,7 +412,13 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
     if (lane < len) {
         mc = s_mc[lane];
         int E = s_e[lane];
-        for (uint32_t U = mc; U; U &= U - 1) E += int(s_beta[__ffs(U) - 1]);
+        uint32_t qf = 0; // Q(Mc_m): pairs j' < j of Mc_m with P(j', j) = 1
+        for (uint32_t U = mc; U; U &= U - 1) {
+            const uint32_t j = __ffs(U) - 1;
+            E += int(s_beta[j]);
+            qf ^= parity32(mc & s_p[j]);
+        }
+        E += 2 * int(qf);
         odd = (E & 1) != 0;
         base = s_ss[lane] ^ ((uint32_t(E) >> 1) & 1u);
     }
@@ -465,8 +457,8 @@ constexpr int kSlice = 64; // words per staged V slice (2 per lane)
 // XOR_{j'<j in M} V_j'x this is  parity(|dz & x0|) ^ Q(M),  dz = XOR_{j in M} V_jz and
 // Q(M) = XOR_{j'<j, both in M} P(j', j),  P(j', j) = parity(sum_i |V_jz[i] & V_j'x[i]|).
 // So the absorb pass only XORs row deltas; the quadratic form is a per-row 32-bit fold.
-// C1 k_batch_member: M[r] (bit m = row r absorbs V_m) for every row, written over colbits;
-//    blocks >= row_blocks compute row j of the pair-parity matrix: pmat[j] bit j' = P(j', j).
+// C1 k_batch_member: M[r] (bit m = row r absorbs V_m) for every row, written over colbits (the
+//    pair-parity matrix rows P(j', j) arrive with the batch block, from k_pivot_rows).
 // C2 k_batch_absorb: persistent, one CTA per SM walks (slice, row) items slice-major; for its
 //    64-word slice it stages, per group of 4 consecutive V's, all 16 XOR combinations
 //    T[g][S] = XOR_{j in S} V_{4g+j} (x and z; T[g][0] = 0) in shared memory, so a row
@@ -486,11 +478,10 @@ __global__ void __launch_bounds__(256)
 k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint64_t g0,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-               uint32_t *__restrict__ pmat, uint32_t row_blocks, unsigned long long *__restrict__ touched,
+               unsigned long long *__restrict__ touched,
                uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index) {
     pdl_wait();
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
-    __shared__ uint32_t s_p;
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
     // The batch's collapses are done deciding: advance the speculation position and the coin
@@ -498,26 +489,6 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
     if (blockIdx.x == 0 && tid == 0 && len) {
         if (d_pos) *d_pos += len;
         *coin_index += len;
-    }
-    if (blockIdx.x >= row_blocks) {
-        // Pair-parity row j over one word chunk (chunks x 256 threads stride the words); the
-        // chunks' partial rows are XOR-combined by k_batch_signs (no zeroing, no atomics).
-        const uint32_t e = blockIdx.x - row_blocks, j = e / kPmatChunks, ch = e % kPmatChunks;
-        if (tid == 0) s_p = 0;
-        __syncthreads();
-        uint32_t mask = 0;
-        if (j < len) {
-            for (uint64_t i = uint64_t(ch) * blockDim.x + tid; i < k; i += uint64_t(kPmatChunks) * blockDim.x) {
-                const u64 vz = Vz[uint64_t(j) * vstride + i];
-                for (uint32_t jp = 0; jp < j; ++jp)
-                    mask ^= (uint32_t(__popcll(vz & Vx[uint64_t(jp) * vstride + i])) & 1u) << jp;
-            }
-        }
-        mask = __reduce_xor_sync(0xffffffffu, mask);
-        if ((tid & 31) == 0 && mask) atomicXor(&s_p, mask);
-        __syncthreads();
-        if (tid == 0) pmat[j * kPmatChunks + ch] = s_p;
-        return;
     }
     if (tid < kB) {
         s_vb[tid] = vinfo[VI_VB + tid];
@@ -689,7 +660,7 @@ __global__ void __launch_bounds__(256)
 k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
               const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-              const uint32_t *__restrict__ pmat, int *__restrict__ err) {
+              int *__restrict__ err) {
     pdl_wait();
     __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB];
     const uint32_t len = bctl[BL_LEN];
@@ -704,12 +675,7 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
         }
         s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
     }
-    if (tid < kB) {
-        uint32_t p = 0;
-        if (tid < len)
-            for (uint32_t ch = 0; ch < kPmatChunks; ++ch) p ^= pmat[tid * kPmatChunks + ch];
-        s_p[tid] = p;
-    }
+    if (tid < kB) s_p[tid] = tid < len ? vinfo[VI_PMAT + tid] : 0u;
     __syncthreads();
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
     uint32_t f = 0;
@@ -767,7 +733,7 @@ void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b, bool zero
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     // Control words and the pivot kernels' phase sums, zeroed ahead of the chain.
-    launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount);
+    launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount, ms.vinfo);
     // The pivot rows and vinfo of the block (everything before bctl), zeroed for a sharded batch.
     const uint64_t zw = zero_block ? uint64_t(reinterpret_cast<uint64_t *>(ms.vinfo) - ms.batch_block) +
                                          (kVinfoWords * 4 + 7) / 8
@@ -797,7 +763,7 @@ void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx
     // (ms.pcount was zeroed by batch_colbits, which always precedes on this tableau.)
     launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
                  t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan);
-    launch_chain(k_pivot_rows, dim3(unsigned((t.rm_pitch + kRowThreads - 1) / kRowThreads)),
+    launch_chain(k_pivot_rows, dim3(unsigned((t.rm_pitch + kRowWords - 1) / kRowWords)),
                  dim3(kRowThreads), 0, t.stream, t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz,
                  ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
     launch_chain(k_pivot_finish, dim3(1), dim3(32), 0, t.stream, t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo,
@@ -839,9 +805,9 @@ void batch_apply(DeviceTableau &t) {
         ms.partial = static_cast<uint8_t *>(cache_acquire(t.device, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
-    launch_chain(k_batch_member, dim3(row_blocks + kB * kPmatChunks), dim3(256), 0, t.stream, ms.colbits,
-                 nrows, t.ng, t.g0, ms.Vx, ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl, ms.gconst, row_blocks,
-                 t.prof ? t.prof->d_rows : nullptr, ms.d_pos, ms.coin_index);
+    launch_chain(k_batch_member, dim3(row_blocks), dim3(256), 0, t.stream, ms.colbits, nrows, t.ng, t.g0, ms.Vx,
+                 ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl, t.prof ? t.prof->d_rows : nullptr, ms.d_pos,
+                 ms.coin_index);
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (t.prof) {
         QSR_CUDA(cudaEventCreate(&ea));
@@ -856,7 +822,7 @@ void batch_apply(DeviceTableau &t) {
         t.prof->ev.emplace_back(ea, eb);
     }
     launch_chain(k_batch_signs, dim3(row_blocks), dim3(256), 0, t.stream, t.s, nrows, nslices, ms.colbits,
-                 ms.partial, ms.vinfo, ms.bctl, ms.gconst, ms.err);
+                 ms.partial, ms.vinfo, ms.bctl, ms.err);
     count_launch(3);
 }
 
