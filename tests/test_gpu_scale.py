@@ -10,8 +10,9 @@ default in the `-m gpu` suite against the reference compiled unmodified (oracle/
   strided absorb order at 1,564 row blocks, against the reference measure_window
   (measure.hpp:381-442) run on the downloaded snapshot;
 * c5 width, snapshot parity: a 180,000-qubit tableau scrambled by 150 layers of the c5
-  circuit; layer 151 (a >= 16k-gate window, so k_gate_window<1,1,4>) on both sides, then the
-  first measurements of c5's final Bernoulli(0.01) window on both sides.
+  circuit; layer 151 (a >= 16k-gate window, so k_gate_window<1,1,4>) on both sides, the fused
+  streamed run of the same 151 layers against that, then the first measurements of c5's final
+  Bernoulli(0.01) window on both sides.
 The CPU work is bounded (tens of seconds to a few minutes on the box's host cores).
 """
 import os
@@ -168,6 +169,12 @@ def test_c5_width_snapshot_window_and_collapses(q, ref):
     gx, gz, gs = t.planes()
     assert _same(gs, s) and _same(gx, x) and _same(gz, z)
     del gx, gz, gs
+    # The fused, streamed product path (SWAP relabelling, single-qubit runs folded into the next
+    # two-qubit gate, rows un-permuted at the end) over the same C5_LAYERS + 1 layers.
+    fused = q.run_single_shot(q.generate_random(n, C5_LAYERS + 1, 42, 0.0), 7)
+    fx, fz, fs = fused.tableau.planes()
+    assert _same(fs, s) and _same(fx, x) and _same(fz, z)
+    del fused, fx, fz, fs
     meas = mwin[0][:C5_MEASURE]
     rng = q.RandomStream(7, 0)
     rec = q.MeasurementRecord()
