@@ -22,7 +22,7 @@ def check(name, cond):
     ok &= bool(cond)
 
 
-for n, depth, p, seed in [(130, 30, 1.0, 1), (200, 40, 0.5, 2), (65, 20, 1.0, 3)]:
+for n, depth, p, seed in [(130, 30, 1.0, 1), (200, 40, 0.5, 2), (65, 20, 1.0, 3), (2500, 40, 1.0, 4)]:
     c = q.generate_random(n, depth, seed, p)
     x, z, s, rec, _ = o.run_single_shot(n, c.gate_array, 7)
     r = q.run_single_shot(c, 7)  # streamed, fused, batched collapses (PDL chain)
@@ -33,9 +33,9 @@ for n, depth, p, seed in [(130, 30, 1.0, 1), (200, 40, 0.5, 2), (65, 20, 1.0, 3)
     for _ in range(2):  # eager, then CUDA-graph replay
         e.run(7)
     check(f"engine n={n}", np.array_equal(e.record(), rec))
-    se = q.ShardedEngine(c, 2)  # local exchange: the sharded protocol on one device
+    se = q.ShardedEngine(c, min(2, (n + 63) // 64))  # local exchange (3 shards at n = 2,500 exhaust racecheck's host memory)
     se.run(7)
-    check(f"sharded x2 n={n}", np.array_equal(se.record(), rec))
+    check(f"sharded n={n}", np.array_equal(se.record(), rec))
     meas, words, _ = o.sample(n, c.gate_array, 300, 7)
     smp = q.sample(c, 300, 7)
     check(f"sample n={n}", np.array_equal(smp.words, words))
