@@ -416,8 +416,9 @@ def main():
 
     # e2e through the public API with host buffers, every step: N = 1 -> qsr_run_single_shot
     # (schedule, validation, packed gate upload, simulation, record download) + final tableau
-    # download into pinned memory; N > 1 -> ShardedEngine create (schedule + upload per rank),
-    # run, record download and this rank's tableau columns.
+    # download into pinned memory; N > 1 -> qsr_sharded_run_circuit on every rank (the same
+    # streamed driver on the rank's shard, sharded measurement), record download and this rank's
+    # tableau columns.
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     # Host buffers: the full tableau at N = 1; each rank's own columns (1/N of it) at N > 1.
     plane = n_pad * 2 * k if world == 1 else n_pad * 2 * kg_local
@@ -431,8 +432,12 @@ def main():
     for i in range(e2e_steps):
         t1 = time.perf_counter()
         if world > 1 or shards > 1:
-            e = make_engine()
-            e.run(run_seed)
+            if world > 1:  # the streamed sharded driver: plan / fuse / upload behind the device
+                e = q.ShardedEngine(circ, world, device=device, exchange="nccl", rank=rank, nccl_id=nccl_id,
+                                    streamed_seed=run_seed)
+            else:
+                e = make_engine()
+                e.run(run_seed)
             _lib.check(_lib.lib.qsr_sharded_record(e._h, _lib.ptr(rec)))
             if world > 1:  # this rank's columns, compact
                 _lib.check(_lib.lib.qsr_sharded_tableau_local(e._h, C.cast(px, _lib.pu64), C.cast(pz, _lib.pu64),

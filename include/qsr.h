@@ -324,6 +324,14 @@ qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
                               const qsr_shard_config *cfg, qsr_sharded **out);
 /* One full single-shot pass (collective); *device_ms = CUDA-event time of this process. */
 qsr_status qsr_sharded_run(qsr_sharded *e, uint64_t seed, double *device_ms);
+/* run_single_shot<uint64_t>(circuit, seed) sharded, end to end from a host circuit (collective):
+ * this process's shard is created, the windows are planned, fused and uploaded while the device
+ * runs them (the streamed driver of qsr_run_single_shot) and measurement windows use the sharded
+ * protocol; `record` (measure_count entries) receives the whole record. One shard per process
+ * (QSR_EXCHANGE_NCCL, or QSR_EXCHANGE_LOCAL with world 1). *out keeps the final tableau shard
+ * (qsr_sharded_tableau_local / qsr_sharded_tableau / qsr_sharded_destroy). */
+qsr_status qsr_sharded_run_circuit(const qsr_circuit *c, const qsr_shard_config *cfg, uint64_t seed,
+                                   qsr_record_entry *record, qsr_sharded **out, double *device_ms);
 qsr_status qsr_sharded_stats(const qsr_sharded *e, double *gate_ms, uint64_t *gate_launches,
                              double *transpose_ms, double *measure_ms, uint64_t *launches);
 /* The full measurement record (identical on every rank). */

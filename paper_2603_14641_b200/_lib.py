@@ -179,6 +179,7 @@ SIGNATURES = {
     "qsr_nccl_unique_id": (i32, [pu8]),
     "qsr_sharded_create": (i32, [P, P, C.POINTER(ShardConfig_t), C.POINTER(P)]),
     "qsr_sharded_run": (i32, [P, u64, pd]),
+    "qsr_sharded_run_circuit": (i32, [P, C.POINTER(ShardConfig_t), u64, P, C.POINTER(P), pd]),
     "qsr_sharded_stats": (i32, [P, pd, pu64, pd, pd, pu64]),
     "qsr_sharded_record": (i32, [P, P]),
     "qsr_sharded_tableau": (i32, [P, pu64, pu64, pu64]),

@@ -99,9 +99,15 @@ void fill_report(qsr_run_report *rep, const RunTimes &rt, const DeviceSchedule &
 struct StreamCounts {
     uint64_t unitary = 0, measures = 0, windows = 0;
 };
+// Optional replacement of the measurement-window step (the generator-row-sharded engine's
+// protocol, shard.cpp): it must leave the window's record in t.ms.out.
+struct MeasureHook {
+    virtual ~MeasureHook() = default;
+    virtual void measure(const std::vector<uint32_t> &qubits, uint64_t seed, RunTimes &rt) = 0;
+};
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                            qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,
-                           FramesSink *frames = nullptr);
+                           FramesSink *frames = nullptr, MeasureHook *measure_hook = nullptr);
 // Host reference-layout <-> device layout (CM: [n_pad][2kg] words; RM: reference i-major).
 void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int layout);
 void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z);

@@ -71,6 +71,7 @@ constexpr uint32_t kDetChunk = 16; // deterministic outcomes whose partials shar
 
 struct qsr_sharded {
     uint64_t n = 0, k = 0;
+    uint64_t measure_count = 0;
     int world = 1;
     int device = 0;
     std::vector<Shard> sh;                 // local shards, ascending global rank
@@ -328,62 +329,114 @@ qsr_status qsr_nccl_unique_id(uint8_t out[128]) {
     });
 }
 
+} // extern "C"
+
+namespace {
+// Shards of this process + the exchange; with `circ` set, also the device-resident (fused)
+// schedule of the resident engine.
+std::unique_ptr<qsr_sharded> make_sharded(const Circuit &circ, const qsr_schedule *s, const qsr_shard_config *cfg,
+                                          bool resident) {
+    auto e = std::make_unique<qsr_sharded>();
+    e->n = circ.num_qubits;
+    e->world = cfg->world;
+    e->device = cfg->device;
+    if (e->n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
+    e->k = (e->n + 63) / 64;
+    if (cfg->world < 1 || uint64_t(cfg->world) > e->k)
+        fail(QSR_INVALID_ARGUMENT, "sharded: world must be in [1, ceil(n/64)]");
+    std::vector<int> my_ranks;
+    if (cfg->exchange == QSR_EXCHANGE_LOCAL) {
+        for (int r = 0; r < cfg->world; ++r) my_ranks.push_back(r);
+    } else if (cfg->exchange == QSR_EXCHANGE_NCCL) {
+        REQUIRE_PTR(cfg->nccl_id);
+        my_ranks.push_back(cfg->rank);
+    } else {
+        fail(QSR_INVALID_ARGUMENT, "sharded: unknown exchange");
+    }
+    QSR_CUDA(cudaSetDevice(cfg->device));
+    std::vector<cudaStream_t> streams;
+    for (int r : my_ranks) {
+        uint64_t j0 = 0, kg = 0;
+        shard_range(e->n, cfg->world, r, j0, kg);
+        Shard sd;
+        sd.j0 = j0;
+        sd.t = std::make_unique<DeviceTableau>(e->n, cfg->device, j0, kg);
+        streams.push_back(sd.t->stream);
+        e->sh.push_back(std::move(sd));
+    }
+    e->measure_count = circ.measure_count();
+    if (resident) {
+        e->ds = s ? upload_schedule(e->n, *s, cfg->device, e->sh[0].t->stream, true)
+                  : upload_circuit(circ, cfg->device, e->sh[0].t->stream, true);
+        if (e->ds->measure_count != e->measure_count)
+            fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
+    }
+    const uint64_t nm = std::max<uint64_t>(e->measure_count, 1);
+    for (auto &sd : e->sh) {
+        const uint64_t sw = det_slot_words(*sd.t);
+        QSR_CUDA(cudaMalloc(&sd.d_rec, nm * sizeof(qsr_record_entry)));
+        QSR_CUDA(cudaMalloc(&sd.d_masks, 4 * size_t(cfg->world)));
+        QSR_CUDA(cudaMalloc(&sd.d_plan, 16));
+        QSR_CUDA(cudaMalloc(&sd.det_send, kDetChunk * sw * 8));
+        QSR_CUDA(cudaMemset(sd.det_send, 0, kDetChunk * sw * 8));
+        QSR_CUDA(cudaMalloc(&sd.det_recv, kDetChunk * sw * 8 * size_t(cfg->world)));
+    }
+    QSR_CUDA(cudaMallocHost(&e->h_ctl, 2 * 8 * sizeof(uint32_t)));
+    for (auto &ev : e->bev) QSR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    if (cfg->exchange == QSR_EXCHANGE_LOCAL)
+        e->ex = make_local_exchange(cfg->world, streams);
+    else
+        e->ex = make_nccl_exchange(cfg->world, cfg->rank, streams[0], cfg->nccl_id);
+    QSR_CUDA(cudaDeviceSynchronize());
+    return e;
+}
+
+// The streamed driver (stream.cpp) on this process's one shard, with the sharded protocol for
+// every measurement window.
+struct ShardMeasure final : MeasureHook {
+    qsr_sharded &e;
+    explicit ShardMeasure(qsr_sharded &ee) : e(ee) {}
+    void measure(const std::vector<uint32_t> &qubits, uint64_t seed, RunTimes &rt) override {
+        e.measure_window(qubits, seed, rt);
+    }
+};
+} // namespace
+
+extern "C" {
+
 qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
                               const qsr_shard_config *cfg, qsr_sharded **out) {
     return guard([&] {
         REQUIRE_PTR(c);
         REQUIRE_PTR(cfg);
         REQUIRE_PTR(out);
+        *out = make_sharded(*c, s, cfg, /*resident=*/true).release();
+    });
+}
+
+qsr_status qsr_sharded_run_circuit(const qsr_circuit *c, const qsr_shard_config *cfg, uint64_t seed,
+                                   qsr_record_entry *record, qsr_sharded **out, double *device_ms) {
+    return guard([&] {
+        REQUIRE_PTR(c);
+        REQUIRE_PTR(cfg);
+        REQUIRE_PTR(out);
         const Circuit &circ = *c;
-        auto e = std::make_unique<qsr_sharded>();
-        e->n = circ.num_qubits;
-        e->world = cfg->world;
-        e->device = cfg->device;
-        if (e->n == 0) fail(QSR_INVALID_ARGUMENT, "Tableau: n must be >= 1");
-        e->k = (e->n + 63) / 64;
-        if (cfg->world < 1 || uint64_t(cfg->world) > e->k)
-            fail(QSR_INVALID_ARGUMENT, "sharded: world must be in [1, ceil(n/64)]");
-        std::vector<int> my_ranks;
-        if (cfg->exchange == QSR_EXCHANGE_LOCAL) {
-            for (int r = 0; r < cfg->world; ++r) my_ranks.push_back(r);
-        } else if (cfg->exchange == QSR_EXCHANGE_NCCL) {
-            REQUIRE_PTR(cfg->nccl_id);
-            my_ranks.push_back(cfg->rank);
-        } else {
-            fail(QSR_INVALID_ARGUMENT, "sharded: unknown exchange");
+        auto e = make_sharded(circ, nullptr, cfg, /*resident=*/false);
+        if (e->sh.size() != 1)
+            fail(QSR_INVALID_ARGUMENT, "sharded streamed run: one shard per process (NCCL exchange, or world 1)");
+        Shard &sd = e->sh[0];
+        RunTimes rt;
+        StreamCounts sc;
+        ShardMeasure hook(*e);
+        run_circuit_streaming(*sd.t, circ, seed, sd.d_rec, rt, sc, nullptr, &hook);
+        e->last = rt;
+        if (e->measure_count) {
+            REQUIRE_PTR(record);
+            QSR_CUDA(cudaMemcpyAsync(record, sd.d_rec, e->measure_count * sizeof(qsr_record_entry),
+                                     cudaMemcpyDeviceToHost, sd.t->stream));
         }
-        QSR_CUDA(cudaSetDevice(cfg->device));
-        std::vector<cudaStream_t> streams;
-        for (int r : my_ranks) {
-            uint64_t j0 = 0, kg = 0;
-            shard_range(e->n, cfg->world, r, j0, kg);
-            Shard sd;
-            sd.j0 = j0;
-            sd.t = std::make_unique<DeviceTableau>(e->n, cfg->device, j0, kg);
-            streams.push_back(sd.t->stream);
-            e->sh.push_back(std::move(sd));
-        }
-        e->ds = s ? upload_schedule(e->n, *s, cfg->device, e->sh[0].t->stream, true)
-                  : upload_circuit(circ, cfg->device, e->sh[0].t->stream, true);
-        if (e->ds->measure_count != circ.measure_count())
-            fail(QSR_INVALID_ARGUMENT, "schedule does not match the circuit's measurement count");
-        const uint64_t nm = std::max<uint64_t>(e->ds->measure_count, 1);
-        for (auto &sd : e->sh) {
-            const uint64_t sw = det_slot_words(*sd.t);
-            QSR_CUDA(cudaMalloc(&sd.d_rec, nm * sizeof(qsr_record_entry)));
-            QSR_CUDA(cudaMalloc(&sd.d_masks, 4 * size_t(cfg->world)));
-            QSR_CUDA(cudaMalloc(&sd.d_plan, 16));
-            QSR_CUDA(cudaMalloc(&sd.det_send, kDetChunk * sw * 8));
-            QSR_CUDA(cudaMemset(sd.det_send, 0, kDetChunk * sw * 8));
-            QSR_CUDA(cudaMalloc(&sd.det_recv, kDetChunk * sw * 8 * size_t(cfg->world)));
-        }
-        QSR_CUDA(cudaMallocHost(&e->h_ctl, 2 * 8 * sizeof(uint32_t)));
-        for (auto &ev : e->bev) QSR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        if (cfg->exchange == QSR_EXCHANGE_LOCAL)
-            e->ex = make_local_exchange(cfg->world, streams);
-        else
-            e->ex = make_nccl_exchange(cfg->world, cfg->rank, streams[0], cfg->nccl_id);
-        QSR_CUDA(cudaDeviceSynchronize());
+        sd.t->sync();
+        if (device_ms) *device_ms = rt.total_ms;
         *out = e.release();
     });
 }
@@ -391,6 +444,7 @@ qsr_status qsr_sharded_create(const qsr_circuit *c, const qsr_schedule *s,
 qsr_status qsr_sharded_run(qsr_sharded *e, uint64_t seed, double *device_ms) {
     return guard([&] {
         REQUIRE_PTR(e);
+        if (!e->ds) fail(QSR_INVALID_ARGUMENT, "sharded: no resident schedule (object of qsr_sharded_run_circuit)");
         const uint64_t l0 = g_launches;
         e->run(seed);
         e->launches = g_launches - l0;
@@ -421,7 +475,7 @@ qsr_status qsr_sharded_gate_bytes(const qsr_sharded *e, double *bytes) {
 qsr_status qsr_sharded_record(const qsr_sharded *e, qsr_record_entry *record) {
     return guard([&] {
         REQUIRE_PTR(e);
-        const uint64_t nm = e->ds->measure_count;
+        const uint64_t nm = e->measure_count;
         if (!nm) return;
         REQUIRE_PTR(record);
         QSR_CUDA(cudaSetDevice(e->device));

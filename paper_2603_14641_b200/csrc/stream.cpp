@@ -88,7 +88,7 @@ class BucketDir {
 
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                            qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,
-                           FramesSink *frames) {
+                           FramesSink *frames, MeasureHook *measure_hook) {
     const uint64_t G = c.gates.size();
     const uint32_t n = c.num_qubits;
     t.ensure_gate_buf(std::max<uint64_t>(G, 1));
@@ -252,7 +252,10 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                         t.ensure_window_cap(cnt);
                         const auto tm = clk::now();
                         QSR_CUDA(cudaMemcpyAsync(t.ms.mqubits, mq.data(), cnt * 4, cudaMemcpyHostToDevice, t.stream));
-                        measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
+                        if (measure_hook)
+                            measure_hook->measure(mq, seed, rt);
+                        else
+                            measure_window_device(t, cnt, seed, mq, flags, true, &rt.t_ms, &rt.ge_ms, &rt.cmp_ms);
                         t_meas += since(tm);
                         if (frames) frames->measure(mq.data(), cnt, t.stream);
                         QSR_CUDA(cudaMemcpyAsync(d_record + rec_off, t.ms.out, cnt * sizeof(qsr_record_entry),

@@ -752,7 +752,11 @@ class ShardedEngine:
     passes the same 128-byte `nccl_id` and the constructor is collective."""
 
     def __init__(self, circuit: Circuit, world: int, device: int = 0, exchange: str = "local",
-                 rank: int = 0, nccl_id: Optional[bytes] = None, schedule: Optional[Schedule] = None):
+                 rank: int = 0, nccl_id: Optional[bytes] = None, schedule: Optional[Schedule] = None,
+                 *, streamed_seed: Optional[int] = None):
+        """streamed_seed: run_single_shot(circuit, seed) end to end at construction (the streamed
+        driver, qsr_sharded_run_circuit; one shard per process) instead of building the resident
+        engine; record() / tableau_planes() then read that run's result."""
         cfg = _lib.ShardConfig_t()
         cfg.world, cfg.rank, cfg.device = world, rank, device
         cfg.exchange = {"local": _lib.EXCHANGE_LOCAL, "nccl": _lib.EXCHANGE_NCCL}[exchange]
@@ -763,10 +767,18 @@ class ShardedEngine:
             self._id = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             cfg.nccl_id = C.cast(self._id, C.POINTER(C.c_uint8))
         h = C.c_void_p()
-        check(lib.qsr_sharded_create(circuit._h, schedule._h if schedule is not None else None,
-                                     C.byref(cfg), C.byref(h)))
-        self._h = h
         self._nm = circuit.measure_count()
+        self.device_ms = None
+        if streamed_seed is None:
+            check(lib.qsr_sharded_create(circuit._h, schedule._h if schedule is not None else None,
+                                         C.byref(cfg), C.byref(h)))
+        else:
+            self._streamed_record = np.zeros(max(self._nm, 1), dtype=ENTRY_DTYPE)
+            ms = C.c_double()
+            check(lib.qsr_sharded_run_circuit(circuit._h, C.byref(cfg), streamed_seed, ptr(self._streamed_record),
+                                              C.byref(h), C.byref(ms)))
+            self.device_ms = ms.value
+        self._h = h
         self.n = circuit.num_qubits
         self.world, self.rank, self.exchange = world, rank, exchange
 

@@ -187,3 +187,33 @@ def test_sample_sharded_by_shot(q, oracle, shots):
             nw = rec.kf
             got[:, w0:w0 + nw] = np.asarray(rec.words, dtype=np.uint64).reshape(rows, nw)
         np.testing.assert_array_equal(got, full, err_msg=f"world={world}")
+
+
+@pytest.mark.parametrize("exchange", ["local", "nccl"])
+@pytest.mark.parametrize("case", ["final", "segments"])
+def test_sharded_streamed_run_circuit(q, oracle, exchange, case):
+    """qsr_sharded_run_circuit: the streamed driver (planning + fusion + upload overlapped with the
+    device) on this process's shard, measurement windows through the sharded protocol — the N > 1
+    e2e path of bench.py, exercised here at world 1 (one GPU)."""
+    n = 300
+    if case == "final":
+        c = q.generate_random(n, 40, 31, 0.5)
+    else:  # mid-circuit measure-all windows between unitary segments
+        c = q.Circuit(n, np.concatenate([q.generate_random(n, 20, 40 + r, 1.0).gate_array for r in range(3)]))
+    x, z, s, rec, _ = oracle.run_single_shot(n, c.gate_array, 5)
+    kw = dict(rank=0, nccl_id=q.nccl_unique_id()) if exchange == "nccl" else {}
+    e = q.ShardedEngine(c, 1, exchange=exchange, streamed_seed=5, **kw)
+    assert e.device_ms > 0
+    np.testing.assert_array_equal(e.record(), rec)
+    gx, gz, gs = e.tableau_planes()
+    np.testing.assert_array_equal(gx, x)
+    np.testing.assert_array_equal(gz, z)
+    np.testing.assert_array_equal(gs, s)
+    with pytest.raises(q.InvalidArgument):  # a resident-engine call on a streamed object
+        e.run(5)
+
+
+def test_sharded_streamed_needs_one_shard_per_process(q):
+    c = q.generate_random(200, 5, 1, 0.5)
+    with pytest.raises(q.InvalidArgument):
+        q.ShardedEngine(c, 2, exchange="local", streamed_seed=1)
