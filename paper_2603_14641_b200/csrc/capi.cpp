@@ -982,7 +982,6 @@ void qsr_engine_destroy(qsr_engine *e) { delete e; }
 struct qsr_frames {
     int device = 0;
     cudaStream_t stream = nullptr;
-    bool owns_stream = true; // false while riding a resident engine's stream (qsr_engine_sample)
     int num_sms = 148;
     uint64_t n = 0, shots = 0, kf = 0, pitch = 0; // kf: shot-words held here
     uint64_t j0 = 0;                                // global index of the first one
@@ -1005,13 +1004,7 @@ struct qsr_frames {
         if (rec) plane_cache().release(device, rec_cap * pitch * 8, rec);
         for (void *p : {(void *)gate_buf, (void *)d_idx})
             if (p) cudaFree(p);
-        if (stream && owns_stream) cudaStreamDestroy(stream);
-    }
-    void own_stream() { // leave the borrowed stream: later calls (downloads) run on a private one
-        if (owns_stream) return;
-        QSR_CUDA(cudaStreamSynchronize(stream));
-        QSR_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-        owns_stream = true;
+        if (stream) cudaStreamDestroy(stream);
     }
     void ensure_rows(uint64_t rows) {
         if (rows <= rec_cap) return;
@@ -1042,8 +1035,7 @@ void check_word_bits(unsigned wbits) {
 }
 
 std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t seed, int device,
-                                        uint64_t j0 = 0, uint64_t nw = 0, unsigned wbits = 64,
-                                        cudaStream_t borrow = nullptr) {
+                                        uint64_t j0 = 0, uint64_t nw = 0, unsigned wbits = 64) {
     check_word_bits(wbits);
     if (shots < 1) fail(QSR_INVALID_ARGUMENT, "init_frames: shots must be >= 1");
     if (n > kMaxQubits) fail(QSR_INVALID_ARGUMENT, "init_frames: n exceeds the supported maximum");
@@ -1051,12 +1043,7 @@ std::unique_ptr<qsr_frames> make_frames(uint64_t n, uint64_t shots, uint64_t see
     f->device = device;
     QSR_CUDA(cudaSetDevice(device));
     QSR_CUDA(cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (borrow) {
-        f->stream = borrow;
-        f->owns_stream = false;
-    } else {
-        QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
-    }
+    QSR_CUDA(cudaStreamCreateWithFlags(&f->stream, cudaStreamNonBlocking));
     f->n = n;
     f->shots = shots;
     f->kf = nw ? nw : (shots + 63) / 64;
@@ -1468,7 +1455,6 @@ qsr_status qsr_engine_sample(qsr_engine *e, uint64_t shots, uint64_t seed, int w
         cudaEventDestroy(b);
         e->launches = g_launches - l0;
         if (device_ms) *device_ms = ms;
-        f->own_stream();
         *out = f.release();
     });
 }

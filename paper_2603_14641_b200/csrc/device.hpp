@@ -168,6 +168,10 @@ void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx
 void configure_batch_kernels(int device); // per-device kernel attributes (current device)
 void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st);
 void batch_apply(DeviceTableau &t);
+// One GPU: the whole batch after the column bits in four launches (select; pivot rows +
+// memberships; absorb with the signs / coins / record of the V's in CTA 0; sign pass).
+void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b, uint64_t seed,
+                 uint32_t *d_pos, uint32_t expect);
 // Deterministic outcome of measuring q (measure.hpp:343-376), sharded form: this shard's
 // ordered partial product is written to `slot` ([x: rm_pitch][z: rm_pitch][e: 16 words]);
 // det_combine folds `nslots` slots (in shard order, stride det_slot_words) into the outcome,

@@ -313,12 +313,24 @@ __global__ void k_batch_reset(uint32_t *__restrict__ bctl, int *__restrict__ pco
 constexpr int kRowWords = 8;
 constexpr int kRowThreads = kB * kRowWords;
 
-__global__ void __launch_bounds__(kRowThreads)
-k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch, uint64_t ng,
-             uint64_t g0, const uint32_t *__restrict__ fq, uint64_t *__restrict__ Vx,
-             uint64_t *__restrict__ Vz, uint64_t vstride, uint32_t *__restrict__ vinfo,
-             const uint32_t *__restrict__ bctl, int *__restrict__ pcount) {
-    pdl_wait();
+struct RowsArgs {
+    uint64_t *x, *z;
+    uint64_t pitch, ng, g0;
+    const uint32_t *fq;
+    uint64_t *Vx, *Vz;
+    uint64_t vstride;
+    uint32_t *vinfo;
+    const uint32_t *bctl;
+    int *pcount;
+};
+
+__device__ __forceinline__ void rows_body(const RowsArgs &a, uint32_t block) {
+    uint64_t *__restrict__ x = a.x, *__restrict__ z = a.z, *__restrict__ Vx = a.Vx, *__restrict__ Vz = a.Vz;
+    const uint64_t pitch = a.pitch, ng = a.ng, g0 = a.g0, vstride = a.vstride;
+    const uint32_t *__restrict__ fq = a.fq;
+    uint32_t *__restrict__ vinfo = a.vinfo;
+    const uint32_t *__restrict__ bctl = a.bctl;
+    int *__restrict__ pcount = a.pcount;
     __shared__ u64 s_sx[kB][kRowWords], s_sz[kB][kRowWords], s_vx[kB][kRowWords];
     __shared__ uint32_t s_c[kB], s_l[kB];
     const uint32_t len = bctl[BL_LEN];
@@ -329,7 +341,7 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
         s_l[tid] = tid < len ? vinfo[VI_L + tid] : 0u;
     }
     __syncthreads();
-    const uint64_t i = uint64_t(blockIdx.x) * kRowWords + w;
+    const uint64_t i = uint64_t(block) * kRowWords + w;
     const bool act = i < pitch;
     {   // stage: thread (m, w) loads S_{c_m} word i (x and z)
         const uint64_t rs = ng + s_c[m];
@@ -377,23 +389,45 @@ k_pivot_rows(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
     z[(ng + c) * pitch + i] = i == (q >> 6) ? (1ull << (q & 63)) : 0ull;
 }
 
+__global__ void __launch_bounds__(kRowThreads) k_pivot_rows(RowsArgs a) {
+    pdl_wait();
+    rows_body(a, blockIdx.x);
+}
+
 // B3. Signs of the V_m (telescoped phase, file header), coins, record entries and the signs of
 // the replaced pairs. One warp: lane m stages collapse m's inputs and draws its coin (coins depend
 // only on their index), lane 0 runs the sign chain over shared memory, lanes write the results.
-__global__ void __launch_bounds__(32)
-k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
-               const uint32_t *__restrict__ fq, const uint32_t *__restrict__ fidx,
-               uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-               const int *__restrict__ pcount, uint64_t seed,
-               uint64_t *__restrict__ coin_index, qsr_record_entry *__restrict__ out,
-               int *__restrict__ err, const uint8_t *__restrict__ coin_table) {
-    pdl_wait();
+struct FinishArgs {
+    uint64_t *s;
+    uint64_t ng, g0;
+    const uint32_t *fq, *fidx;
+    uint32_t *vinfo;
+    const uint32_t *bctl;
+    const int *pcount;
+    uint64_t seed;
+    const uint64_t *coin_index;
+    qsr_record_entry *out;
+    int *err;
+    const uint8_t *coin_table;
+};
+
+// One warp (lane = threadIdx.x & 31).
+__device__ __forceinline__ void finish_body(const FinishArgs &a) {
+    uint64_t *__restrict__ s = a.s;
+    const uint64_t ng = a.ng, g0 = a.g0, seed = a.seed;
+    const uint32_t *__restrict__ fq = a.fq, *__restrict__ fidx = a.fidx, *__restrict__ bctl = a.bctl;
+    uint32_t *__restrict__ vinfo = a.vinfo;
+    const int *__restrict__ pcount = a.pcount;
+    const uint64_t *__restrict__ coin_index = a.coin_index;
+    qsr_record_entry *__restrict__ out = a.out;
+    int *__restrict__ err = a.err;
+    const uint8_t *__restrict__ coin_table = a.coin_table;
     __shared__ uint32_t s_c[kB], s_mc[kB], s_ss[kB], s_coin[kB], s_vsign[kB], s_beta[kB], s_p[kB];
     __shared__ int s_e[kB];
-    const uint32_t lane = threadIdx.x;
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
-    const uint64_t idx0 = *coin_index; // advanced by len in k_batch_member
+    const uint64_t idx0 = *coin_index; // advanced by len in k_batch_signs
     if (lane < len) {
         const uint64_t c = vinfo[VI_C + lane] - g0, rs = ng + c;
         s_c[lane] = uint32_t(c);
@@ -449,6 +483,11 @@ k_pivot_finish(uint64_t *__restrict__ s, uint64_t ng, uint64_t g0,
     }
 }
 
+__global__ void __launch_bounds__(32) k_pivot_finish(FinishArgs a) {
+    pdl_wait();
+    finish_body(a);
+}
+
 constexpr int kSlice = 64; // words per staged V slice (2 per lane)
 
 // ---- phase C: membership pass, slice-major absorb pass, sign pass -----------------------
@@ -474,22 +513,21 @@ constexpr int kGroups = kB / 4;              // 8 groups of 4 V's
 constexpr size_t kTableWords = size_t(kGroups) * 16 * 2 * kSlice; // 128 KB
 constexpr size_t kAbsorbSmem = kTableWords * sizeof(u64);
 
-__global__ void __launch_bounds__(256)
-k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint64_t g0,
-               const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
-               uint64_t k, const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-               unsigned long long *__restrict__ touched,
-               uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index) {
-    pdl_wait();
+struct MemberArgs {
+    uint32_t *colbits;
+    uint64_t nrows, ng, g0;
+    const uint32_t *vinfo, *bctl;
+    unsigned long long *touched;
+};
+
+__device__ __forceinline__ void member_body(const MemberArgs &a, uint32_t block) {
+    uint32_t *__restrict__ colbits = a.colbits;
+    const uint64_t nrows = a.nrows, ng = a.ng, g0 = a.g0;
+    const uint32_t *__restrict__ vinfo = a.vinfo, *__restrict__ bctl = a.bctl;
+    unsigned long long *__restrict__ touched = a.touched;
     __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
-    // The batch's collapses are done deciding: advance the speculation position and the coin
-    // index on every shard alike (k_pivot_finish drew coins idx0 .. idx0 + len - 1).
-    if (blockIdx.x == 0 && tid == 0 && len) {
-        if (d_pos) *d_pos += len;
-        *coin_index += len;
-    }
     if (tid < kB) {
         s_vb[tid] = vinfo[VI_VB + tid];
         const uint32_t cg = vinfo[VI_C + tid];
@@ -502,7 +540,7 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
         s_vbcol[tid] = col;
     }
     __syncthreads();
-    const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
+    const uint64_t r = uint64_t(block) * blockDim.x + tid;
     if (len == 0) return;
     uint32_t M = 0;
     if (r < nrows) {
@@ -524,16 +562,33 @@ k_batch_member(uint32_t *__restrict__ colbits, uint64_t nrows, uint64_t ng, uint
     }
 }
 
+__global__ void __launch_bounds__(256) k_batch_member(MemberArgs a) {
+    pdl_wait();
+    member_body(a, blockIdx.x);
+}
+
+// One-GPU chain: the pivot rows (blocks < rblocks) and the memberships (the rest) in one launch —
+// both need only the select's output.
+__global__ void __launch_bounds__(256) k_rows_member(RowsArgs ra, MemberArgs ma, uint32_t rblocks) {
+    pdl_wait();
+    if (blockIdx.x < rblocks) rows_body(ra, blockIdx.x);
+    else member_body(ma, blockIdx.x - rblocks);
+}
+
 __global__ void __launch_bounds__(kAThreads, 1)
 k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch,
                uint64_t nrows, const uint32_t *__restrict__ member,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
-               const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial, uint64_t stride) {
+               const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial, uint64_t stride,
+               FinishArgs fin, int do_finish) {
     pdl_wait();
     extern __shared__ __align__(16) u64 tab[]; // [g][S][plane][kSlice]
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // One-GPU chain: B3 (signs of the V's, coins, record) rides in CTA 0's first warp; only the
+    // sign pass after this kernel reads its output.
+    if (do_finish && blockIdx.x == 0 && warp == 0) finish_body(fin);
     const uint32_t ngroups = (len + 3) / 4;
     const uint64_t nslices = (pitch + kSlice - 1) / kSlice;
     // Work items are (slice, row group of kARows rows). Within a slice, blocks of kAWarps
@@ -660,12 +715,18 @@ __global__ void __launch_bounds__(256)
 k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
               const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-              int *__restrict__ err) {
+              int *__restrict__ err, uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index) {
     pdl_wait();
     __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB];
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x;
+    // The batch is decided: advance the speculation position and the coin index, on every shard
+    // alike (B3 drew coins idx0 .. idx0 + len - 1).
+    if (blockIdx.x == 0 && tid == 0) {
+        if (d_pos) *d_pos += len;
+        *coin_index += len;
+    }
     if (tid == 0) {
         uint32_t vs = 0, b0 = 0, b1 = 0;
         for (uint32_t j = 0; j < len; ++j) {
@@ -757,18 +818,36 @@ void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st) {
     count_launch();
 }
 
-void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
-                  uint64_t seed, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
+namespace {
+RowsArgs rows_args(DeviceTableau &t, const uint32_t *d_fq) {
+    MeasureScratch &ms = t.ms;
+    return RowsArgs{t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz, ms.vstride, ms.vinfo, ms.bctl, ms.pcount};
+}
+FinishArgs finish_args(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint64_t seed) {
+    MeasureScratch &ms = t.ms;
+    return FinishArgs{t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo, ms.bctl, ms.pcount, seed, ms.coin_index, ms.out, ms.err,
+                      ms.coin_table};
+}
+MemberArgs member_args(DeviceTableau &t) {
+    MeasureScratch &ms = t.ms;
+    return MemberArgs{ms.colbits, 2 * t.ng, t.ng, t.g0, ms.vinfo, ms.bctl, t.prof ? t.prof->d_rows : nullptr};
+}
+void launch_select(DeviceTableau &t, uint32_t b, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
     MeasureScratch &ms = t.ms;
     // (ms.pcount was zeroed by batch_colbits, which always precedes on this tableau.)
     launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
                  t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan);
-    launch_chain(k_pivot_rows, dim3(unsigned((t.rm_pitch + kRowWords - 1) / kRowWords)),
-                 dim3(kRowThreads), 0, t.stream, t.x, t.z, t.rm_pitch, t.ng, t.g0, d_fq, ms.Vx, ms.Vz,
-                 ms.vstride, ms.vinfo, ms.bctl, ms.pcount);
-    launch_chain(k_pivot_finish, dim3(1), dim3(32), 0, t.stream, t.s, t.ng, t.g0, d_fq, d_fidx, ms.vinfo,
-                 ms.bctl, ms.pcount, seed, ms.coin_index, ms.out, ms.err, ms.coin_table);
-    count_launch(3);
+    count_launch();
+}
+uint32_t rows_blocks(const DeviceTableau &t) { return uint32_t((t.rm_pitch + kRowWords - 1) / kRowWords); }
+} // namespace
+
+void batch_pivots(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b,
+                  uint64_t seed, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
+    launch_select(t, b, d_pos, expect, d_plan);
+    launch_chain(k_pivot_rows, dim3(rows_blocks(t)), dim3(kRowThreads), 0, t.stream, rows_args(t, d_fq));
+    launch_chain(k_pivot_finish, dim3(1), dim3(32), 0, t.stream, finish_args(t, d_fq, d_fidx, seed));
+    count_launch(2);
 }
 
 // Function attributes are per device context: raise the absorb pass's dynamic shared memory
@@ -794,7 +873,10 @@ uint64_t absorb_stride(uint64_t nfull) {
     return st;
 }
 
-void batch_apply(DeviceTableau &t) {
+namespace {
+// Member pass (unless `member` is false: the fused chain ran it with the pivot rows), absorb
+// (with B3 in CTA 0 when `fin` is set), signs.
+void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     configure_batch_kernels(t.device);
@@ -805,25 +887,41 @@ void batch_apply(DeviceTableau &t) {
         ms.partial = static_cast<uint8_t *>(cache_acquire(t.device, ms.partial_bytes));
     }
     const uint32_t row_blocks = uint32_t((nrows + 255) / 256);
-    launch_chain(k_batch_member, dim3(row_blocks), dim3(256), 0, t.stream, ms.colbits, nrows, t.ng, t.g0, ms.Vx,
-                 ms.Vz, ms.vstride, t.k, ms.vinfo, ms.bctl, t.prof ? t.prof->d_rows : nullptr, ms.d_pos,
-                 ms.coin_index);
+    if (member) {
+        launch_chain(k_batch_member, dim3(row_blocks), dim3(256), 0, t.stream, member_args(t));
+        count_launch();
+    }
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (t.prof) {
         QSR_CUDA(cudaEventCreate(&ea));
         QSR_CUDA(cudaEventCreate(&eb));
         QSR_CUDA(cudaEventRecord(ea, t.stream));
     }
+    const FinishArgs none{};
     launch_chain(k_batch_absorb, dim3(unsigned(t.num_sms)), dim3(kAThreads), kAbsorbSmem, t.stream, t.x, t.z,
                  t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
-                 absorb_stride(nrows / (uint64_t(kARows) * kAWarps)));
+                 absorb_stride(nrows / (uint64_t(kARows) * kAWarps)), fin ? *fin : none, fin ? 1 : 0);
     if (t.prof) {
         QSR_CUDA(cudaEventRecord(eb, t.stream));
         t.prof->ev.emplace_back(ea, eb);
     }
     launch_chain(k_batch_signs, dim3(row_blocks), dim3(256), 0, t.stream, t.s, nrows, nslices, ms.colbits,
-                 ms.partial, ms.vinfo, ms.bctl, ms.err);
-    count_launch(3);
+                 ms.partial, ms.vinfo, ms.bctl, ms.err, ms.d_pos, ms.coin_index);
+    count_launch(2);
+}
+} // namespace
+
+void batch_apply(DeviceTableau &t) { apply_passes(t, true, nullptr); }
+
+void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b, uint64_t seed,
+                 uint32_t *d_pos, uint32_t expect) {
+    launch_select(t, b, d_pos, expect, nullptr);
+    configure_batch_kernels(t.device);
+    const uint32_t rb = rows_blocks(t), mb = uint32_t((2 * t.ng + 255) / 256);
+    launch_chain(k_rows_member, dim3(rb + mb), dim3(256), 0, t.stream, rows_args(t, d_fq), member_args(t), rb);
+    count_launch();
+    const FinishArgs fin = finish_args(t, d_fq, d_fidx, seed);
+    apply_passes(t, false, &fin);
 }
 
 } // namespace qsr

@@ -469,8 +469,7 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
             while (qsize < 2 && spec < fq.size()) {
                 const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
                 batch_colbits(t, ms.fq + spec, b);
-                batch_pivots(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec));
-                batch_apply(t);
+                batch_fused(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec));
                 QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 4 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
                 QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
                 queue[(qhead + qsize) % 2] = Pending{spec, b, slot};
