@@ -130,7 +130,57 @@ void pinned_slot_release(uint32_t *p) {
     std::lock_guard<std::mutex> g(g_pinned_mu);
     g_pinned_free.push_back(p);
 }
+
+// Two page-locked staging buffers for downloads into pageable memory (download_2d), shared by
+// the process and allocated on first use.
+constexpr size_t kStageBytes = size_t(16) << 20;
+std::mutex g_stage_mu;
+uint8_t *g_stage[2] = {nullptr, nullptr};
 } // namespace
+
+// Device -> host copy of `rows` rows of `width` bytes. Page-locked destinations take one DMA
+// copy. Pageable ones go through the two pinned staging buffers in chunks of whole rows: chunk
+// i + 1 is in flight while chunk i is copied out on the host. (A direct copy into pageable
+// memory is staged by the driver at a fraction of PCIe bandwidth and has stalled for seconds
+// on freshly allocated arrays.)
+void download_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t rows,
+                 cudaStream_t st) {
+    if (!rows || !width) return;
+    cudaPointerAttributes at{};
+    const bool pinned = cudaPointerGetAttributes(&at, dst) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError(); // (a pageable pointer may leave an error on older runtimes)
+    if (pinned || width > kStageBytes) {
+        QSR_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, st));
+        QSR_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    std::lock_guard<std::mutex> g(g_stage_mu);
+    for (auto &b : g_stage)
+        if (!b) QSR_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&b), kStageBytes, cudaHostAllocPortable));
+    const size_t per = std::max<size_t>(1, kStageBytes / width);
+    const size_t nchunks = (rows + per - 1) / per;
+    cudaEvent_t ev[2];
+    for (auto &e : ev) QSR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    auto enqueue = [&](size_t c) {
+        const size_t r0 = c * per, nr = std::min(per, rows - r0);
+        QSR_CUDA(cudaMemcpy2DAsync(g_stage[c & 1], width, static_cast<const uint8_t *>(src) + r0 * spitch, spitch,
+                                   width, nr, cudaMemcpyDeviceToHost, st));
+        QSR_CUDA(cudaEventRecord(ev[c & 1], st));
+    };
+    enqueue(0);
+    for (size_t c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) enqueue(c + 1); // its buffer was copied out in iteration c - 1
+        QSR_CUDA(cudaEventSynchronize(ev[c & 1]));
+        const size_t r0 = c * per, nr = std::min(per, rows - r0);
+        uint8_t *d = static_cast<uint8_t *>(dst) + r0 * dpitch;
+        if (dpitch == width) {
+            std::memcpy(d, g_stage[c & 1], nr * width);
+        } else {
+            for (size_t r = 0; r < nr; ++r) std::memcpy(d + r * dpitch, g_stage[c & 1] + r * width, width);
+        }
+    }
+    for (auto e : ev) cudaEventDestroy(e);
+}
 
 void *cache_acquire(int device, uint64_t bytes) { return plane_cache().acquire(device, bytes); }
 void cache_release(int device, uint64_t bytes, void *p, cudaStream_t after) {
@@ -1196,11 +1246,8 @@ qsr_status qsr_frames_download(const qsr_frames *f, uint64_t *xf, uint64_t *zf) 
         REQUIRE_PTR(f);
         QSR_CUDA(cudaSetDevice(f->device));
         if (f->n == 0) return;
-        if (xf) QSR_CUDA(cudaMemcpy2DAsync(xf, f->kf * 8, f->xf, f->pitch * 8, f->kf * 8, f->n,
-                                           cudaMemcpyDeviceToHost, f->stream));
-        if (zf) QSR_CUDA(cudaMemcpy2DAsync(zf, f->kf * 8, f->zf, f->pitch * 8, f->kf * 8, f->n,
-                                           cudaMemcpyDeviceToHost, f->stream));
-        QSR_CUDA(cudaStreamSynchronize(f->stream));
+        if (xf) download_2d(xf, f->kf * 8, f->xf, f->pitch * 8, f->kf * 8, f->n, f->stream);
+        if (zf) download_2d(zf, f->kf * 8, f->zf, f->pitch * 8, f->kf * 8, f->n, f->stream);
     });
 }
 
@@ -1258,19 +1305,7 @@ qsr_status qsr_frames_record(const qsr_frames *f, uint64_t *nrows, uint32_t *mea
         if (words && !f->measured.empty()) {
             QSR_CUDA(cudaSetDevice(f->device));
             const uint64_t rows = f->measured.size();
-            if (f->pitch == f->kf) {
-                QSR_CUDA(cudaMemcpyAsync(words, f->rec, rows * f->kf * 8, cudaMemcpyDeviceToHost, f->stream));
-            } else {
-                // Strip the row padding on the device (a pitched copy into pageable host memory
-                // runs at a fraction of PCIe bandwidth), then one linear download.
-                uint64_t *packed = nullptr;
-                QSR_CUDA(cudaMallocAsync(&packed, rows * f->kf * 8, f->stream));
-                QSR_CUDA(cudaMemcpy2DAsync(packed, f->kf * 8, f->rec, f->pitch * 8, f->kf * 8, rows,
-                                           cudaMemcpyDeviceToDevice, f->stream));
-                QSR_CUDA(cudaMemcpyAsync(words, packed, rows * f->kf * 8, cudaMemcpyDeviceToHost, f->stream));
-                QSR_CUDA(cudaFreeAsync(packed, f->stream));
-            }
-            QSR_CUDA(cudaStreamSynchronize(f->stream));
+            download_2d(words, f->kf * 8, f->rec, f->pitch * 8, f->kf * 8, rows, f->stream);
         }
     });
 }

@@ -26,6 +26,10 @@ void cuda_check(cudaError_t e, const char *what);
 // The per-device caching allocator behind tableau planes and scratch (capi.cpp): a released
 // block is reused by the next acquire of the same size on the same device. `after`: the owner's
 // stream when the block may still be read by queued work; the next acquire waits for it.
+// Device -> host copy of rows x width bytes (pitched on both sides); pageable destinations are
+// staged through pinned buffers (capi.cpp).
+void download_2d(void *dst, size_t dpitch, const void *src, size_t spitch, size_t width, size_t rows,
+                 cudaStream_t st);
 void *cache_acquire(int device, uint64_t bytes);
 void cache_release(int device, uint64_t bytes, void *p, cudaStream_t after = nullptr);
 #define QSR_CUDA(call) ::qsr::cuda_check((call), #call)

@@ -389,10 +389,8 @@ void upload_planes(DeviceTableau &t, const uint64_t *x, const uint64_t *z, int l
 void download_planes(DeviceTableau &t, uint64_t *x, uint64_t *z) {
     TraceScope tr("download_planes");
     if (t.layout == QSR_COLUMN_MAJOR) {
-        if (x) QSR_CUDA(cudaMemcpy2DAsync(x, 2 * t.kg * 8, t.x, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad,
-                                          cudaMemcpyDeviceToHost, t.stream));
-        if (z) QSR_CUDA(cudaMemcpy2DAsync(z, 2 * t.kg * 8, t.z, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad,
-                                          cudaMemcpyDeviceToHost, t.stream));
+        if (x) download_2d(x, 2 * t.kg * 8, t.x, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad, t.stream);
+        if (z) download_2d(z, 2 * t.kg * 8, t.z, t.cm_pitch * 8, 2 * t.kg * 8, t.n_pad, t.stream);
         t.sync();
         return;
     }

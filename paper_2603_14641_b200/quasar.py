@@ -869,12 +869,20 @@ class FrameTableau:
         zf = np.ascontiguousarray(zf, dtype=np.uint64)
         check(lib.qsr_frames_upload(self._h, ptr(xf, C.c_uint64), ptr(zf, C.c_uint64)))
 
-    def record(self) -> "ShotRecord":
+    def record(self, out: Optional[np.ndarray] = None) -> "ShotRecord":
+        """The ShotRecord (frames.hpp:97-107). `out`: an optional uint64 host buffer of at least
+        rows x kf words (e.g. PinnedBuffer(...).array) the words are downloaded into; the
+        record's `words` is then a view of it."""
         nrows = C.c_uint64()
         check(lib.qsr_frames_record(self._h, C.byref(nrows), None, None))
         _, shots, kf = self._info()
         measured = np.zeros(nrows.value, dtype=np.uint32)
-        words = np.zeros(nrows.value * kf, dtype=np.uint64)
+        if out is not None:
+            if out.dtype != np.uint64 or not out.flags.c_contiguous or out.size < nrows.value * kf:
+                raise ValueError("record: out must be a contiguous uint64 array of >= rows x kf words")
+            words = out[:nrows.value * kf]
+        else:
+            words = np.zeros(nrows.value * kf, dtype=np.uint64)
         if nrows.value:
             check(lib.qsr_frames_record(self._h, C.byref(nrows), ptr(measured, C.c_uint32),
                                         ptr(words, C.c_uint64)))
@@ -918,9 +926,10 @@ def measure_sample(f: FrameTableau, window: Window, record=None, seed: int = 0, 
 
 
 def sample(circuit: Circuit, shots: int, seed: int, report: Optional[RunReport] = None,
-           device: int = 0, word_bits: int = 64) -> ShotRecord:
+           device: int = 0, word_bits: int = 64, out: Optional[np.ndarray] = None) -> ShotRecord:
     """sample<W>(circuit, shots, seed, report) (frames.hpp:163-204), W = word_bits in {8, 16, 32,
-    64}. The record keeps 64-bit words; ShotRecord.row_bytes(W) gives the reference's W rows."""
+    64}. The record keeps 64-bit words; ShotRecord.row_bytes(W) gives the reference's W rows.
+    `out`: optional host buffer for the record words (FrameTableau.record)."""
     h = C.c_void_p()
     rep = _lib.Report_t()
     check(lib.qsr_sample_word(circuit._h, shots, seed, word_bits, device, C.byref(h), C.byref(rep)))
@@ -928,11 +937,30 @@ def sample(circuit: Circuit, shots: int, seed: int, report: Optional[RunReport] 
     if report is not None:
         r = RunReport.from_c(rep)
         report.__dict__.update(r.__dict__)
-    return f.record()
+    return f.record(out)
+
+
+class PinnedBuffer:
+    """Page-locked host memory from libqsr (qsr_host_alloc): device->host downloads into it run
+    at PCIe speed, where a fresh pageable numpy array costs page faults and a staged copy."""
+
+    def __init__(self, nbytes: int, dtype=np.uint64):
+        self._p = C.c_void_p()
+        check(lib.qsr_host_alloc(max(int(nbytes), 8), C.byref(self._p)))
+        n = max(int(nbytes), 8) // np.dtype(dtype).itemsize
+        buf = (C.c_char * (n * np.dtype(dtype).itemsize)).from_address(self._p.value)
+        self.array = np.frombuffer(buf, dtype=dtype, count=n)
+
+    def __del__(self):
+        if getattr(self, "_p", None) and self._p.value:
+            self.array = None
+            lib.qsr_host_free(self._p)
+            self._p = C.c_void_p()
 
 
 def sample_shard(circuit: Circuit, shots: int, seed: int, world: int, rank: int,
-                 report: Optional[RunReport] = None, device: int = 0) -> Tuple[int, ShotRecord]:
+                 report: Optional[RunReport] = None, device: int = 0,
+                 out: Optional[np.ndarray] = None) -> Tuple[int, ShotRecord]:
     """sample() sharded by shot: this rank's shot-word slice. Returns (w0, record) where the
     record's rows hold the slice's kf = nw words (global words w0 .. w0+nw-1)."""
     h = C.c_void_p()
@@ -944,7 +972,7 @@ def sample_shard(circuit: Circuit, shots: int, seed: int, world: int, rank: int,
         report.__dict__.update(r.__dict__)
     j0, nw = C.c_uint64(), C.c_uint64()
     check(lib.qsr_frames_shot_words(h, C.byref(j0), C.byref(nw)))
-    return j0.value, f.record()
+    return j0.value, f.record(out)
 
 
 def device_count() -> int:

@@ -49,3 +49,22 @@ def test_engine_profile_counts_absorb_launches(q, oracle):
     assert prof["absorb_rows"] > 0 and prof["absorb_ms"] > 0 and prof["row_words"] == (n + 63) // 64
     x, z, s, rec, _ = oracle.run_single_shot(n, c.gate_array, 7)
     np.testing.assert_array_equal(e.record(), rec)  # the profiled run is a normal run
+
+
+def test_sample_record_into_pinned_buffer(q, oracle):
+    """sample(..., out=PinnedBuffer.array): the record words land in the caller's page-locked
+    buffer (the c4 e2e leg), identical to the reference; a too-small buffer is refused."""
+    n, shots = 300, 2000
+    c = q.generate_random(n, 20, 8, 1.0)
+    meas, words, _ = oracle.sample(n, c.gate_array, shots, 6)
+    buf = q.PinnedBuffer(8 * len(meas) * ((shots + 63) // 64) + 64)
+    buf.array[:] = 0xDEADBEEF
+    rec = q.sample(c, shots, 6, out=buf.array)
+    np.testing.assert_array_equal(rec.words, words)
+    assert rec.words.ctypes.data == buf.array.ctypes.data
+    _, part = q.sample_shard(c, shots, 6, 2, 1, out=buf.array)
+    kf = (shots + 63) // 64
+    np.testing.assert_array_equal(part.words.reshape(len(meas), -1),
+                                  words.reshape(len(meas), kf)[:, kf // 2:])
+    with pytest.raises(ValueError):
+        q.sample(c, shots, 6, out=buf.array[:10])
