@@ -36,9 +36,15 @@ for n, depth, p, seed in [(130, 30, 1.0, 1), (200, 40, 0.5, 2), (65, 20, 1.0, 3)
     se = q.ShardedEngine(c, min(2, (n + 63) // 64))  # local exchange (3 shards at n = 2,500 exhaust racecheck's host memory)
     se.run(7)
     check(f"sharded n={n}", np.array_equal(se.record(), rec))
+    st = q.ShardedEngine(c, 1, exchange="local", streamed_seed=7)  # streamed driver + sharded protocol
+    check(f"sharded streamed n={n}", np.array_equal(st.record(), rec))
+    del st
     meas, words, _ = o.sample(n, c.gate_array, 300, 7)
-    smp = q.sample(c, 300, 7)
+    smp = q.sample(c, 300, 7)  # record staged through the pinned buffers (pageable destination)
     check(f"sample n={n}", np.array_equal(smp.words, words))
+    pb = q.PinnedBuffer(8 * len(meas) * 5 + 8)
+    smp = q.sample(c, 300, 7, out=pb.array)  # straight into a pinned buffer
+    check(f"sample pinned n={n}", np.array_equal(smp.words, words))
     rs, _ = e.sample(300, 7)
     check(f"engine sample n={n}", np.array_equal(rs.words, words))
     t = q.Tableau.zero_state(n)
