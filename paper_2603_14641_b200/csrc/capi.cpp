@@ -122,7 +122,8 @@ uint32_t *pinned_slot() {
         }
     }
     uint32_t *p = nullptr;
-    QSR_CUDA(cudaMallocHost(&p, 2 * 4 * 4));
+    QSR_CUDA(cudaMallocHost(&p, 2 * 8 * 4));
+    std::memset(p, 0, 2 * 8 * 4);
     return p;
 }
 void pinned_slot_release(uint32_t *p) {

@@ -68,7 +68,8 @@ struct MeasureScratch {
     uint32_t *vinfo = nullptr;
     uint32_t *bctl = nullptr;
     uint32_t *d_pos = nullptr;      // speculative batch position (k_batch.cu)
-    uint32_t *h_bctl = nullptr;     // pinned [2][4] batch control read-back slots
+    uint32_t *h_bctl = nullptr;     // pinned [2][8] batch control read-back slots (len, stopped,
+                                    // OR-mask, skipped, sequence number: k_batch_signs writes them)
     cudaEvent_t bev[2] = {nullptr, nullptr};
     uint8_t *partial = nullptr;     // [slices][2ng] per-(row, slice) phase bytes (k_batch.cu)
     uint64_t partial_bytes = 0;
@@ -174,8 +175,13 @@ void set_device_u32(uint32_t *p, uint32_t v, cudaStream_t st);
 void batch_apply(DeviceTableau &t);
 // One GPU: the whole batch after the column bits in four launches (select; pivot rows +
 // memberships; absorb with the signs / coins / record of the V's in CTA 0; sign pass).
+// With `host_slot`, the sign pass also writes the batch's control words there (page-locked host
+// memory) followed by `seq`, so the host learns the batch length without a copy in the stream.
+// With `next_fq` (next_b qubits), the sign pass also computes the next batch's column bits and
+// active ballot (what batch_colbits would), so that batch needs no column-bit launch.
 void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b, uint64_t seed,
-                 uint32_t *d_pos, uint32_t expect);
+                 uint32_t *d_pos, uint32_t expect, uint32_t *host_slot = nullptr, uint32_t seq = 0,
+                 const uint32_t *next_fq = nullptr, uint32_t next_b = 0);
 // Deterministic outcome of measuring q (measure.hpp:343-376), sharded form: this shard's
 // ordered partial product is written to `slot` ([x: rm_pitch][z: rm_pitch][e: 16 words]);
 // det_combine folds `nslots` slots (in shard order, stride det_slot_words) into the outcome,

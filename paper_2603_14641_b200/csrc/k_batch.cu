@@ -120,11 +120,14 @@ __global__ void __launch_bounds__(kSelThreads)
 k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
                uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
                uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect,
-               const uint32_t *__restrict__ plan) {
+               const uint32_t *__restrict__ plan, int *__restrict__ pcount) {
     pdl_wait();
     if (plan) { // sharded: only the batch's leader selects (the others' blocks stay zero)
         if (!plan[0]) return;
         b = min(b, plan[1]);
+    } else { // one GPU, no reset launch: zero the sums k_pivot_rows accumulates into
+        if (threadIdx.x < 2 * kB) pcount[threadIdx.x] = 0;
+        if (threadIdx.x < kB) vinfo[VI_PMAT + threadIdx.x] = 0u;
     }
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
@@ -265,7 +268,8 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     }
     if (tid == 0) {
         bctl[BL_LEN] = len;
-        bctl[BL_DET] = s_stop; // (d_pos advances in k_batch_member, on every shard)
+        bctl[BL_DET] = s_stop; // (d_pos advances in k_batch_signs, on every shard)
+        bctl[BL_SKIP] = 0;
     }
 }
 
@@ -711,13 +715,30 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
     }
 }
 
+// The next batch's column-bit pass riding the sign pass (one GPU, speculative successor): b = 0
+// means none.
+struct NextCols {
+    const uint64_t *x;
+    uint64_t pitch, ng;
+    const uint32_t *fq;
+    uint32_t b;
+    uint32_t *nz;
+};
+
 __global__ void __launch_bounds__(256)
 k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
-              const uint32_t *__restrict__ member, const uint8_t *__restrict__ partial,
+              uint32_t *member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
-              int *__restrict__ err, uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index) {
+              int *__restrict__ err, uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index,
+              uint32_t *__restrict__ host_slot, uint32_t seq, NextCols nc) {
     pdl_wait();
-    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB];
+    __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB], s_nq[kB];
+    if (host_slot && blockIdx.x == 0 && threadIdx.x == 0) { // the batch is decided: tell the host
+        volatile uint32_t *h = host_slot;
+        for (int i = 0; i < 4; ++i) h[i] = bctl[i];
+        __threadfence_system();
+        h[4] = seq;
+    }
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x;
@@ -727,22 +748,22 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
         if (d_pos) *d_pos += len;
         *coin_index += len;
     }
-    if (tid == 0) {
-        uint32_t vs = 0, b0 = 0, b1 = 0;
-        for (uint32_t j = 0; j < len; ++j) {
-            vs |= (vinfo[VI_SIGN + j] & 1u) << j;
-            b0 |= (vinfo[VI_BETA + j] & 1u) << j;
-            b1 |= ((vinfo[VI_BETA + j] >> 1) & 1u) << j;
-        }
-        s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
+    if (tid < kB) { // one warp: lane j loads V_j's words, ballots form the masks (kB == 32)
+        const bool v = tid < len;
+        const uint32_t sg = v ? vinfo[VI_SIGN + tid] : 0u, beta = v ? vinfo[VI_BETA + tid] : 0u;
+        s_p[tid] = v ? vinfo[VI_PMAT + tid] : 0u;
+        const uint32_t vs = __ballot_sync(0xffffffffu, sg & 1u), b0 = __ballot_sync(0xffffffffu, beta & 1u),
+                       b1 = __ballot_sync(0xffffffffu, (beta >> 1) & 1u);
+        if (tid == 0) s_vs_mask = vs, s_b0_mask = b0, s_b1_mask = b1;
+        if (tid < nc.b) s_nq[tid] = nc.fq[tid];
     }
-    if (tid < kB) s_p[tid] = tid < len ? vinfo[VI_PMAT + tid] : 0u;
     __syncthreads();
     const uint64_t r = uint64_t(blockIdx.x) * blockDim.x + tid;
     uint32_t f = 0;
     bool odd = false;
+    uint32_t M = 0;
     if (r < nrows) {
-        const uint32_t M = member[r];
+        M = member[r];
         if (M) {
             int E = 0;
             for (uint64_t sl = 0; sl < nslices; ++sl) E += partial[sl * nrows + r];
@@ -757,6 +778,22 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
     if (__any_sync(0xffffffffu, odd) && (tid & 31) == 0) atomicExch(err, 1);
     if ((tid & 31) == 0 && bits && r < nrows)
         reinterpret_cast<uint32_t *>(s)[r >> 5] ^= bits; // rows r..r+31 own this half-word
+    if (nc.b) { // the next batch's column bits and active ballot (k_colbits), from the final rows
+        uint32_t cb = 0;
+        if (r < nrows) {
+            const uint64_t *row = nc.x + r * nc.pitch;
+            uint32_t wi = 0xFFFFFFFFu;
+            uint64_t word = 0;
+            for (uint32_t m = 0; m < nc.b; ++m) {
+                const uint32_t q = s_nq[m];
+                if ((q >> 6) != wi) { wi = q >> 6; word = __ldcg(row + wi); }
+                cb |= uint32_t((word >> (q & 63)) & 1u) << m;
+            }
+            member[r] = cb; // (this thread read its membership above)
+        }
+        const uint32_t act = __ballot_sync(0xffffffffu, r >= nc.ng && r < nrows && cb != 0);
+        if ((tid & 31) == 0 && r >= nc.ng && r < nrows) nc.nz[(r - nc.ng) >> 5] = act;
+    }
 }
 
 } // namespace
@@ -793,8 +830,12 @@ static void launch_chain(void (*k)(P...), dim3 grid, dim3 block, size_t smem, cu
 void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b, bool zero_block) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
-    // Control words and the pivot kernels' phase sums, zeroed ahead of the chain.
-    launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount, ms.vinfo);
+    // Sharded batches: control words and the pivot kernels' phase sums zeroed ahead of the chain
+    // on every shard (the one-GPU chain's select does this itself: one launch fewer per batch).
+    if (zero_block) {
+        launch_chain(k_batch_reset, dim3(1), dim3(2 * kB), 0, t.stream, ms.bctl, ms.pcount, ms.vinfo);
+        count_launch();
+    }
     // The pivot rows and vinfo of the block (everything before bctl), zeroed for a sharded batch.
     const uint64_t zw = zero_block ? uint64_t(reinterpret_cast<uint64_t *>(ms.vinfo) - ms.batch_block) +
                                          (kVinfoWords * 4 + 7) / 8
@@ -802,7 +843,7 @@ void batch_colbits(DeviceTableau &t, const uint32_t *d_fq, uint32_t b, bool zero
     launch_chain(k_colbits, dim3(unsigned((nrows + 255) / 256)), dim3(256), 0, t.stream,
                  static_cast<const uint64_t *>(t.x), t.rm_pitch, nrows, t.ng, d_fq, b, ms.colbits,
                  ms.bctl + BL_STAB_OR, ms.nz, ms.batch_block, zw);
-    count_launch(2);
+    count_launch();
 }
 
 void shard_plan(DeviceTableau &t, const uint32_t *d_masks, int world, int rank, uint32_t b, uint32_t expect,
@@ -834,9 +875,9 @@ MemberArgs member_args(DeviceTableau &t) {
 }
 void launch_select(DeviceTableau &t, uint32_t b, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
     MeasureScratch &ms = t.ms;
-    // (ms.pcount was zeroed by batch_colbits, which always precedes on this tableau.)
+    // (Sharded: ms.pcount was zeroed by batch_colbits; one GPU: by the select itself.)
     launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
-                 t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan);
+                 t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan, ms.pcount);
     count_launch();
 }
 uint32_t rows_blocks(const DeviceTableau &t) { return uint32_t((t.rm_pitch + kRowWords - 1) / kRowWords); }
@@ -876,7 +917,8 @@ uint64_t absorb_stride(uint64_t nfull) {
 namespace {
 // Member pass (unless `member` is false: the fused chain ran it with the pivot rows), absorb
 // (with B3 in CTA 0 when `fin` is set), signs.
-void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin) {
+void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin, uint32_t *host_slot = nullptr,
+                  uint32_t seq = 0, const uint32_t *next_fq = nullptr, uint32_t next_b = 0) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     configure_batch_kernels(t.device);
@@ -906,7 +948,8 @@ void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin) {
         t.prof->ev.emplace_back(ea, eb);
     }
     launch_chain(k_batch_signs, dim3(row_blocks), dim3(256), 0, t.stream, t.s, nrows, nslices, ms.colbits,
-                 ms.partial, ms.vinfo, ms.bctl, ms.err, ms.d_pos, ms.coin_index);
+                 ms.partial, ms.vinfo, ms.bctl, ms.err, ms.d_pos, ms.coin_index, host_slot, seq,
+                 NextCols{t.x, t.rm_pitch, t.ng, next_fq, next_fq ? next_b : 0u, ms.nz});
     count_launch(2);
 }
 } // namespace
@@ -914,14 +957,15 @@ void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin) {
 void batch_apply(DeviceTableau &t) { apply_passes(t, true, nullptr); }
 
 void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b, uint64_t seed,
-                 uint32_t *d_pos, uint32_t expect) {
+                 uint32_t *d_pos, uint32_t expect, uint32_t *host_slot, uint32_t seq, const uint32_t *next_fq,
+                 uint32_t next_b) {
     launch_select(t, b, d_pos, expect, nullptr);
     configure_batch_kernels(t.device);
     const uint32_t rb = rows_blocks(t), mb = uint32_t((2 * t.ng + 255) / 256);
     launch_chain(k_rows_member, dim3(rb + mb), dim3(256), 0, t.stream, rows_args(t, d_fq), member_args(t), rb);
     count_launch();
     const FinishArgs fin = finish_args(t, d_fq, d_fidx, seed);
-    apply_passes(t, false, &fin);
+    apply_passes(t, false, &fin, host_slot, seq, next_fq, next_b);
 }
 
 } // namespace qsr

@@ -16,6 +16,8 @@
 //           k_det_partial / k_finish (ordered deterministic product, or steps 3-4)
 // Every kernel reads its control block from device memory, so a whole measurement window is
 // enqueued without a host round trip per collapse.
+#include <atomic>
+
 #include "common.cuh"
 #include "device.hpp"
 
@@ -418,6 +420,14 @@ void configure_measure_kernels(DeviceTableau &t) {
                                       int(smem)));
 }
 
+namespace {
+uint32_t next_batch_seq() {
+    static std::atomic<uint32_t> seq{0};
+    uint32_t v = ++seq;
+    return v ? v : ++seq; // (0 is a fresh slot's value)
+}
+} // namespace
+
 void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
                            const std::vector<uint32_t> &qubits, std::vector<uint8_t> &flags_host,
                            bool timed, double *t_ms, double *ge_ms, double *cmp_ms) {
@@ -465,13 +475,52 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
         int qhead = 0, qsize = 0, slot = 0;
         size_t pos = 0, spec = 0;
         set_device_u32(ms.d_pos, 0, t.stream);
+        // The sign pass of each batch writes its control words + a sequence number into a pinned
+        // slot (no copy or event between the batches' kernels, so the launch chain stays
+        // programmatic across batches); the host waits for the sequence number. QSR_HOSTPOLL=0:
+        // a 16-byte copy + event per batch instead.
+        static const bool poll = [] {
+            const char *e = getenv("QSR_HOSTPOLL");
+            return !(e && e[0] == '0');
+        }();
+        uint32_t seqs[2] = {0, 0};
+        auto wait_slot = [&](int s) {
+            if (!poll) {
+                QSR_CUDA(cudaEventSynchronize(ms.bev[s]));
+                return;
+            }
+            volatile const uint32_t *h = ms.h_bctl + 8 * s;
+            for (uint32_t spin = 1; h[4] != seqs[s]; ++spin) {
+                if ((spin & 1023u) == 0) {
+                    const cudaError_t q = cudaStreamQuery(t.stream);
+                    if (q != cudaSuccess && q != cudaErrorNotReady) QSR_CUDA(q);
+                    if (q == cudaSuccess && h[4] != seqs[s])
+                        fail(QSR_LOGIC_ERROR, "measure_window: batch control words never arrived");
+                }
+            }
+            std::atomic_thread_fence(std::memory_order_acquire); // the control words, after seq
+        };
+        // The sign pass of each batch computes its speculative successor's column bits (QSR_FUSE_COLS=0:
+        // a separate column-bit launch per batch).
+        static const bool fuse_cols = [] {
+            const char *e = getenv("QSR_FUSE_COLS");
+            return !(e && e[0] == '0');
+        }();
+        bool cols_ready = false; // the previous batch's sign pass computed this batch's column bits
         while (pos < fq.size()) {
             while (qsize < 2 && spec < fq.size()) {
                 const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
-                batch_colbits(t, ms.fq + spec, b);
-                batch_fused(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec));
-                QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 4 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
-                QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
+                if (!cols_ready) batch_colbits(t, ms.fq + spec, b);
+                const size_t nxt = spec + b;
+                const uint32_t nb = fuse_cols && nxt < fq.size() ? uint32_t(std::min<size_t>(kMaxBatch, fq.size() - nxt)) : 0;
+                seqs[slot] = next_batch_seq(); // process-wide: pinned slots are recycled across tableaux
+                batch_fused(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec),
+                            poll ? ms.h_bctl + 8 * slot : nullptr, seqs[slot], nb ? ms.fq + nxt : nullptr, nb);
+                cols_ready = nb != 0;
+                if (!poll) {
+                    QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 8 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
+                    QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
+                }
                 queue[(qhead + qsize) % 2] = Pending{spec, b, slot};
                 ++qsize;
                 slot ^= 1;
@@ -480,19 +529,20 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
             const Pending p = queue[qhead];
             qhead = (qhead + 1) % 2;
             --qsize;
-            QSR_CUDA(cudaEventSynchronize(ms.bev[p.slot]));
-            const uint32_t *h = ms.h_bctl + 4 * p.slot;
+            wait_slot(p.slot);
+            volatile const uint32_t *h = ms.h_bctl + 8 * p.slot;
             if (h[3]) continue; // skipped (behind a batch that stopped early)
             pos = p.start + h[0];
             if (h[1]) {         // stopped: the measurement at pos is deterministic now
                 while (qsize) { // the speculative batch behind it is a no-op; drain it
-                    QSR_CUDA(cudaEventSynchronize(ms.bev[queue[qhead].slot]));
+                    wait_slot(queue[qhead].slot);
                     qhead = (qhead + 1) % 2;
                     --qsize;
                 }
                 deterministic_at(pos++);
                 set_device_u32(ms.d_pos, uint32_t(pos), t.stream);
                 spec = pos;
+                cols_ready = false; // the drained batch's successor columns were for another position
             }
         }
     } else {
