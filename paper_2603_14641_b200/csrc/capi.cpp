@@ -229,6 +229,10 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
         {reinterpret_cast<void **>(&ms.batch_block), ms.batch_block_bytes},
         {reinterpret_cast<void **>(&ms.nz), (ng / 32 + 1) * 4},
         {reinterpret_cast<void **>(&ms.pcount), 2 * kMaxBatch * sizeof(int)},
+        {reinterpret_cast<void **>(&ms.vinfo_b), (kVinfoWords + 8) * 4},
+        {reinterpret_cast<void **>(&ms.colbits_b), 2 * ng * 4},
+        {reinterpret_cast<void **>(&ms.nz_b), (ng / 32 + 1) * 4},
+        {reinterpret_cast<void **>(&ms.pcount_b), 2 * kMaxBatch * sizeof(int)},
         {reinterpret_cast<void **>(&ms.d_pos), 4},
     };
     arena_bytes = 0;
@@ -245,6 +249,7 @@ DeviceTableau::DeviceTableau(uint64_t n_, int dev, uint64_t j0, uint64_t kg_) : 
     ms.vstride = 2 * rm_pitch;
     ms.vinfo = reinterpret_cast<uint32_t *>(ms.batch_block + vwords);
     ms.bctl = ms.vinfo + kVinfoWords;
+    ms.bctl_b = ms.vinfo_b + kVinfoWords;
     ms.h_bctl = pinned_slot();
     for (auto &e : ms.bev) QSR_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     configure_measure_kernels(*this);

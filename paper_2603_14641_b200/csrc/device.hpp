@@ -40,7 +40,7 @@ inline void count_launch(uint64_t n = 1) { g_launches += n; }
 inline uint64_t round_up(uint64_t v, uint64_t m) { return (v + m - 1) / m * m; }
 
 constexpr int kMaxBatch = 32; // collapses per batched pass (k_batch.cu)
-constexpr int kVinfoWords = 7 * kMaxBatch; // per-batch pivot info (k_batch.cu)
+constexpr int kVinfoWords = 8 * kMaxBatch; // per-batch pivot info (k_batch.cu)
 
 // Scratch used by the measurement pipeline; sized for one tableau.
 struct MeasureScratch {
@@ -75,6 +75,10 @@ struct MeasureScratch {
     uint64_t partial_bytes = 0;
     uint32_t *nz = nullptr;         // [ng/32] active-stabilizer ballot of the batch
     int *pcount = nullptr;          // [2*kMaxBatch] per-pivot phase / beta counters
+    // Second buffer set for chained one-GPU batches (batch_chained): batch k+1's select writes
+    // these while batch k still reads the first set.
+    uint32_t *vinfo_b = nullptr, *bctl_b = nullptr, *colbits_b = nullptr, *nz_b = nullptr;
+    int *pcount_b = nullptr;
     uint32_t *fq = nullptr, *fidx = nullptr; // flagged qubits / window indices [window_cap]
     // Caller-drawn coins for the current measurement window (nullptr = device Philox).
     uint8_t *coin_table = nullptr;
@@ -177,6 +181,19 @@ void batch_apply(DeviceTableau &t);
 // memberships; absorb with the signs / coins / record of the V's in CTA 0; sign pass).
 // With `host_slot`, the sign pass also writes the batch's control words there (page-locked host
 // memory) followed by `seq`, so the host learns the batch length without a copy in the stream.
+// One GPU, chained batches: this batch in the tableau's current buffers (ms.vinfo / bctl / colbits
+// / nz / pcount), the next one's select inside this batch's absorb (its last CTA) into `nxt`, with
+// column bits the membership pass derives (nfq / nb: the next batch's qubits; nfq2 / nb2: the one
+// after, whose V bits the sign pass forms). `standalone`: this batch's column bits and select
+// are launched first (the window's first batch, or after an early stop).
+struct BatchBufs {
+    uint32_t *vinfo, *bctl, *colbits, *nz;
+    int *pcount;
+};
+void batch_chained(DeviceTableau &t, const BatchBufs &nxt, const uint32_t *d_fq, const uint32_t *d_fidx,
+                   uint32_t b, uint64_t seed, bool standalone, uint32_t *d_pos, uint32_t expect,
+                   const uint32_t *nfq, uint32_t nb, const uint32_t *nfq2, uint32_t nb2, uint32_t *host_slot,
+                   uint32_t seq);
 // With `next_fq` (next_b qubits), the sign pass also computes the next batch's column bits and
 // active ballot (what batch_colbits would), so that batch needs no column-bit launch.
 void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx, uint32_t b, uint64_t seed,

@@ -43,12 +43,13 @@ namespace {
 using u64 = unsigned long long;
 constexpr int kB = kMaxBatch; // collapses per batch (<= 32: u32 membership masks)
 enum : uint32_t { BL_LEN = 0, BL_DET = 1, BL_STAB_OR = 2, BL_SKIP = 3 };
-// vinfo layout (u32 [7*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m |
+// vinfo layout (u32 [8*kB]): vb | sign of V_m | c_m (global) | beta(V_m) mod 4 | Mc_m |
 // L_m = row m of (I + Mc)^-1 over GF(2) (V_m = XOR_{j in L_m} S_{c_j} at batch start) |
-// pair-parity row P_m (bit j' < m: parity(sum_i |V_mz[i] & V_j'x[i]|))
+// pair-parity row P_m (bit j' < m: parity(sum_i |V_mz[i] & V_j'x[i]|)) | X bits of V_m at the
+// next batch's qubits (one GPU, chained batches)
 enum : uint32_t { VI_VB = 0, VI_SIGN = kB, VI_C = 2 * kB, VI_BETA = 3 * kB, VI_MC = 4 * kB, VI_L = 5 * kB,
-                  VI_PMAT = 6 * kB };
-static_assert(7 * kB == kVinfoWords, "vinfo layout");
+                  VI_PMAT = 6 * kB, VI_VBN = 7 * kB };
+static_assert(8 * kB == kVinfoWords, "vinfo layout");
 
 __device__ __forceinline__ uint32_t parity32(uint32_t v) { return __popc(v) & 1u; }
 // Kernels of the batch chain launch with programmatic stream serialization (launch_chain): each
@@ -113,32 +114,81 @@ __global__ void k_colbits(const uint64_t *__restrict__ x, uint64_t pitch, uint64
 // incrementally, so a step is O(1) per candidate. If none of them qualifies, the stabilizers
 // after the window are scanned with memberships recomputed from the column bits.
 constexpr int kSelThreads = 256;
-constexpr int kSelRows = 4;
-constexpr int kWin = kSelThreads * kSelRows;
+constexpr int kWin = 1024; // candidates (kWin / T per thread)
 
-__global__ void __launch_bounds__(kSelThreads)
-k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict__ nz,
-               uint64_t n_gen, uint64_t ng, uint64_t g0, uint32_t b, uint32_t *__restrict__ vinfo,
-               uint32_t *__restrict__ bctl, uint32_t *__restrict__ d_pos, uint32_t expect,
-               const uint32_t *__restrict__ plan, int *__restrict__ pcount) {
-    pdl_wait();
+// X bits of V_j (j < len) at the next batch's qubits nfq[0..nb): lane i reads row S_{c_i} (its
+// final state, batch start) at those qubits, and V_j = XOR_{i in L_j} S_{c_i} (one warp).
+__device__ __forceinline__ uint32_t vbn_lane(uint32_t lane, bool valid, uint64_t c_local, uint32_t L,
+                                             const uint64_t *__restrict__ x, uint64_t pitch, uint64_t ng,
+                                             const uint32_t *__restrict__ nfq, uint32_t nb) {
+    uint32_t xb = 0;
+    if (valid) {
+        const uint64_t *row = x + (ng + c_local) * pitch;
+        uint32_t wi = 0xFFFFFFFFu;
+        uint64_t word = 0;
+        for (uint32_t m = 0; m < nb; ++m) {
+            const uint32_t q = nfq[m];
+            if ((q >> 6) != wi) { wi = q >> 6; word = __ldcg(row + wi); }
+            xb |= uint32_t((word >> (q & 63)) & 1u) << m;
+        }
+    }
+    uint32_t v = 0;
+    for (uint32_t i = 0; i < 32; ++i) {
+        const uint32_t xi = __shfl_sync(0xffffffffu, xb, i);
+        if ((L >> i) & 1u) v ^= xi;
+    }
+    return v;
+}
+
+struct SelectArgs {
+    const uint32_t *colbits, *nz;
+    uint64_t n_gen, ng, g0;
+    uint32_t b;
+    uint32_t *vinfo, *bctl;
+    uint32_t *d_pos; // standalone one-GPU batches: valid iff *d_pos == expect
+    uint32_t expect;
+    const uint32_t *plan; // sharded: the leader plan (nullptr on one GPU)
+    int *pcount;          // one GPU: zeroed here (no reset launch)
+    // Chained one-GPU batch (selected inside the previous batch's absorb): valid iff the previous
+    // batch collapsed all prev_b of its measurements (its control words, another buffer set).
+    const uint32_t *prev_bctl;
+    uint32_t prev_b;
+    // Standalone one-GPU batch: also the X bits of its V's at the next batch's qubits (VI_VBN).
+    const uint64_t *x;
+    uint64_t pitch;
+    const uint32_t *nfq;
+    uint32_t nb;
+};
+
+template <int T>
+__device__ __forceinline__ void select_body(const SelectArgs &a) {
+    constexpr int R = kWin / T;
+    const uint32_t *__restrict__ colbits = a.colbits, *__restrict__ nz = a.nz;
+    const uint64_t n_gen = a.n_gen, ng = a.ng, g0 = a.g0;
+    uint32_t b = a.b;
+    uint32_t *__restrict__ vinfo = a.vinfo, *__restrict__ bctl = a.bctl;
+    const uint32_t *__restrict__ plan = a.plan;
     if (plan) { // sharded: only the batch's leader selects (the others' blocks stay zero)
         if (!plan[0]) return;
         b = min(b, plan[1]);
     } else { // one GPU, no reset launch: zero the sums k_pivot_rows accumulates into
-        if (threadIdx.x < 2 * kB) pcount[threadIdx.x] = 0;
+        if (threadIdx.x < 2 * kB) a.pcount[threadIdx.x] = 0;
         if (threadIdx.x < kB) vinfo[VI_PMAT + threadIdx.x] = 0u;
     }
     __shared__ uint32_t s_rows[kWin];
     __shared__ uint32_t s_vbcol[kB], s_vb[kB], s_c[kB], s_mc[kB];
-    __shared__ uint32_t s_scan[kSelThreads / 32];
+    __shared__ uint32_t s_scan[T / 32];
     __shared__ uint32_t s_nwin, s_next, s_minb[2], s_len, s_stop;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t nzw = (n_gen + 31) / 32;
     if (tid < kB) s_vbcol[tid] = 0;
     // Speculative batches (measure_window_device): a batch enqueued behind one that stopped
-    // early starts at the wrong position and turns into a no-op.
-    if (!plan && d_pos && *d_pos != expect) {
+    // early (a chained batch: the previous batch's length; a standalone one: the device position)
+    // turns into a no-op.
+    const bool stale = !plan && (a.prev_bctl ? (a.prev_bctl[BL_LEN] != a.prev_b || a.prev_bctl[BL_DET] != 0u ||
+                                                a.prev_bctl[BL_SKIP] != 0u)
+                                             : (a.d_pos && *a.d_pos != a.expect));
+    if (stale) {
         if (tid < kB) vinfo[VI_C + tid] = 0xFFFFFFFFu;
         if (tid == 0) { bctl[BL_LEN] = 0; bctl[BL_DET] = 0; bctl[BL_SKIP] = 1; }
         return;
@@ -146,7 +196,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     if (tid == 0) { s_nwin = 0; s_next = uint32_t(n_gen); s_len = b; s_stop = 0; s_minb[0] = s_minb[1] = 0xFFFFFFFFu; }
     __syncthreads();
     // Window: the first kWin active stabilizers in ascending order.
-    for (uint64_t base = 0; base < nzw; base += kSelThreads) {
+    for (uint64_t base = 0; base < nzw; base += T) {
         const uint64_t w = base + tid;
         const uint32_t word = w < nzw ? nz[w] : 0u;
         const uint32_t cnt = __popc(word);
@@ -166,17 +216,17 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
             if (pos == uint32_t(kWin) - 1) s_next = row + 1;
         }
         __syncthreads();
-        if (tid == kSelThreads - 1) s_nwin = min(off + incl, uint32_t(kWin));
+        if (tid == T - 1) s_nwin = min(off + incl, uint32_t(kWin));
         __syncthreads();
         if (s_nwin >= uint32_t(kWin)) break;
     }
     const uint32_t nwin = s_nwin;
     // cur[u]: the candidate's current X bits at the batch's qubits (batch-start bits XOR the vb
     // of every V it absorbed), so its bit at q_m is one shift and absorbing V_m one XOR.
-    uint32_t row[kSelRows], cur[kSelRows], M[kSelRows];
+    uint32_t row[R], cur[R], M[R];
 #pragma unroll
-    for (int u = 0; u < kSelRows; ++u) {
-        const uint32_t e = tid + u * kSelThreads;
+    for (int u = 0; u < R; ++u) {
+        const uint32_t e = tid + u * T;
         row[u] = e < nwin ? s_rows[e] : 0xFFFFFFFFu;
         cur[u] = e < nwin ? colbits[ng + row[u]] : 0u;
         M[u] = 0;
@@ -186,7 +236,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         const uint32_t pm = m & 1u;
         uint32_t best = 0xFFFFFFFFu, bits = 0;
 #pragma unroll
-        for (int u = 0; u < kSelRows; ++u) {
+        for (int u = 0; u < R; ++u) {
             const uint32_t bit = (cur[u] >> m) & 1u;
             bits |= bit << u;
             if (bit) best = min(best, row[u]); // used pivots are inert (cur = 0)
@@ -198,7 +248,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         if (s_minb[pm] == 0xFFFFFFFFu) {
             // Fallback: stabilizers after the window, memberships from the column bits.
             const uint32_t vc = s_vbcol[m];
-            for (uint64_t g0r = s_next; g0r < n_gen; g0r += kSelThreads) {
+            for (uint64_t g0r = s_next; g0r < n_gen; g0r += T) {
                 const uint64_t g = g0r + tid;
                 uint32_t cand = 0xFFFFFFFFu;
                 if (g < n_gen) {
@@ -224,7 +274,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         }
         // A pivot from the window: its owner holds cur and the memberships in registers.
 #pragma unroll
-        for (int u = 0; u < kSelRows; ++u) {
+        for (int u = 0; u < R; ++u) {
             if (row[u] == c) {
                 s_vb[m] = cur[u];
                 s_c[m] = c;
@@ -244,7 +294,7 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
         const uint32_t vb = s_vb[m];
         if (tid < kB) s_vbcol[tid] |= ((vb >> tid) & 1u) << m; // read by the fallback only
 #pragma unroll
-        for (int u = 0; u < kSelRows; ++u) {
+        for (int u = 0; u < R; ++u) {
             if (row[u] == c) { cur[u] = 0; M[u] = 0; row[u] = 0xFFFFFFFFu; } // now +/-Z_q: inert
             else if ((bits >> u) & 1u) { M[u] |= 1u << m; cur[u] ^= vb; }
         }
@@ -265,6 +315,8 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
             if ((mc >> j) & 1u) acc ^= lj;
         }
         vinfo[VI_L + tid] = v ? (acc ^ (1u << tid)) : 0u;
+        if (a.nb) vinfo[VI_VBN + tid] = vbn_lane(tid, v, s_c[tid], v ? (acc ^ (1u << tid)) : 0u, a.x, a.pitch, ng,
+                                                 a.nfq, a.nb);
     }
     if (tid == 0) {
         bctl[BL_LEN] = len;
@@ -273,7 +325,10 @@ k_pivot_select(const uint32_t *__restrict__ colbits, const uint32_t *__restrict_
     }
 }
 
-
+__global__ void __launch_bounds__(kSelThreads) k_pivot_select(SelectArgs a) {
+    pdl_wait();
+    select_body<kSelThreads>(a);
+}
 
 __global__ void k_set_u32(uint32_t *p, uint32_t v) { *p = v; }
 
@@ -522,6 +577,14 @@ struct MemberArgs {
     uint64_t nrows, ng, g0;
     const uint32_t *vinfo, *bctl;
     unsigned long long *touched;
+    // Chained one-GPU batches: the next batch's column bits and active ballot, from each row's
+    // current X bits at its qubits (rows other than the pivots are not rewritten before the
+    // absorb) and the X bits there of the V's it will absorb (VI_VBN).
+    const uint64_t *x;
+    uint64_t pitch;
+    const uint32_t *nfq;
+    uint32_t nb;
+    uint32_t *colbits_next, *nz_next;
 };
 
 __device__ __forceinline__ void member_body(const MemberArgs &a, uint32_t block) {
@@ -529,10 +592,12 @@ __device__ __forceinline__ void member_body(const MemberArgs &a, uint32_t block)
     const uint64_t nrows = a.nrows, ng = a.ng, g0 = a.g0;
     const uint32_t *__restrict__ vinfo = a.vinfo, *__restrict__ bctl = a.bctl;
     unsigned long long *__restrict__ touched = a.touched;
-    __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB];
+    __shared__ uint32_t s_vbcol[kB], s_c[kB], s_vb[kB], s_vbn[kB], s_nq[kB];
     const uint32_t len = bctl[BL_LEN];
     const uint32_t tid = threadIdx.x;
     if (tid < kB) {
+        s_vbn[tid] = a.nb ? vinfo[VI_VBN + tid] : 0u;
+        if (tid < a.nb) s_nq[tid] = a.nfq[tid];
         s_vb[tid] = vinfo[VI_VB + tid];
         const uint32_t cg = vinfo[VI_C + tid];
         s_c[tid] = (cg != 0xFFFFFFFFu && cg >= g0 && cg < g0 + ng) ? uint32_t(cg - g0) : 0xFFFFFFFFu;
@@ -546,7 +611,7 @@ __device__ __forceinline__ void member_body(const MemberArgs &a, uint32_t block)
     __syncthreads();
     const uint64_t r = uint64_t(block) * blockDim.x + tid;
     if (len == 0) return;
-    uint32_t M = 0;
+    uint32_t M = 0, ncb = 0;
     if (r < nrows) {
         // Pivot stabilizers are final already; replaced destabilizers restart from V_m after
         // collapse m; every other row starts from its batch-start column bits.
@@ -559,6 +624,29 @@ __device__ __forceinline__ void member_body(const MemberArgs &a, uint32_t block)
         }
         M = skip ? 0u : membership(cb, s_vbcol, start, len);
         colbits[r] = M;
+        if (a.nb) { // (the pivot stabilizers become +/-Z_q: no X bits, ncb = 0)
+            if (!skip) {
+                if (start) {
+                    ncb = s_vbn[start - 1]; // destabilizer D_c <- V_{start-1}
+                } else {
+                    const uint64_t *row = a.x + r * a.pitch;
+                    uint32_t wi = 0xFFFFFFFFu;
+                    uint64_t word = 0;
+                    for (uint32_t m = 0; m < a.nb; ++m) {
+                        const uint32_t q = s_nq[m];
+                        if ((q >> 6) != wi) { wi = q >> 6; word = __ldcg(row + wi); }
+                        ncb |= uint32_t((word >> (q & 63)) & 1u) << m;
+                    }
+                }
+                for (uint32_t U = M; U; U &= U - 1) ncb ^= s_vbn[__ffs(U) - 1];
+            }
+            a.colbits_next[r] = ncb;
+        }
+    }
+    if (a.nb) {
+        const bool stab = r >= ng && r < nrows;
+        const uint32_t act = __ballot_sync(0xffffffffu, stab && ncb != 0u);
+        if ((tid & 31) == 0 && stab) a.nz_next[(r - ng) >> 5] = act;
     }
     if (touched) { // profile runs only: rows the absorb pass rewrites
         const uint32_t b = __ballot_sync(0xffffffffu, M != 0u);
@@ -584,8 +672,16 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
                uint64_t nrows, const uint32_t *__restrict__ member,
                const uint64_t *__restrict__ Vx, const uint64_t *__restrict__ Vz, uint64_t vstride,
                const uint32_t *__restrict__ bctl, uint8_t *__restrict__ partial, uint64_t stride,
-               FinishArgs fin, int do_finish) {
+               FinishArgs fin, int do_finish, SelectArgs sel, int sel_cta) {
     pdl_wait();
+    // Chained one-GPU batches: the last CTA selects the next batch's pivots (from column bits the
+    // membership pass already derived) while the others absorb this one; it runs even when this
+    // batch is empty, so the next batch's control words are always written.
+    if (sel_cta && blockIdx.x == gridDim.x - 1) {
+        select_body<kAThreads>(sel);
+        return;
+    }
+    const uint32_t grid = gridDim.x - (sel_cta ? 1u : 0u);
     extern __shared__ __align__(16) u64 tab[]; // [g][S][plane][kSlice]
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
@@ -603,7 +699,7 @@ k_batch_absorb(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitc
     const uint64_t ngr = (nrows + kARows - 1) / kARows;
     const uint64_t nblk = nrows / (uint64_t(kARows) * kAWarps), nmapped = nblk * kAWarps;
     const uint64_t total = nslices * ngr;
-    const uint64_t item0 = total * blockIdx.x / gridDim.x, item1 = total * (blockIdx.x + 1) / gridDim.x;
+    const uint64_t item0 = total * blockIdx.x / grid, item1 = total * (blockIdx.x + 1) / grid;
     const uint64_t step = nblk ? stride % nblk : 0;
     uint64_t it = item0;
     while (it < item1) {
@@ -724,13 +820,23 @@ struct NextCols {
     uint32_t b;
     uint32_t *nz;
 };
+// Chained batches: the X bits of batch k+1's V's at batch k+2's qubits (VI_VBN of k+1), formed by
+// batch k's sign pass, the first point where batch k+1's pivot rows are final. nb = 0: none.
+struct VbnNext {
+    const uint64_t *x;
+    uint64_t pitch, ng;
+    uint32_t *vinfo;
+    const uint32_t *bctl;
+    const uint32_t *nfq;
+    uint32_t nb;
+};
 
 __global__ void __launch_bounds__(256)
 k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
               uint32_t *member, const uint8_t *__restrict__ partial,
               const uint32_t *__restrict__ vinfo, const uint32_t *__restrict__ bctl,
               int *__restrict__ err, uint32_t *__restrict__ d_pos, uint64_t *__restrict__ coin_index,
-              uint32_t *__restrict__ host_slot, uint32_t seq, NextCols nc) {
+              uint32_t *__restrict__ host_slot, uint32_t seq, NextCols nc, VbnNext vn) {
     pdl_wait();
     __shared__ uint32_t s_vs_mask, s_b0_mask, s_b1_mask, s_p[kB], s_nq[kB];
     if (host_slot && blockIdx.x == 0 && threadIdx.x == 0) { // the batch is decided: tell the host
@@ -742,6 +848,14 @@ k_batch_signs(uint64_t *__restrict__ s, uint64_t nrows, uint64_t nslices,
     const uint32_t len = bctl[BL_LEN];
     if (len == 0) return;
     const uint32_t tid = threadIdx.x;
+    if (vn.nb && blockIdx.x == 0 && tid < kB) {
+        const uint32_t lenn = vn.bctl[BL_SKIP] ? 0u : vn.bctl[BL_LEN];
+        if (lenn) {
+            const bool v = tid < lenn;
+            const uint32_t cg = v ? vn.vinfo[VI_C + tid] : 0u, L = v ? vn.vinfo[VI_L + tid] : 0u;
+            vn.vinfo[VI_VBN + tid] = vbn_lane(tid, v, cg, L, vn.x, vn.pitch, vn.ng, vn.nfq, vn.nb);
+        }
+    }
     // The batch is decided: advance the speculation position and the coin index, on every shard
     // alike (B3 drew coins idx0 .. idx0 + len - 1).
     if (blockIdx.x == 0 && tid == 0) {
@@ -871,14 +985,32 @@ FinishArgs finish_args(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d
 }
 MemberArgs member_args(DeviceTableau &t) {
     MeasureScratch &ms = t.ms;
-    return MemberArgs{ms.colbits, 2 * t.ng, t.ng, t.g0, ms.vinfo, ms.bctl, t.prof ? t.prof->d_rows : nullptr};
+    return MemberArgs{ms.colbits, 2 * t.ng, t.ng, t.g0, ms.vinfo, ms.bctl, t.prof ? t.prof->d_rows : nullptr,
+                      nullptr, 0, nullptr, 0, nullptr, nullptr};
+}
+SelectArgs select_args(DeviceTableau &t, uint32_t b, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
+    MeasureScratch &ms = t.ms;
+    SelectArgs a{};
+    a.colbits = ms.colbits;
+    a.nz = ms.nz;
+    a.n_gen = t.n_gen;
+    a.ng = t.ng;
+    a.g0 = t.g0;
+    a.b = b;
+    a.vinfo = ms.vinfo;
+    a.bctl = ms.bctl;
+    a.d_pos = d_pos;
+    a.expect = expect;
+    a.plan = d_plan;
+    a.pcount = ms.pcount; // (sharded: zeroed by batch_colbits; one GPU: by the select itself)
+    return a;
+}
+void launch_select(const SelectArgs &a, cudaStream_t st) {
+    launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, st, a);
+    count_launch();
 }
 void launch_select(DeviceTableau &t, uint32_t b, uint32_t *d_pos, uint32_t expect, const uint32_t *d_plan) {
-    MeasureScratch &ms = t.ms;
-    // (Sharded: ms.pcount was zeroed by batch_colbits; one GPU: by the select itself.)
-    launch_chain(k_pivot_select, dim3(1), dim3(kSelThreads), 0, t.stream, ms.colbits, ms.nz, t.n_gen,
-                 t.ng, t.g0, b, ms.vinfo, ms.bctl, d_pos, expect, d_plan, ms.pcount);
-    count_launch();
+    launch_select(select_args(t, b, d_pos, expect, d_plan), t.stream);
 }
 uint32_t rows_blocks(const DeviceTableau &t) { return uint32_t((t.rm_pitch + kRowWords - 1) / kRowWords); }
 } // namespace
@@ -918,7 +1050,8 @@ namespace {
 // Member pass (unless `member` is false: the fused chain ran it with the pivot rows), absorb
 // (with B3 in CTA 0 when `fin` is set), signs.
 void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin, uint32_t *host_slot = nullptr,
-                  uint32_t seq = 0, const uint32_t *next_fq = nullptr, uint32_t next_b = 0) {
+                  uint32_t seq = 0, const uint32_t *next_fq = nullptr, uint32_t next_b = 0,
+                  const SelectArgs *chain_sel = nullptr, VbnNext vn = VbnNext{}) {
     MeasureScratch &ms = t.ms;
     const uint64_t nrows = 2 * t.ng;
     configure_batch_kernels(t.device);
@@ -940,16 +1073,18 @@ void apply_passes(DeviceTableau &t, bool member, const FinishArgs *fin, uint32_t
         QSR_CUDA(cudaEventRecord(ea, t.stream));
     }
     const FinishArgs none{};
+    const SelectArgs no_sel{};
     launch_chain(k_batch_absorb, dim3(unsigned(t.num_sms)), dim3(kAThreads), kAbsorbSmem, t.stream, t.x, t.z,
                  t.rm_pitch, nrows, ms.colbits, ms.Vx, ms.Vz, ms.vstride, ms.bctl, ms.partial,
-                 absorb_stride(nrows / (uint64_t(kARows) * kAWarps)), fin ? *fin : none, fin ? 1 : 0);
+                 absorb_stride(nrows / (uint64_t(kARows) * kAWarps)), fin ? *fin : none, fin ? 1 : 0,
+                 chain_sel ? *chain_sel : no_sel, chain_sel ? 1 : 0);
     if (t.prof) {
         QSR_CUDA(cudaEventRecord(eb, t.stream));
         t.prof->ev.emplace_back(ea, eb);
     }
     launch_chain(k_batch_signs, dim3(row_blocks), dim3(256), 0, t.stream, t.s, nrows, nslices, ms.colbits,
                  ms.partial, ms.vinfo, ms.bctl, ms.err, ms.d_pos, ms.coin_index, host_slot, seq,
-                 NextCols{t.x, t.rm_pitch, t.ng, next_fq, next_fq ? next_b : 0u, ms.nz});
+                 NextCols{t.x, t.rm_pitch, t.ng, next_fq, next_fq ? next_b : 0u, ms.nz}, vn);
     count_launch(2);
 }
 } // namespace
@@ -966,6 +1101,53 @@ void batch_fused(DeviceTableau &t, const uint32_t *d_fq, const uint32_t *d_fidx,
     count_launch();
     const FinishArgs fin = finish_args(t, d_fq, d_fidx, seed);
     apply_passes(t, false, &fin, host_slot, seq, next_fq, next_b);
+}
+
+void batch_chained(DeviceTableau &t, const BatchBufs &nxt, const uint32_t *d_fq, const uint32_t *d_fidx,
+                   uint32_t b, uint64_t seed, bool standalone, uint32_t *d_pos, uint32_t expect,
+                   const uint32_t *nfq, uint32_t nb, const uint32_t *nfq2, uint32_t nb2, uint32_t *host_slot,
+                   uint32_t seq) {
+    MeasureScratch &ms = t.ms;
+    configure_batch_kernels(t.device);
+    if (standalone) { // column bits + select of this batch, and its V's bits at the next batch's qubits
+        batch_colbits(t, d_fq, b);
+        SelectArgs a = select_args(t, b, d_pos, expect, nullptr);
+        a.x = t.x;
+        a.pitch = t.rm_pitch;
+        a.nfq = nfq;
+        a.nb = nb;
+        launch_select(a, t.stream);
+    }
+    MemberArgs ma = member_args(t);
+    if (nb) {
+        ma.x = t.x;
+        ma.pitch = t.rm_pitch;
+        ma.nfq = nfq;
+        ma.nb = nb;
+        ma.colbits_next = nxt.colbits;
+        ma.nz_next = nxt.nz;
+    }
+    const uint32_t rb = rows_blocks(t), mb = uint32_t((2 * t.ng + 255) / 256);
+    launch_chain(k_rows_member, dim3(rb + mb), dim3(256), 0, t.stream, rows_args(t, d_fq), ma, rb);
+    count_launch();
+    const FinishArgs fin = finish_args(t, d_fq, d_fidx, seed);
+    SelectArgs sel{};
+    if (nb) { // the next batch's select, in the absorb's last CTA
+        sel.colbits = nxt.colbits;
+        sel.nz = nxt.nz;
+        sel.n_gen = t.n_gen;
+        sel.ng = t.ng;
+        sel.g0 = t.g0;
+        sel.b = nb;
+        sel.vinfo = nxt.vinfo;
+        sel.bctl = nxt.bctl;
+        sel.pcount = nxt.pcount;
+        sel.prev_bctl = ms.bctl;
+        sel.prev_b = b;
+    }
+    VbnNext vn{};
+    if (nb && nb2) vn = VbnNext{t.x, t.rm_pitch, t.ng, nxt.vinfo, nxt.bctl, nfq2, nb2};
+    apply_passes(t, false, &fin, host_slot, seq, nullptr, 0, nb ? &sel : nullptr, vn);
 }
 
 } // namespace qsr

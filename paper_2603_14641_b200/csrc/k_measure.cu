@@ -507,16 +507,48 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
             return !(e && e[0] == '0');
         }();
         bool cols_ready = false; // the previous batch's sign pass computed this batch's column bits
+        // Chained batches (QSR_CHAIN=0: off): batch k+1's select runs in batch k's absorb (its last
+        // CTA) on column bits batch k's membership pass derives; the two batches alternate between
+        // two buffer sets. A batch after an early stop starts standalone.
+        static const bool chain = [] {
+            const char *e = getenv("QSR_CHAIN");
+            return !(e && e[0] == '0');
+        }();
+        const BatchBufs sets[2] = {{ms.vinfo, ms.bctl, ms.colbits, ms.nz, ms.pcount},
+                                   {ms.vinfo_b, ms.bctl_b, ms.colbits_b, ms.nz_b, ms.pcount_b}};
+        auto use_set = [&](int p) {
+            ms.vinfo = sets[p].vinfo;
+            ms.bctl = sets[p].bctl;
+            ms.colbits = sets[p].colbits;
+            ms.nz = sets[p].nz;
+            ms.pcount = sets[p].pcount;
+        };
+        int par = 0;
+        bool chained = false; // this batch's select already ran in the previous batch's absorb
+        auto next_size = [&](size_t at) {
+            return at < fq.size() ? uint32_t(std::min<size_t>(kMaxBatch, fq.size() - at)) : 0u;
+        };
         while (pos < fq.size()) {
             while (qsize < 2 && spec < fq.size()) {
                 const uint32_t b = uint32_t(std::min<size_t>(kMaxBatch, fq.size() - spec));
-                if (!cols_ready) batch_colbits(t, ms.fq + spec, b);
                 const size_t nxt = spec + b;
-                const uint32_t nb = fuse_cols && nxt < fq.size() ? uint32_t(std::min<size_t>(kMaxBatch, fq.size() - nxt)) : 0;
                 seqs[slot] = next_batch_seq(); // process-wide: pinned slots are recycled across tableaux
-                batch_fused(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec),
-                            poll ? ms.h_bctl + 8 * slot : nullptr, seqs[slot], nb ? ms.fq + nxt : nullptr, nb);
-                cols_ready = nb != 0;
+                uint32_t *hs = poll ? ms.h_bctl + 8 * slot : nullptr;
+                if (chain) {
+                    const uint32_t nb = next_size(nxt), nb2 = nb ? next_size(nxt + nb) : 0u;
+                    use_set(par);
+                    batch_chained(t, sets[par ^ 1], ms.fq + spec, ms.fidx + spec, b, seed, !chained, ms.d_pos,
+                                  uint32_t(spec), nb ? ms.fq + nxt : nullptr, nb, nb2 ? ms.fq + nxt + nb : nullptr,
+                                  nb2, hs, seqs[slot]);
+                    chained = nb != 0;
+                    par ^= 1;
+                } else {
+                    if (!cols_ready) batch_colbits(t, ms.fq + spec, b);
+                    const uint32_t nb = fuse_cols ? next_size(nxt) : 0u;
+                    batch_fused(t, ms.fq + spec, ms.fidx + spec, b, seed, ms.d_pos, uint32_t(spec), hs, seqs[slot],
+                                nb ? ms.fq + nxt : nullptr, nb);
+                    cols_ready = nb != 0;
+                }
                 if (!poll) {
                     QSR_CUDA(cudaMemcpyAsync(ms.h_bctl + 8 * slot, ms.bctl, 16, cudaMemcpyDeviceToHost, t.stream));
                     QSR_CUDA(cudaEventRecord(ms.bev[slot], t.stream));
@@ -543,8 +575,10 @@ void measure_window_device(DeviceTableau &t, uint64_t m, uint64_t seed,
                 set_device_u32(ms.d_pos, uint32_t(pos), t.stream);
                 spec = pos;
                 cols_ready = false; // the drained batch's successor columns were for another position
+                chained = false;
             }
         }
+        use_set(0); // (the other paths and the sharded engine use the first set)
     } else {
         for (uint64_t i = 0; i < m; ++i) {
             if (!flags_host[i]) continue;

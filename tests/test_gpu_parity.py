@@ -300,14 +300,15 @@ def test_mixed_bell_and_random(q, oracle):
 
 @pytest.mark.parametrize("env", [{"QSR_MEASURE_BATCH": "0"}, {"QSR_FUSE": "0"}, {"QSR_STREAM": "0"},
                                  {"QSR_GRAPHS": "0"}, {"QSR_PDL": "0"}, {"QSR_HOSTPOLL": "0"},
-                                 {"QSR_FUSE_COLS": "0"}])
+                                 {"QSR_FUSE_COLS": "0", "QSR_CHAIN": "0"}, {"QSR_CHAIN": "0"}])
 def test_alternate_collapse_paths_match(q, env):
     """Every alternate path must agree with the default and the oracle: QSR_MEASURE_BATCH=0 (one
     collapse per pass, the path of uploaded tableaux), QSR_FUSE=0 (no gate fusion), QSR_STREAM=0
     (schedule first, then run), QSR_GRAPHS=0 (no graph replay), QSR_PDL=0 (plain launches instead
     of programmatic dependent launches), QSR_HOSTPOLL=0 (batch control words read back by a copy
-    + event per batch instead of the sign pass's pinned-memory write), QSR_FUSE_COLS=0 (a column-bit
-    launch per batch instead of the previous sign pass computing them)."""
+    + event per batch instead of the sign pass's pinned-memory write), QSR_CHAIN=0 (every batch's
+    select in its own launch after its column bits, which the previous sign pass computes) and with
+    QSR_FUSE_COLS=0 (a column-bit launch per batch)."""
     import subprocess
     import sys
     code = (
