@@ -286,6 +286,19 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
             } else {
                 const cudaStream_t fs = frames->own ? frames->own : t.stream;
                 cudaEvent_t fa = nullptr, fb = nullptr;
+                const bool delayed = frames->own != nullptr;
+                if (delayed) {
+                    // The reference shot's windows first, alone on the GPU; the frames' windows of
+                    // this run follow on their own stream (beside the shot's next measurement
+                    // window, which only needs these windows' tableau).
+                    for (uint64_t v = w; v < w1; ++v)
+                        launch_gate_window(t, ds.d_gates + ds.offsets[v], ds.offsets[v + 1] - ds.offsets[v]);
+                    cudaEvent_t done;
+                    QSR_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                    QSR_CUDA(cudaEventRecord(done, t.stream));
+                    QSR_CUDA(cudaStreamWaitEvent(fs, done, 0));
+                    QSR_CUDA(cudaEventDestroy(done));
+                }
                 if (frames->own) {
                     QSR_CUDA(cudaEventCreate(&fa));
                     QSR_CUDA(cudaEventCreate(&fb));
@@ -294,7 +307,7 @@ void run_device(DeviceTableau &t, const DeviceSchedule &ds, uint64_t seed,
                 for (uint64_t v = w; v < w1; ++v) {
                     const uint64_t *g = ds.d_gates + ds.offsets[v];
                     const uint64_t cnt = ds.offsets[v + 1] - ds.offsets[v];
-                    launch_gate_window(t, g, cnt);
+                    if (!delayed) launch_gate_window(t, g, cnt);
                     frames->unitary(g, cnt, fs);
                     if (v < ds.wwords.size()) {
                         rt.gate_bytes += (8.0 * ds.wwords[v] + 16.0) * 2.0 * double(t.kg);
