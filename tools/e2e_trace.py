@@ -1,7 +1,7 @@
 """Phase trace of the end-to-end C-ABI call at c5 (QSR_TRACE=1): run_single_shot with host
 buffers + final tableau download into pinned memory.
 
-    QSR_TRACE=1 python tools/e2e_trace.py [n] [depth]
+    QSR_TRACE=1 python tools/e2e_trace.py [n] [depth] [p] [runs]
 """
 import ctypes as C
 import sys
@@ -16,7 +16,9 @@ from paper_2603_14641_b200 import quasar as q  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 180000
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 1000
-c = q.generate_random(n, depth, 42, 0.01)
+p = float(sys.argv[3]) if len(sys.argv) > 3 else 0.01
+runs = int(sys.argv[4]) if len(sys.argv) > 4 else 2
+c = q.generate_random(n, depth, 42, p)
 k = (n + 63) // 64
 plane = 64 * k * 2 * k
 px, pz = C.c_void_p(), C.c_void_p()
@@ -24,7 +26,7 @@ _lib.check(_lib.lib.qsr_host_alloc(plane * 8, C.byref(px)))
 _lib.check(_lib.lib.qsr_host_alloc(plane * 8, C.byref(pz)))
 ps = np.empty(2 * k, dtype=np.uint64)
 rec = np.zeros(max(c.measure_count(), 1), dtype=_lib.ENTRY_DTYPE)
-for i in range(2):
+for i in range(runs):
     t0 = time.perf_counter()
     h = C.c_void_p()
     rep = _lib.Report_t()
