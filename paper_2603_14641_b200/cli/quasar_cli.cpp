@@ -12,11 +12,13 @@
 // error), 3 resource error (host or device memory) — tools/quasar.cpp:40-43, 386-395. Usage
 // errors use CLI11's codes (104 conversion, 105 validation, 106 required, 109 extras).
 //
-// `verify` cannot call the reference's scalar CHP / state-vector oracles (they are test
-// infrastructure here), so its differential leg compares the engine's two independent run paths
-// (the fused, streamed whole-circuit run against window-by-window calls on a device tableau),
-// checks the final tableau is a stabilizer group (device kernel), and keeps the reference's
-// statistical leg with a small state-vector checker of its own.
+// `verify` does not link the reference's scalar CHP / state-vector oracles (they are test
+// infrastructure here). Its differential leg checks the fused, streamed whole-circuit run
+// against (a) window-by-window calls on a device tableau and (b) an independent scalar cell
+// tableau of its own (the role of oracle::run_scalar, tools/quasar.cpp:165-236), record and
+// final tableau bit for bit, and checks the final tableau is a stabilizer group (device
+// kernel); the statistical leg keeps the reference's chi-square test with a small state-vector
+// checker of its own.
 #include <algorithm>
 #include <cerrno>
 #include <cmath>
@@ -564,6 +566,192 @@ struct VerifyOpts {
     uint64_t seed = 1;
 };
 
+// Independent scalar check for the differential leg (the role oracle::run_scalar plays in
+// tools/quasar.cpp:165-236): one byte per tableau cell, every gate a loop over the 2n rows and
+// every collapse the strictly ordered row products of the CHP algorithm, no bit packing, no
+// device code. Semantics it must agree with: gate rules gates.hpp:35-115, products and their
+// mod-4 phase tableau.hpp:337-350, the collapse measure.hpp:381-442 (pivot = lowest stabilizer
+// with X at q; later pivots absorb it; other anticommuting destabilizers absorb it; D_c <- S_c,
+// S_c <- Z_q with the coin as sign), deterministic outcomes as the ordered product of the
+// stabilizers whose destabilizer has X at q, and the window order of simulator.hpp:46-76
+// (probabilistic at window start -> collapse in order; the rest resolved after the collapses).
+class CellTableau {
+  public:
+    explicit CellTableau(uint32_t n) : n_(n), x_(size_t(2) * n * n, 0), z_(size_t(2) * n * n, 0), s_(2 * n, 0) {
+        for (uint32_t i = 0; i < n; ++i) {
+            x(i, i) = 1;     // destabilizer i = X_i
+            z(n + i, i) = 1; // stabilizer i = Z_i
+        }
+    }
+    uint8_t &x(size_t g, size_t q) { return x_[g * n_ + q]; }
+    uint8_t &z(size_t g, size_t q) { return z_[g * n_ + q]; }
+    uint8_t x(size_t g, size_t q) const { return x_[g * n_ + q]; }
+    uint8_t z(size_t g, size_t q) const { return z_[g * n_ + q]; }
+    uint8_t sign(size_t g) const { return s_[g]; }
+
+    void gate(const qsr_gate &g) {
+        for (size_t r = 0; r < 2 * size_t(n_); ++r) {
+            uint8_t &a = x(r, g.q0), &b = z(r, g.q0);
+            uint8_t dummy_x = 0, dummy_z = 0;
+            const bool two = g.kind >= QSR_CX;
+            uint8_t &c = two ? x(r, g.q1) : dummy_x, &d = two ? z(r, g.q1) : dummy_z;
+            s_[r] ^= conjugate(g.kind, a, b, c, d);
+        }
+    }
+
+    // Single-cell Clifford conjugation; returns the sign flip.
+    static uint8_t conjugate(uint8_t kind, uint8_t &x0, uint8_t &z0, uint8_t &x1, uint8_t &z1) {
+        uint8_t f = 0;
+        switch (kind) {
+        case QSR_X: f = z0; break;
+        case QSR_Y: f = x0 ^ z0; break;
+        case QSR_Z: f = x0; break;
+        case QSR_H: f = x0 & z0; std::swap(x0, z0); break;
+        case QSR_S: f = x0 & z0; z0 ^= x0; break;
+        case QSR_SDG: f = x0 & (z0 ^ 1); z0 ^= x0; break;
+        case QSR_CX: f = x0 & z1 & ((x1 ^ z0) ^ 1); x1 ^= x0; z0 ^= z1; break;
+        case QSR_CZ: f = x0 & x1 & (z0 ^ z1); z1 ^= x0; z0 ^= x1; break;
+        case QSR_CY: // SDG(t), CX, S(t)
+            f = conjugate(QSR_SDG, x1, z1, x1, z1);
+            f ^= conjugate(QSR_CX, x0, z0, x1, z1);
+            f ^= conjugate(QSR_S, x1, z1, x1, z1);
+            break;
+        case QSR_SWAP: std::swap(x0, x1); std::swap(z0, z1); break;
+        case QSR_ISWAP: // SWAP, CZ, S(c), S(t)
+            std::swap(x0, x1);
+            std::swap(z0, z1);
+            f = conjugate(QSR_CZ, x0, z0, x1, z1);
+            f ^= conjugate(QSR_S, x0, z0, x0, z0);
+            f ^= conjugate(QSR_S, x1, z1, x1, z1);
+            break;
+        default: throw std::runtime_error("verify: unknown gate kind");
+        }
+        return f & 1;
+    }
+
+    // i-exponent (mod 4) of P(xc,zc) * P(xt,zt) for one qubit: +1 / -1 / 0.
+    static int phase(uint8_t xc, uint8_t zc, uint8_t xt, uint8_t zt) {
+        if (xc && zc) return (zt && !xt) ? 1 : (xt && !zt) ? -1 : 0;          // Y * (Z | X)
+        if (xc) return (xt && zt) ? 1 : (zt && !xt) ? -1 : 0;                 // X * (Y | Z)
+        if (zc) return (xt && !zt) ? 1 : (xt && zt) ? -1 : 0;                 // Z * (X | Y)
+        return 0;
+    }
+
+    // row t <- row c * row t (bits XOR, sign with the product's phase).
+    void mult(size_t t, size_t c) {
+        int e = 0;
+        for (size_t q = 0; q < n_; ++q) e += phase(x(c, q), z(c, q), x(t, q), z(t, q));
+        if (e & 1) throw std::runtime_error("verify: product of anticommuting rows");
+        for (size_t q = 0; q < n_; ++q) {
+            x(t, q) ^= x(c, q);
+            z(t, q) ^= z(c, q);
+        }
+        s_[t] ^= s_[c] ^ uint8_t((e & 3) == 2);
+    }
+
+    int lowest_pivot(uint32_t q) const {
+        for (uint32_t t = 0; t < n_; ++t)
+            if (x(n_ + t, q)) return int(t);
+        return -1;
+    }
+
+    bool deterministic(uint32_t q) const {
+        std::vector<uint8_t> ax(n_, 0), az(n_, 0);
+        int e = 0;
+        for (uint32_t g = 0; g < n_; ++g) {
+            if (!x(g, q)) continue;
+            e += 2 * s_[n_ + g];
+            for (uint32_t p = 0; p < n_; ++p) {
+                e += phase(ax[p], az[p], x(n_ + g, p), z(n_ + g, p));
+                ax[p] ^= x(n_ + g, p);
+                az[p] ^= z(n_ + g, p);
+            }
+        }
+        if (e & 1) throw std::runtime_error("verify: imaginary deterministic phase");
+        return ((e >> 1) & 1) != 0;
+    }
+
+    // Collapse of a probabilistic Z_q; the coin is the next word of the measurement stream.
+    bool collapse(uint32_t q, uint64_t coin) {
+        const int c = lowest_pivot(q);
+        for (uint32_t t = uint32_t(c) + 1; t < n_; ++t)
+            if (x(n_ + t, q)) mult(n_ + t, n_ + c); // (D_c absorbing D_t is overwritten below)
+        for (uint32_t g = 0; g < n_; ++g)
+            if (g != uint32_t(c) && x(g, q)) mult(g, n_ + c);
+        for (uint32_t p = 0; p < n_; ++p) {
+            x(c, p) = x(n_ + c, p);
+            z(c, p) = z(n_ + c, p);
+            x(n_ + c, p) = 0;
+            z(n_ + c, p) = p == q;
+        }
+        s_[c] = s_[n_ + c];
+        s_[n_ + c] = uint8_t(coin & 1);
+        return s_[n_ + c] != 0;
+    }
+
+  private:
+    uint32_t n_;
+    std::vector<uint8_t> x_, z_, s_;
+};
+
+// Scalar run in the schedule's window order; coins from Philox stream 0 (rng.hpp:98).
+std::vector<qsr_record_entry> scalar_run(uint32_t n, const qsr_schedule *s, uint64_t seed, CellTableau &t) {
+    uint64_t nw = 0, ng = 0;
+    int mode = 0;
+    check(qsr_schedule_info(s, &nw, &ng, &mode));
+    const qsr_gate *g = qsr_schedule_gates(s);
+    const uint64_t *off = qsr_schedule_offsets(s);
+    const uint8_t *ism = qsr_schedule_is_measurement(s);
+    std::vector<qsr_record_entry> rec;
+    uint64_t coin = 0;
+    (void)n;
+    for (uint64_t w = 0; w < nw; ++w) {
+        const uint64_t b = off[w], e = off[w + 1];
+        if (!ism[w]) {
+            for (uint64_t i = b; i < e; ++i) t.gate(g[i]);
+            continue;
+        }
+        std::vector<qsr_record_entry> out(e - b);
+        std::vector<char> prob(e - b);
+        for (uint64_t m = b; m < e; ++m) prob[m - b] = t.lowest_pivot(g[m].q0) >= 0;
+        for (uint64_t m = b; m < e; ++m) {
+            const uint32_t q = g[m].q0;
+            out[m - b] = {q, 0, 0};
+            if (!prob[m - b]) continue;
+            if (t.lowest_pivot(q) < 0) { // decided by an earlier collapse of this window
+                out[m - b] = {q, uint8_t(t.deterministic(q)), 1};
+                continue;
+            }
+            out[m - b] = {q, uint8_t(t.collapse(q, qsr_philox_word(seed, 0, 0, coin++))), 0};
+        }
+        for (uint64_t m = b; m < e; ++m)
+            if (!prob[m - b]) out[m - b] = {g[m].q0, uint8_t(t.deterministic(g[m].q0)), 1};
+        rec.insert(rec.end(), out.begin(), out.end());
+    }
+    return rec;
+}
+
+// Device tableau (reference layout, downloaded) against the scalar cells, bit for bit.
+bool same_as_cells(const qsr_tableau *d, const CellTableau &c, uint32_t n) {
+    uint64_t nn = 0, k = 0, npad = 0;
+    int layout = 0;
+    check(qsr_tableau_info(d, &nn, &k, &npad, &layout));
+    std::vector<uint64_t> x(npad * 2 * k), z(npad * 2 * k), s(2 * k);
+    check(qsr_tableau_download(d, x.data(), z.data(), s.data()));
+    for (uint64_t g = 0; g < 2 * uint64_t(n); ++g) {
+        const uint64_t col = g < n ? g : npad + (g - n); // tableau.hpp:90 rm_col
+        const uint64_t sidx = g < n ? g : k * 64 + (g - n);
+        if (((s[sidx / 64] >> (sidx % 64)) & 1) != c.sign(g)) return false;
+        for (uint64_t q = 0; q < n; ++q) {
+            // ColumnMajor: word (q, col / 64); RowMajor: word (q / 64, col) with pitch 2 n_pad.
+            const uint64_t wi = layout == QSR_COLUMN_MAJOR ? q * 2 * k + col / 64 : (q / 64) * 2 * npad + col;
+            const unsigned bit = unsigned(layout == QSR_COLUMN_MAJOR ? col % 64 : q % 64);
+            if (((x[wi] >> bit) & 1) != c.x(g, q) || ((z[wi] >> bit) & 1) != c.z(g, q)) return false;
+        }
+    }
+    return true;
+}
+
 // Window-by-window run on a device tableau (apply_window / measure_window per window: no
 // fusion, no streaming, no batching across windows).
 std::vector<qsr_record_entry> stepwise(const qsr_circuit *c, const qsr_schedule *s, uint64_t seed, int device,
@@ -635,11 +823,18 @@ int cmd_verify(const VerifyOpts &opt, int device) {
         TableauH whole, step;
         Shot a = run_shot(c.p, nullptr, run_seed, device, &whole);
         std::vector<qsr_record_entry> b = stepwise(c.p, s.p, run_seed, device, step);
-        bool same = a.record.size() == b.size();
-        for (size_t i = 0; same && i < b.size(); ++i)
-            same = a.record[i].qubit == b[i].qubit && a.record[i].outcome == b[i].outcome &&
-                   a.record[i].deterministic == b[i].deterministic;
-        if (!same || !same_tableau(whole.p, step.p)) fail_line("differential");
+        auto same_record = [](const std::vector<qsr_record_entry> &u, const std::vector<qsr_record_entry> &v) {
+            bool eq = u.size() == v.size();
+            for (size_t i = 0; eq && i < v.size(); ++i)
+                eq = u[i].qubit == v[i].qubit && u[i].outcome == v[i].outcome &&
+                     u[i].deterministic == v[i].deterministic;
+            return eq;
+        };
+        if (!same_record(a.record, b) || !same_tableau(whole.p, step.p)) fail_line("differential");
+        // Independent leg: the scalar cell tableau on the same schedule and coins.
+        CellTableau cells(n);
+        const std::vector<qsr_record_entry> sc = scalar_run(n, s.p, run_seed, cells);
+        if (!same_record(a.record, sc) || !same_as_cells(whole.p, cells, n)) fail_line("differential-scalar");
         const std::string group = text_of([&](char *buf, uint64_t cap, uint64_t *len) {
             return qsr_tableau_check_validity(whole.p, buf, cap, len);
         });
