@@ -21,7 +21,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", str(PKG.parent / "include")]
 SOURCES = ["host_circuit.cpp", "capi.cpp", "engine.cpp", "k_gates.cu", "k_transpose.cu", "k_measure.cu", "k_batch.cu",
            "k_frames.cu", "exchange.cu", "shard.cpp", "stream.cpp", "fuse.cpp", "qasm.cpp", "k_validity.cu"]
-HEADERS = ["host.hpp", "device.hpp", "common.cuh", "abi.hpp", "engine.hpp", "exchange.hpp", "fuse.hpp"]
+HEADERS = ["host.hpp", "device.hpp", "common.cuh", "abi.hpp", "engine.hpp", "exchange.hpp", "fuse.hpp", "stream_plan.hpp"]
 
 
 def _newest_header() -> float:

@@ -27,6 +27,7 @@
 
 #include "engine.hpp"
 #include "fuse.hpp"
+#include "stream_plan.hpp"
 
 namespace qsr {
 
@@ -64,27 +65,6 @@ struct PinnedRing {
 };
 
 } // namespace
-
-// Buckets of packed gates per window key, in pages that never move: the planner appends to keys
-// at or above the published limit while the emitter reads (and recycles) keys below it.
-class BucketDir {
-  public:
-    explicit BucketDir(uint64_t max_keys) : pages_((max_keys + kPage - 1) / kPage) {}
-    std::vector<uint64_t> &operator[](uint64_t key) {
-        auto &pg = pages_[key / kPage];
-        if (!pg) pg = std::make_unique<Page>();
-        return (*pg)[key % kPage];
-    }
-    std::vector<uint64_t> *find(uint64_t key) {
-        auto &pg = pages_[key / kPage];
-        return pg ? &(*pg)[key % kPage] : nullptr;
-    }
-
-  private:
-    static constexpr uint64_t kPage = 1024;
-    using Page = std::array<std::vector<uint64_t>, kPage>;
-    std::vector<std::unique_ptr<Page>> pages_;
-};
 
 void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
                            qsr_record_entry *d_record, RunTimes &rt, StreamCounts &counts,
@@ -299,7 +279,6 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
         }
         cv.notify_one();
     };
-    uint64_t max_key = 0;
     auto halt = [&] {
         {
             std::lock_guard<std::mutex> lk(mu);
@@ -308,49 +287,28 @@ void run_circuit_streaming(DeviceTableau &t, const Circuit &c, uint64_t seed,
         cv.notify_one();
         emit_thread.join();
     };
+    ChunkPlanner<decltype(fresh_bucket)> planner(n, buckets, fresh_bucket);
     try {
-        std::vector<uint32_t> wire(n, 0); // round << 1 | last gate was a MEASURE
         const qsr_gate *gates = c.gates.data();
         // Small chunks first (the device starts after ~a layer), then kPlanChunk.
         uint64_t chunk = uint64_t(1) << 17;
         for (uint64_t i0 = 0; i0 < G; i0 += chunk, chunk = std::min(chunk * 2, kPlanChunk)) {
             const uint64_t i1 = std::min(G, i0 + chunk);
             const auto tp = clk::now();
-            for (uint64_t i = i0; i < i1; ++i) {
-                const qsr_gate g = gates[i];
-                const uint32_t kind = g.kind;
-                if (kind > QSR_MEASURE) fail(QSR_INVALID_ARGUMENT, "unknown gate kind");
-                const bool two = kind >= QSR_CX && kind <= QSR_ISWAP;
-                const uint32_t q0 = g.q0, q1 = two ? g.q1 : g.q0;
-                if (q0 >= n || q1 >= n) fail(QSR_OUT_OF_RANGE, "gate operand out of range");
-                if (two && q0 == q1) fail(QSR_INVALID_ARGUMENT, "two-qubit gate with equal operands");
-                const uint32_t w0 = wire[q0], w1 = wire[q1];
-                const uint32_t r0 = w0 >> 1, r1 = w1 >> 1;
-                const uint32_t meas = kind == QSR_MEASURE;
-                const uint32_t r = meas ? (r0 > 1 ? r0 : 1) : 1 + (r0 > r1 ? r0 : r1);
-                if (meas & w0 & 1u) fail(QSR_INVALID_ARGUMENT, "measure_window: qubit measured twice");
-                wire[q0] = (r << 1) | meas;
-                wire[q1] = (r << 1) | meas;
-                const uint64_t key = 2 * uint64_t(r) + meas;
-                max_key = std::max(max_key, key);
-                std::vector<uint64_t> &bk = buckets[key];
-                if (bk.capacity() == 0) fresh_bucket(bk);
-                bk.push_back(pack_gate(g));
-            }
+            planner.plan(gates, i0, i1);
             t_plan += since(tp);
             {
                 std::lock_guard<std::mutex> lk(mu);
                 if (stop) break; // the emitter failed
             }
             if (i1 == G) break;
-            uint32_t rmin = 0xFFFFFFFFu;
-            for (uint32_t q = 0; q < n; ++q) rmin = std::min(rmin, wire[q] >> 1);
-            publish(2 * uint64_t(rmin) + 1, false);
+            publish(2 * uint64_t(planner.min_round()) + 1, false);
         }
     } catch (...) {
         halt();
         throw;
     }
+    const uint64_t max_key = planner.max_key();
     publish(max_key + 1, true);
     emit_thread.join();
     if (emit_error) std::rethrow_exception(emit_error);
