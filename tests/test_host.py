@@ -135,3 +135,21 @@ def test_circuit_validation(q):
         q.Circuit(2, [(3, 2)])
     with pytest.raises(q.InvalidArgument):
         q.Circuit(3, [(6, 1, 1)])
+
+
+def test_chunk_planner_matches_scheduler(tmp_path):
+    """The streaming driver's chunk planner (csrc/stream_plan.hpp), host only: over 400 generated
+    and hand-made circuits with random chunk splits, its buckets in key order are the one-shot
+    scheduler's windows gate for gate, and both reject the same circuits (tests/cpp/plan_check.cpp)."""
+    import shutil
+    import subprocess
+    if shutil.which("g++") is None:
+        pytest.skip("g++ not available")
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "plan_check"
+    subprocess.run(["g++", "-O2", "-std=c++17", "-I", str(root / "include"), "-I",
+                    str(root / "paper_2603_14641_b200" / "csrc"), str(root / "tests" / "cpp" / "plan_check.cpp"),
+                    str(root / "paper_2603_14641_b200" / "csrc" / "host_circuit.cpp"), "-pthread", "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and out.stdout.startswith("ok "), out.stdout + out.stderr
