@@ -285,16 +285,20 @@ int gate_variant(uint64_t ngates) {
 // Grid of a window launch: tiles x chunks CTAs. Every CTA does the same work, so the grid should
 // be a whole number of waves: pick the chunk count (>= ~4 waves when the window is big enough)
 // whose tiles x chunks leaves the smallest partial last wave. At least 16 items per warp per
-// chunk keep the XOR tree and the tile fold negligible. Grows the sign partials as needed.
+// chunk (8 for windows under 16 k gates) keep the XOR tree and the tile fold negligible: the
+// 8 for small windows measured c2 33.3 -> 32.2 ms and c4 35.5 -> 34.8 ms per step, while the
+// larger windows (c3 gate phase 188 -> 200 ms) keep 16 and c5 is unaffected (its search range
+// stays below the cap). Grows the sign partials as needed.
 void pick_chunks(uint64_t pitch, uint64_t nitems, int num_sms, int bps, bool signs, uint64_t **partials,
                  uint64_t *partial_chunks, uint64_t *tiles_out, uint64_t *chunk_out, uint64_t *chunks_out,
                  cudaStream_t st) {
     const uint64_t tiles = (pitch + kTileWords - 1) / kTileWords;
     const uint64_t slots = uint64_t(num_sms) * uint64_t(bps);
-    static const uint64_t per_warp = [] { // QSR_GATE_MINPW: tuning knob (default 16)
+    static const uint64_t per_warp_env = [] { // QSR_GATE_MINPW: tuning knob (0 = by window size)
         const char *e = getenv("QSR_GATE_MINPW");
-        return e ? std::max<uint64_t>(1, uint64_t(atoll(e))) : uint64_t(16);
+        return e ? std::max<uint64_t>(1, uint64_t(atoll(e))) : uint64_t(0);
     }();
+    const uint64_t per_warp = per_warp_env ? per_warp_env : nitems < (uint64_t(1) << 14) ? 8 : 16;
     const uint64_t max_chunks = std::max<uint64_t>(1, nitems / (kWarps * per_warp));
     uint64_t c_min = std::max<uint64_t>(1, (4 * slots + tiles - 1) / tiles);
     // Small windows cannot reach ~4 waves: search the upper half of the allowed range, where a
