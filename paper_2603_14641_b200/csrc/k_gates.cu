@@ -270,16 +270,20 @@ k_gate_window(uint64_t *__restrict__ x, uint64_t *__restrict__ z, uint64_t pitch
 // 4 = <4,2>.
 // QSR_GATE_VARIANT selects one for tuning runs; the default is the measured best
 // (profiles/r01_gate_tune.log: <2,3> 6.37 TB/s at c5, <1,4> 6.31, <2,4> 6.07 with spills).
-// Default: <1,4> for windows of >= 16k gates (fused c5 windows, ~45k gates: 216.7 vs 226.2 ms per
-// 100 windows at 180k qubits,
-// no spills at 64 registers), <2,3> for small ones (20k qubits: 10.5 vs 11.1 ms per 300).
+// Default: <1,4> (fused c5 windows, ~45k gates: 216.7 vs 226.2 ms per 100 windows at 180k qubits,
+// no spills at 64 registers; round 1 kept <2,3> for windows under 16k gates, 20k qubits: 10.5 vs
+// 11.1 ms per 300, which no longer holds — see gate_variant).
 int gate_variant(uint64_t ngates) {
     static int v = [] {
         const char *e = getenv("QSR_GATE_VARIANT");
         return e ? atoi(e) : -1;
     }();
     if (v >= 0) return v;
-    return ngates >= (uint64_t(1) << 14) ? 1 : 0;
+    // <1,4> for every window since small windows are chunked at >= 8 gates per warp (pick_chunks):
+    // same box, interleaved, c2 32.1 -> 31.1 ms and c4 34.6 -> 32.7 ms against <2,3> below 16 k
+    // gates (round 1's choice for them, measured before that chunking and the PDL launches).
+    (void)ngates;
+    return 1;
 }
 
 // Grid of a window launch: tiles x chunks CTAs. Every CTA does the same work, so the grid should
